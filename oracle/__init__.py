@@ -1,0 +1,262 @@
+"""oracle — TEST INFRASTRUCTURE ONLY.
+
+Plain CPU oracle for the custom-intersector hot path of arXiv 1912.12786
+(oracle S: brute force, oracle.c; oracle BVH + contract walker C, walker.c).
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  The
+product (``paper_1912_12786_b200``) never imports it and it never imports
+the product; the two share no code.  See oracle/oracle.h for citations.
+
+Parity status (DESIGN.md §"Oracle pins"): every function here is pinned by
+``tests/test_oracle_pins.py`` (closed forms, brute force, invariants); none
+is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+CLOSEST, ANY = 0, 1
+NONE, DEFAULT, ALPHA_TEX, ALPHA_PROC, COUNT = 0, 1, 2, 3, 4
+X1, X2, X3, X4 = 1, 2, 4, 8
+
+HIT_DTYPE = np.dtype([("t", "<f4"), ("u", "<f4"), ("v", "<f4"), ("prim", "<u4")])
+COUNT_DTYPE = np.dtype([("boxes", "<u4"), ("tris", "<u4"), ("alpha", "<u4")])
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (no FMA contraction, IEEE semantics)."""
+    srcs = [os.path.join(_HERE, f) for f in ("oracle.c", "walker.c")]
+    hdr = os.path.join(_HERE, "oracle.h")
+    if not force and os.path.exists(LIB_PATH):
+        newest = max(os.path.getmtime(p) for p in srcs + [hdr])
+        if os.path.getmtime(LIB_PATH) >= newest:
+            return LIB_PATH
+    cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off", "-fno-fast-math",
+           "-fno-strict-aliasing", "-pthread", "-D_GNU_SOURCE", "-Wall", "-Wno-unused-function",
+           "-o", LIB_PATH + ".tmp"] + srcs + ["-lm"]
+    subprocess.check_call(cmd)
+    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    return LIB_PATH
+
+
+class _Scene(C.Structure):
+    _fields_ = [("num_tris", C.c_uint32), ("vertices", C.c_void_p), ("geom_ids", C.c_void_p),
+                ("texcoords", C.c_void_p), ("num_geoms", C.c_uint32),
+                ("geom_texture", C.c_void_p), ("num_textures", C.c_uint32),
+                ("tex_w", C.c_void_p), ("tex_h", C.c_void_p), ("tex_rgba", C.c_void_p)]
+
+
+class _Hit(C.Structure):
+    _fields_ = [("t", C.c_float), ("u", C.c_float), ("v", C.c_float), ("prim", C.c_uint32)]
+
+
+class _Bvh(C.Structure):
+    _fields_ = [("root_ref", C.c_uint32), ("root_lo", C.c_float * 3), ("root_hi", C.c_float * 3),
+                ("num_nodes", C.c_uint32), ("num_tris", C.c_uint32), ("num_textures", C.c_uint32),
+                ("nodes", C.c_void_p), ("tris", C.c_void_p), ("sides", C.c_void_p),
+                ("texdescs", C.c_void_p), ("texels", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = C.CDLL(LIB_PATH)
+        L.oracle_trace.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_uint64, C.c_int, C.c_int,
+                                   C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_int]
+        L.oracle_eval_pair.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_uint32, C.c_int,
+                                       C.c_float, C.c_uint32, C.POINTER(_Hit)]
+        L.oracle_mt.argtypes = [C.c_void_p] * 4 + [C.c_float] + [C.POINTER(C.c_float)] * 3
+        L.oracle_tex_alpha.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_float, C.c_float]
+        L.oracle_tex_alpha.restype = C.c_float
+        L.oracle_lerp2.argtypes = [C.c_void_p] * 3 + [C.c_float, C.c_float, C.c_void_p]
+        L.oracle_build_bvh.argtypes = [C.POINTER(_Scene), C.c_uint32, C.POINTER(_Bvh)]
+        L.oracle_bvh_free.argtypes = [C.POINTER(_Bvh)]
+        L.walker_trace.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_uint64, C.c_int, C.c_int,
+                                   C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_int]
+        L.walker_slab.argtypes = [C.c_void_p] * 3 + [C.c_float, C.POINTER(C.c_float),
+                                                       C.POINTER(C.c_float)]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def default_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+class OracleScene:
+    """or_scene view over a workloads.Scene (keeps the numpy arrays alive)."""
+
+    def __init__(self, scene):
+        self.vertices = np.ascontiguousarray(scene.vertices, dtype=np.float32)
+        self.geom_ids = np.ascontiguousarray(scene.geom_ids, dtype=np.uint32)
+        self.texcoords = np.ascontiguousarray(scene.texcoords, dtype=np.float32)
+        self.geom_texture = np.ascontiguousarray(scene.geom_texture, dtype=np.uint32)
+        texs = list(scene.textures) if scene.textures else [np.full((1, 1, 4), 255, np.uint8)]
+        self.textures = [np.ascontiguousarray(t, dtype=np.uint8) for t in texs]
+        self.tex_w = np.array([t.shape[1] for t in self.textures], dtype=np.uint32)
+        self.tex_h = np.array([t.shape[0] for t in self.textures], dtype=np.uint32)
+        self._ptrs = (C.c_void_p * len(self.textures))(*[t.ctypes.data for t in self.textures])
+        self.c = _Scene(self.vertices.shape[0], _ptr(self.vertices), _ptr(self.geom_ids),
+                        _ptr(self.texcoords), self.geom_texture.shape[0], _ptr(self.geom_texture),
+                        len(self.textures), _ptr(self.tex_w), _ptr(self.tex_h),
+                        C.cast(self._ptrs, C.c_void_p))
+
+
+def _as_scene(scene):
+    return scene if isinstance(scene, OracleScene) else OracleScene(scene)
+
+
+def _rays(rays):
+    data = rays.data if hasattr(rays, "data") and not isinstance(rays, np.ndarray) else rays
+    return np.ascontiguousarray(data, dtype=np.float32).reshape(-1, 8)
+
+
+def trace(scene, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,
+          flags=False, ties=False, nthreads=None):
+    """Brute-force oracle S.  Returns hits (HIT_DTYPE) [, flags uint32] [, ntie uint32]."""
+    sc = _as_scene(scene)
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty(n, dtype=HIT_DTYPE)
+    fl = np.zeros(n, dtype=np.uint32) if flags else None
+    nt = np.zeros(n, dtype=np.uint32) if ties else None
+    rc = lib().oracle_trace(C.byref(sc.c), _ptr(r), n, query, isect, alpha_threshold,
+                            checker_freq, _ptr(hits), _ptr(fl), _ptr(nt),
+                            nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"oracle_trace failed ({rc})")
+    out = [hits]
+    if flags:
+        out.append(fl)
+    if ties:
+        out.append(nt)
+    return out[0] if len(out) == 1 else tuple(out)
+
+
+def eval_pair(scene, ray, prim, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8):
+    """(accepted, t, u, v) of one ray against one caller-indexed triangle."""
+    sc = _as_scene(scene)
+    r = np.ascontiguousarray(ray, dtype=np.float32).reshape(8)
+    h = _Hit()
+    acc = lib().oracle_eval_pair(C.byref(sc.c), _ptr(r), int(prim), isect, alpha_threshold,
+                                 checker_freq, C.byref(h))
+    return bool(acc), h.t, h.u, h.v
+
+
+def mt(ray, v0, v1, v2, tmax=None):
+    r = np.ascontiguousarray(ray, dtype=np.float32).reshape(8)
+    a = [np.ascontiguousarray(x, dtype=np.float32).reshape(3) for x in (v0, v1, v2)]
+    t, u, v = C.c_float(), C.c_float(), C.c_float()
+    hit = lib().oracle_mt(_ptr(r), _ptr(a[0]), _ptr(a[1]), _ptr(a[2]),
+                          float(r[7] if tmax is None else tmax), C.byref(t), C.byref(u), C.byref(v))
+    return bool(hit), t.value, u.value, v.value
+
+
+def tex_alpha(tex, s, t):
+    tex = np.ascontiguousarray(tex, dtype=np.uint8)
+    return lib().oracle_tex_alpha(tex.shape[1], tex.shape[0], _ptr(tex), s, t)
+
+
+def slab(lo, hi, ray, best_t=None):
+    """(hit, tnear, tfar) of the walker's slab test (App. A.2)."""
+    r = np.ascontiguousarray(ray, dtype=np.float32).reshape(8)
+    lo = np.ascontiguousarray(lo, dtype=np.float32).reshape(3)
+    hi = np.ascontiguousarray(hi, dtype=np.float32).reshape(3)
+    tn, tf = C.c_float(), C.c_float()
+    hit = lib().walker_slab(_ptr(lo), _ptr(hi), _ptr(r), float(r[7] if best_t is None else best_t),
+                            C.byref(tn), C.byref(tf))
+    return bool(hit), tn.value, tf.value
+
+
+def lerp2(a, b, c, u, v):
+    arrs = [np.ascontiguousarray(x, dtype=np.float32).reshape(2) for x in (a, b, c)]
+    out = np.zeros(2, dtype=np.float32)
+    lib().oracle_lerp2(_ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), u, v, _ptr(out))
+    return out
+
+
+# ----------------------------------------------------------------------------
+# BVH in the export layout (DESIGN.md §"Data layout")
+# ----------------------------------------------------------------------------
+
+@dataclass
+class BvhArrays:
+    root_ref: int
+    root_lo: np.ndarray      # float32[3]
+    root_hi: np.ndarray      # float32[3]
+    nodes: np.ndarray        # uint32[num_nodes, 16]  (64 B pair nodes)
+    tris: np.ndarray         # uint32[num_tris, 12]   (48 B)
+    sides: np.ndarray        # uint32[num_tris, 8]    (32 B)
+    texdescs: np.ndarray     # uint32[num_textures, 4] (16 B: offset lo/hi, w, h)
+    texels: np.ndarray       # uint32[total texels]
+
+    def c_struct(self):
+        keep = [np.ascontiguousarray(x) for x in (self.nodes, self.tris, self.sides,
+                                                   self.texdescs, self.texels)]
+        self._keep = keep
+        return _Bvh(self.root_ref, (C.c_float * 3)(*self.root_lo.tolist()),
+                    (C.c_float * 3)(*self.root_hi.tolist()), keep[0].shape[0], keep[1].shape[0],
+                    keep[3].shape[0], _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]), _ptr(keep[3]),
+                    _ptr(keep[4]))
+
+
+def build_bvh(scene, max_leaf: int = 4) -> BvhArrays:
+    """Oracle-side object-median BVH in the export layout."""
+    sc = _as_scene(scene)
+    b = _Bvh()
+    rc = lib().oracle_build_bvh(C.byref(sc.c), max_leaf, C.byref(b))
+    if rc != 0:
+        lib().oracle_bvh_free(C.byref(b))
+        raise ValueError(f"oracle_build_bvh failed ({rc})")
+
+    def grab(ptr, count, width):
+        if count == 0:
+            return np.zeros((0, width), dtype=np.uint32)
+        arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint32)), shape=(count * width,))
+        return arr.copy().reshape(count, width)
+
+    total = 0
+    td = grab(b.texdescs, b.num_textures, 4)
+    for row in td:
+        total = max(total, int(row[0]) + (int(row[1]) << 32) + int(row[2]) * int(row[3]))
+    out = BvhArrays(b.root_ref, np.array(b.root_lo, dtype=np.float32),
+                    np.array(b.root_hi, dtype=np.float32), grab(b.nodes, b.num_nodes, 16),
+                    grab(b.tris, b.num_tris, 12), grab(b.sides, b.num_tris, 8), td,
+                    grab(b.texels, total, 1).reshape(-1))
+    lib().oracle_bvh_free(C.byref(b))
+    return out
+
+
+def walk(bvh: BvhArrays, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01,
+         checker_freq=8, nthreads=None):
+    """Contract walker C.  Returns (hits HIT_DTYPE, counts COUNT_DTYPE)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty(n, dtype=HIT_DTYPE)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    cb = bvh.c_struct()
+    rc = lib().walker_trace(C.byref(cb), _ptr(r), n, query, isect, alpha_threshold, checker_freq,
+                            _ptr(hits), _ptr(counts), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace failed ({rc})")
+    return hits, counts

@@ -1,0 +1,132 @@
+/*
+ * oracle.h — TEST INFRASTRUCTURE ONLY.
+ *
+ * The plain, slow, obviously-correct CPU oracle for the custom-intersector
+ * hot path of arXiv 1912.12786 (PAPER.md = /root/reference/PAPER.md).
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference legs may load this library.  It shares no code, header,
+ * table or constant with the product (paper_1912_12786_b200/, include/):
+ * every struct below is re-declared here from the documented layouts in
+ * DESIGN.md, never included from the product.
+ *
+ * Three parts:
+ *   oracle S  (oracle.c)  brute force over every triangle in caller order —
+ *             the plain definition the BVH method must reach exactly
+ *             (PAPER.md:185-190 queries, :228-252 traversal only prunes).
+ *   oracle BVH (walker.c) a simple object-median BVH written in the export
+ *             layout, so count parity never needs an input from the product.
+ *   walker C  (walker.c)  the traversal contract of DESIGN.md §"Arithmetic
+ *             contract" over an exported/imported BVH;
+ *             the oracle for the counting intersector.
+ *
+ * Arithmetic: IEEE fp32 (the paper's listings use basic_triangle<3,float>
+ * and the literal .01f), compiled with
+ * -ffp-contract=off -fno-fast-math so no FMA contraction happens.
+ */
+#ifndef VSR_ORACLE_H
+#define VSR_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* query kinds */
+enum { OR_CLOSEST = 0, OR_ANY = 1 };
+/* intersector kinds (PAPER.md:195-219 default overload vs intersector;
+   §4 listings: alpha texture :296-316, procedural :319-322, bvh_costs :332-366) */
+enum { OR_NONE = 0, OR_DEFAULT = 1, OR_ALPHA_TEX = 2, OR_ALPHA_PROC = 3, OR_COUNT = 4 };
+
+/* ambiguity flags (SURVEY.md §8(c) exclusion classes), computed in double */
+enum { OR_X1_NEAR_TIE = 1u, OR_X2_EDGE_GRAZE = 2u, OR_X3_TEXEL_EDGE = 4u,
+       OR_X4_CHECKER_EDGE = 8u };
+
+typedef struct {
+  uint32_t num_tris;
+  const float* vertices;       /* 9 floats per triangle: v0, v1, v2          */
+  const uint32_t* geom_ids;    /* num_tris                                    */
+  const float* texcoords;      /* 6 floats per triangle: uv0, uv1, uv2        */
+  uint32_t num_geoms;
+  const uint32_t* geom_texture;/* geom_id -> texture index                    */
+  uint32_t num_textures;
+  const uint32_t* tex_w;       /* per texture width                           */
+  const uint32_t* tex_h;       /* per texture height                          */
+  const uint8_t* const* tex_rgba; /* per texture row-major RGBA8, row j = t-row j */
+} or_scene;
+
+typedef struct { float t, u, v; uint32_t prim; } or_hit;       /* 16 B */
+typedef struct { uint32_t boxes, tris, alpha; } or_counts;      /* walker */
+
+/* Brute-force oracle S.  rays: 8 floats each (o.xyz, tmin, d.xyz, tmax).
+ * flags may be NULL (no double shadow).  ntie may be NULL; else receives the
+ * number of accepted candidates whose t equals the winner's t exactly.
+ * Returns 0 on success. */
+int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, int isect,
+                 float alpha_threshold, uint32_t checker_freq, or_hit* hits,
+                 uint32_t* flags, uint32_t* ntie, int nthreads);
+
+/* One ray against one triangle (caller index) with the intersector's filter.
+ * Returns 1 iff accepted (geometric hit and filter); fills *out either way
+ * with the geometric t,u,v. */
+int oracle_eval_pair(const or_scene* s, const float* ray, uint32_t prim, int isect,
+                     float alpha_threshold, uint32_t checker_freq, or_hit* out);
+
+/* Individual textbook pieces, exposed for the closed-form pins. */
+int oracle_mt(const float* ray, const float* v0, const float* v1, const float* v2,
+              float tmax_cur, float* t, float* u, float* v);
+float oracle_tex_alpha(uint32_t w, uint32_t h, const uint8_t* rgba, float s, float t);
+void oracle_lerp2(const float* a, const float* b, const float* c, float u, float v,
+                  float* out);
+
+/* ---------------- export layout (re-declared from DESIGN.md) -------------- */
+typedef struct {          /* 64 B pair node */
+  float lo0[3], hi0[3], lo1[3], hi1[3];
+  uint32_t ref[2];
+  uint32_t pad[2];
+} or_node;
+typedef struct {          /* 48 B triangle: v0, prim_id, e1, 0, e2, 0 */
+  float v0[3]; uint32_t prim;
+  float e1[3]; uint32_t pad1;
+  float e2[3]; uint32_t pad2;
+} or_tri;
+typedef struct {          /* 32 B sidecar */
+  float uv[6]; uint32_t tex; uint32_t pad;
+} or_side;
+typedef struct {          /* 16 B texture descriptor */
+  uint64_t offset; uint32_t w, h;
+} or_texdesc;
+
+typedef struct {
+  uint32_t root_ref;
+  float root_lo[3], root_hi[3];
+  uint32_t num_nodes, num_tris, num_textures;
+  const or_node* nodes;
+  const or_tri* tris;
+  const or_side* sides;
+  const or_texdesc* texdescs;
+  const uint32_t* texels;   /* RGBA8 packed little-endian: a = texel >> 24 */
+} or_bvh;
+
+/* Oracle-side BVH builder: object-median split on the widest centroid axis,
+ * leaves of <= max_leaf triangles, written in the export layout.
+ * Output arrays are malloc'd and owned by the caller (or_bvh_free).
+ * Degenerate triangles (e1 x e2 == 0 exactly) are left out. */
+int oracle_build_bvh(const or_scene* s, uint32_t max_leaf, or_bvh* out);
+void oracle_bvh_free(or_bvh* b);
+
+/* Contract walker C: traversal of SURVEY.md App. A.2 over `b`.
+ * hits required; counts may be NULL.  Returns 0 on success, -1 on
+ * stack overflow (depth > 64) or a malformed reference. */
+int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int isect,
+                 float alpha_threshold, uint32_t checker_freq, or_hit* hits,
+                 or_counts* counts, int nthreads);
+
+/* Slab test of the walker (exposed for pins). Returns box hit; *tn entry
+ * clipped to tmin, *tf exit times (1+2*gamma_3) before the best_t clip. */
+int walker_slab(const float* lo, const float* hi, const float* ray, float best_t, float* tn,
+                float* tf);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,442 @@
+/*
+ * walker.c — TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * (1) oracle_build_bvh: a deliberately simple object-median BVH, written in
+ *     the documented export layout (DESIGN.md §"Data layout"), so that the
+ *     GPU's counting intersector can be checked on a tree the product did not
+ *     build.  Any valid BVH prunes exactly: the tree shape
+ *     changes counts, never accepted hits.
+ * (2) walker_trace: contract walker C — the while-while traversal of
+ *     PAPER.md:228-247 [§3.2 pseudocode] with both `intersect` call sites
+ *     (box and primitive) routed through the intersector,
+ *     under the pinned arithmetic of DESIGN.md §"Arithmetic contract"
+ *     (SURVEY.md App. A.2).  It is the oracle for the bvh_costs counting
+ *     intersector ("++num_boxes", "++num_tris").
+ *
+ * Counting rule (reading A11/A12 in DESIGN.md): the root
+ * box is tested once before the loop and counted; each inner node visited
+ * costs 2 box tests (both children); every triangle hook call counts 1.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define LEAF_BIT 0x80000000u
+#define MAX_STACK 64
+
+/* ====================== oracle BVH builder ================================ */
+typedef struct {
+  const or_scene* s;
+  uint32_t max_leaf;
+  uint32_t* idx;       /* triangle indices being partitioned */
+  float* cen;          /* 3 centroids per triangle (double-free: float) */
+  or_node* nodes;
+  uint32_t num_nodes, cap_nodes;
+  uint32_t* leaf_order; /* output triangle order */
+  uint32_t num_out;
+  int axis_sort;
+  int depth_max;
+} bld_t;
+
+static bld_t* g_bld; /* qsort context (builder is single-threaded) */
+
+static int cmp_axis(const void* a, const void* b) {
+  uint32_t ia = *(const uint32_t*)a, ib = *(const uint32_t*)b;
+  float ca = g_bld->cen[ia * 3 + g_bld->axis_sort], cb = g_bld->cen[ib * 3 + g_bld->axis_sort];
+  if (ca < cb) return -1;
+  if (ca > cb) return 1;
+  return ia < ib ? -1 : (ia > ib ? 1 : 0);
+}
+
+static void tri_bounds(const float* vt, float* lo, float* hi) {
+  for (int k = 0; k < 3; ++k) {
+    float a = vt[k], b = vt[3 + k], c = vt[6 + k];
+    float mn = a < b ? a : b; mn = mn < c ? mn : c;
+    float mx = a > b ? a : b; mx = mx > c ? mx : c;
+    lo[k] = mn; hi[k] = mx;
+  }
+}
+
+static void range_bounds(const bld_t* b, uint32_t beg, uint32_t end, float* lo, float* hi) {
+  lo[0] = lo[1] = lo[2] = INFINITY;
+  hi[0] = hi[1] = hi[2] = -INFINITY;
+  for (uint32_t k = beg; k < end; ++k) {
+    float tl[3], th[3];
+    tri_bounds(b->s->vertices + (size_t)b->idx[k] * 9, tl, th);
+    for (int a = 0; a < 3; ++a) {
+      if (tl[a] < lo[a]) lo[a] = tl[a];
+      if (th[a] > hi[a]) hi[a] = th[a];
+    }
+  }
+}
+
+/* outward padding 2^-20 * max(1,|x|), rounded outward to float */
+static void pad_box(float* lo, float* hi) {
+  for (int a = 0; a < 3; ++a) {
+    double l = lo[a], h = hi[a];
+    double pl = ldexp(fabs(l) > 1.0 ? fabs(l) : 1.0, -20);
+    double ph = ldexp(fabs(h) > 1.0 ? fabs(h) : 1.0, -20);
+    double ld = l - pl, hd = h + ph;
+    float lf = (float)ld, hf = (float)hd;
+    if ((double)lf > ld) lf = nextafterf(lf, -INFINITY);
+    if ((double)hf < hd) hf = nextafterf(hf, INFINITY);
+    lo[a] = lf; hi[a] = hf;
+  }
+}
+
+static uint32_t emit_leaf(bld_t* b, uint32_t beg, uint32_t end) {
+  uint32_t first = b->num_out;
+  for (uint32_t k = beg; k < end; ++k) b->leaf_order[b->num_out++] = b->idx[k];
+  return LEAF_BIT | ((end - beg - 1u) << 26) | first;
+}
+
+/* returns the ref of the subtree over idx[beg,end) */
+static uint32_t build_rec(bld_t* b, uint32_t beg, uint32_t end, int depth) {
+  if (depth > b->depth_max) b->depth_max = depth;
+  uint32_t n = end - beg;
+  if (n <= b->max_leaf) return emit_leaf(b, beg, end);
+  /* widest centroid axis, median split in sorted order */
+  float clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (uint32_t k = beg; k < end; ++k)
+    for (int a = 0; a < 3; ++a) {
+      float c = b->cen[b->idx[k] * 3 + a];
+      if (c < clo[a]) clo[a] = c;
+      if (c > chi[a]) chi[a] = c;
+    }
+  int axis = 0;
+  float ext = chi[0] - clo[0];
+  for (int a = 1; a < 3; ++a)
+    if (chi[a] - clo[a] > ext) { ext = chi[a] - clo[a]; axis = a; }
+  b->axis_sort = axis;
+  qsort(b->idx + beg, n, sizeof(uint32_t), cmp_axis);
+  uint32_t mid = beg + n / 2;
+  uint32_t me = b->num_nodes++;
+  if (me >= b->cap_nodes) return 0xFFFFFFFFu;
+  or_node* nd = &b->nodes[me];
+  memset(nd, 0, sizeof *nd);
+  float lo[3], hi[3];
+  range_bounds(b, beg, mid, lo, hi);
+  pad_box(lo, hi);
+  memcpy(b->nodes[me].lo0, lo, sizeof lo);
+  memcpy(b->nodes[me].hi0, hi, sizeof hi);
+  range_bounds(b, mid, end, lo, hi);
+  pad_box(lo, hi);
+  memcpy(b->nodes[me].lo1, lo, sizeof lo);
+  memcpy(b->nodes[me].hi1, hi, sizeof hi);
+  uint32_t r0 = build_rec(b, beg, mid, depth + 1);
+  uint32_t r1 = build_rec(b, mid, end, depth + 1);
+  b->nodes[me].ref[0] = r0;
+  b->nodes[me].ref[1] = r1;
+  return me;
+}
+
+static int degenerate9(const float* vt) {
+  float e1[3] = {vt[3] - vt[0], vt[4] - vt[1], vt[5] - vt[2]};
+  float e2[3] = {vt[6] - vt[0], vt[7] - vt[1], vt[8] - vt[2]};
+  double cx = (double)e1[1] * e2[2] - (double)e1[2] * e2[1];
+  double cy = (double)e1[2] * e2[0] - (double)e1[0] * e2[2];
+  double cz = (double)e1[0] * e2[1] - (double)e1[1] * e2[0];
+  return cx == 0.0 && cy == 0.0 && cz == 0.0;
+}
+
+int oracle_build_bvh(const or_scene* s, uint32_t max_leaf, or_bvh* out) {
+  memset(out, 0, sizeof *out);
+  if (!s || max_leaf < 1 || max_leaf > 32) return -1;
+  bld_t b;
+  memset(&b, 0, sizeof b);
+  b.s = s;
+  b.max_leaf = max_leaf;
+  b.idx = (uint32_t*)malloc(sizeof(uint32_t) * (s->num_tris + 1));
+  b.cen = (float*)malloc(sizeof(float) * 3 * (s->num_tris + 1));
+  uint32_t m = 0;
+  for (uint32_t i = 0; i < s->num_tris; ++i) {
+    const float* vt = s->vertices + (size_t)i * 9;
+    if (degenerate9(vt)) continue;
+    b.idx[m++] = i;
+    float lo[3], hi[3];
+    tri_bounds(vt, lo, hi);
+    for (int a = 0; a < 3; ++a) b.cen[i * 3 + a] = 0.5f * lo[a] + 0.5f * hi[a];
+  }
+  if (m == 0) { free(b.idx); free(b.cen); return -2; }
+  b.cap_nodes = m;
+  b.nodes = (or_node*)calloc(m, sizeof(or_node));
+  b.leaf_order = (uint32_t*)malloc(sizeof(uint32_t) * m);
+  g_bld = &b;
+  uint32_t root = build_rec(&b, 0, m, 0);
+  g_bld = NULL;
+  float lo[3], hi[3];
+  range_bounds(&b, 0, m, lo, hi);
+  pad_box(lo, hi);
+
+  or_tri* tris = (or_tri*)calloc(m, sizeof(or_tri));
+  or_side* sides = (or_side*)calloc(m, sizeof(or_side));
+  for (uint32_t k = 0; k < m; ++k) {
+    uint32_t i = b.leaf_order[k];
+    const float* vt = s->vertices + (size_t)i * 9;
+    for (int a = 0; a < 3; ++a) {
+      tris[k].v0[a] = vt[a];
+      tris[k].e1[a] = vt[3 + a] - vt[a];
+      tris[k].e2[a] = vt[6 + a] - vt[a];
+    }
+    tris[k].prim = i;
+    memcpy(sides[k].uv, s->texcoords ? s->texcoords + (size_t)i * 6 : (const float[6]){0}, 24);
+    uint32_t g = s->geom_ids ? s->geom_ids[i] : 0u;
+    sides[k].tex = s->geom_texture ? s->geom_texture[g] : g;
+  }
+  uint32_t nt = s->num_textures;
+  or_texdesc* td = (or_texdesc*)calloc(nt ? nt : 1, sizeof(or_texdesc));
+  uint64_t total = 0;
+  for (uint32_t k = 0; k < nt; ++k) {
+    td[k].offset = total; td[k].w = s->tex_w[k]; td[k].h = s->tex_h[k];
+    total += (uint64_t)s->tex_w[k] * s->tex_h[k];
+  }
+  uint32_t* texels = (uint32_t*)malloc(sizeof(uint32_t) * (total ? total : 1));
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint8_t* p = s->tex_rgba[k];
+    uint64_t cnt = (uint64_t)s->tex_w[k] * s->tex_h[k];
+    for (uint64_t q = 0; q < cnt; ++q)
+      texels[td[k].offset + q] = (uint32_t)p[4 * q] | ((uint32_t)p[4 * q + 1] << 8) |
+                                 ((uint32_t)p[4 * q + 2] << 16) | ((uint32_t)p[4 * q + 3] << 24);
+  }
+  out->root_ref = root;
+  memcpy(out->root_lo, lo, sizeof lo);
+  memcpy(out->root_hi, hi, sizeof hi);
+  out->num_nodes = b.num_nodes;
+  out->num_tris = m;
+  out->num_textures = nt;
+  out->nodes = b.nodes;
+  out->tris = tris;
+  out->sides = sides;
+  out->texdescs = td;
+  out->texels = texels;
+  free(b.idx);
+  free(b.cen);
+  free(b.leaf_order);
+  return b.depth_max > MAX_STACK ? -3 : 0;
+}
+
+void oracle_bvh_free(or_bvh* b) {
+  if (!b) return;
+  free((void*)b->nodes);
+  free((void*)b->tris);
+  free((void*)b->sides);
+  free((void*)b->texdescs);
+  free((void*)b->texels);
+  memset(b, 0, sizeof *b);
+}
+
+/* ====================== contract walker C ================================== */
+
+/* Slab test of App. A.2 (no FMA: -ffp-contract=off).  Box hook default. */
+static int slab(const float* lo, const float* hi, const float* o, const float* inv, float tmin,
+                float best_t, float* tn_out) {
+  float t0x = (lo[0] - o[0]) * inv[0], t1x = (hi[0] - o[0]) * inv[0];
+  float t0y = (lo[1] - o[1]) * inv[1], t1y = (hi[1] - o[1]) * inv[1];
+  float t0z = (lo[2] - o[2]) * inv[2], t1z = (hi[2] - o[2]) * inv[2];
+  float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));
+  float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
+  tf = fminf(tf, best_t);
+  *tn_out = tn;
+  return tn <= tf;
+}
+
+/* Exposed for the closed-form pins: guarded reciprocal of
+ * App. A.2 followed by the slab test; tf returned before the best_t clip. */
+int walker_slab(const float* lo, const float* hi, const float* ray, float best_t, float* tn,
+                float* tf) {
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    float dk = ray[4 + a];
+    inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
+  }
+  float t0x = (lo[0] - ray[0]) * inv[0], t1x = (hi[0] - ray[0]) * inv[0];
+  float t0y = (lo[1] - ray[1]) * inv[1], t1y = (hi[1] - ray[1]) * inv[1];
+  float t0z = (lo[2] - ray[2]) * inv[2], t1z = (hi[2] - ray[2]) * inv[2];
+  *tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
+  return slab(lo, hi, ray, inv, ray[3], best_t, tn);
+}
+
+/* Möller–Trumbore on the stored (v0, e1, e2), App. A.1 order. */
+static int mt_tri(const or_tri* tr, const float* o, const float* d, float tmin, float tmax_cur,
+                  float* t, float* u, float* v) {
+  const float* e1 = tr->e1;
+  const float* e2 = tr->e2;
+  float p[3] = {d[1] * e2[2] - d[2] * e2[1], d[2] * e2[0] - d[0] * e2[2],
+                d[0] * e2[1] - d[1] * e2[0]};
+  float det = (e1[0] * p[0] + e1[1] * p[1]) + e1[2] * p[2];
+  if (!(fabsf(det) >= 1e-12f)) return 0;
+  float inv = 1.0f / det;
+  float s[3] = {o[0] - tr->v0[0], o[1] - tr->v0[1], o[2] - tr->v0[2]};
+  *u = ((s[0] * p[0] + s[1] * p[1]) + s[2] * p[2]) * inv;
+  float q[3] = {s[1] * e1[2] - s[2] * e1[1], s[2] * e1[0] - s[0] * e1[2],
+                s[0] * e1[1] - s[1] * e1[0]};
+  *v = ((d[0] * q[0] + d[1] * q[1]) + d[2] * q[2]) * inv;
+  *t = ((e2[0] * q[0] + e2[1] * q[1]) + e2[2] * q[2]) * inv;
+  return (*u >= 0.0f) && (*u <= 1.0f) && (*v >= 0.0f) && (*u + *v <= 1.0f) && (*t >= tmin) &&
+         (*t <= tmax_cur);
+}
+
+static long wrapi(float x, uint32_t n) {
+  long i = (long)floorf(x * (float)n);
+  long m = (long)n;
+  return ((i % m) + m) % m;
+}
+
+static int walk_filter(const or_bvh* b, uint32_t k, int isect, float u, float v, float thr,
+                       uint32_t M) {
+  if (isect == OR_ALPHA_TEX) {
+    const or_side* sd = &b->sides[k];
+    float w = (1.0f - u) - v;
+    float s = (w * sd->uv[0] + u * sd->uv[2]) + v * sd->uv[4];
+    float t = (w * sd->uv[1] + u * sd->uv[3]) + v * sd->uv[5];
+    const or_texdesc* td = &b->texdescs[sd->tex];
+    long i = wrapi(s, td->w), j = wrapi(t, td->h);
+    uint32_t texel = b->texels[td->offset + (uint64_t)j * td->w + (uint64_t)i];
+    float a = (float)(texel >> 24) / 255.0f;
+    return a >= thr;
+  }
+  if (isect == OR_ALPHA_PROC) {
+    float fm = (float)M;
+    int cu = (int)floorf(u * fm), cv = (int)floorf(v * fm);
+    return ((cu + cv) % 2) == 0;
+  }
+  return 1;
+}
+
+typedef struct {
+  const or_bvh* b;
+  const float* rays;
+  uint64_t n;
+  int query, isect;
+  float thr;
+  uint32_t M;
+  or_hit* hits;
+  or_counts* counts;
+  uint64_t next;
+  int err;
+} wjob_t;
+
+static int walk_one(const wjob_t* jb, uint64_t r) {
+  const or_bvh* b = jb->b;
+  const float* ray = jb->rays + r * 8;
+  const float* o = ray;
+  const float* d = ray + 4;
+  float tmin = ray[3];
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    float dk = d[a];
+    inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
+  }
+  or_hit best = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
+  float best_t = ray[7];
+  int have = 0;
+  or_counts c = {0, 0, 0};
+  uint32_t st_ref[MAX_STACK];
+  float st_tn[MAX_STACK];
+  int sp = 0;
+  int bad = 0;
+  float tn;
+
+  c.boxes++;
+  if (!slab(b->root_lo, b->root_hi, o, inv, tmin, best_t, &tn)) goto done;
+  uint32_t cur = b->root_ref;
+  for (;;) {
+    /* inner-node loop */
+    while (!(cur & LEAF_BIT)) {
+      if (cur >= b->num_nodes) { bad = 1; goto done; }
+      const or_node* nd = &b->nodes[cur];
+      float tn0, tn1;
+      c.boxes += 2;
+      int h0 = slab(nd->lo0, nd->hi0, o, inv, tmin, best_t, &tn0);
+      int h1 = slab(nd->lo1, nd->hi1, o, inv, tmin, best_t, &tn1);
+      if (h0 && h1) {
+        uint32_t nearr, farr;
+        float ftn;
+        if (tn1 < tn0) { nearr = nd->ref[1]; farr = nd->ref[0]; ftn = tn0; }
+        else { nearr = nd->ref[0]; farr = nd->ref[1]; ftn = tn1; }
+        if (sp >= MAX_STACK) { bad = 1; goto done; }
+        st_ref[sp] = farr; st_tn[sp] = ftn; sp++;
+        cur = nearr;
+      } else if (h0) {
+        cur = nd->ref[0];
+      } else if (h1) {
+        cur = nd->ref[1];
+      } else {
+        goto pop;
+      }
+    }
+    /* leaf loop */
+    {
+      uint32_t first = cur & 0x03FFFFFFu;
+      uint32_t cnt = ((cur >> 26) & 31u) + 1u;
+      if ((uint64_t)first + cnt > b->num_tris) { bad = 1; goto done; }
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        const or_tri* tr = &b->tris[k];
+        float t, u, v;
+        c.tris++;
+        if (!mt_tri(tr, o, d, tmin, best_t, &t, &u, &v)) continue;
+        if (jb->isect == OR_ALPHA_TEX) c.alpha++;
+        if (!walk_filter(b, k, jb->isect, u, v, jb->thr, jb->M)) continue;
+        if (jb->query == OR_ANY) {
+          best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
+          goto done;
+        }
+        if (!have || t < best_t) {
+          best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
+          best_t = t;
+          have = 1;
+        }
+      }
+    }
+  pop:
+    for (;;) {
+      if (sp == 0) goto done;
+      sp--;
+      if (st_tn[sp] > best_t) continue;
+      cur = st_ref[sp];
+      break;
+    }
+  }
+done:
+  jb->hits[r] = best;
+  if (jb->counts) jb->counts[r] = c;
+  return bad;
+}
+
+static void* wworker(void* arg) {
+  wjob_t* jb = (wjob_t*)arg;
+  const uint64_t chunk = 1024;
+  for (;;) {
+    uint64_t s = __atomic_fetch_add(&jb->next, chunk, __ATOMIC_RELAXED);
+    if (s >= jb->n) break;
+    uint64_t e = s + chunk < jb->n ? s + chunk : jb->n;
+    for (uint64_t r = s; r < e; ++r)
+      if (walk_one(jb, r)) __atomic_store_n(&jb->err, 1, __ATOMIC_RELAXED);
+  }
+  return NULL;
+}
+
+int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int isect,
+                 float thr, uint32_t M, or_hit* hits, or_counts* counts, int nthreads) {
+  if (!b || !rays || !hits) return -1;
+  if (query != OR_CLOSEST && query != OR_ANY) return -1;
+  if (isect < OR_NONE || isect > OR_COUNT) return -1;
+  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  wjob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.b = b; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr;
+  jb.M = M; jb.hits = hits; jb.counts = counts;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads == 1) {
+    wworker(&jb);
+  } else {
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, wworker, &jb);
+    for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+    free(th);
+  }
+  return jb.err ? -1 : 0;
+}
