@@ -1,0 +1,447 @@
+#!/usr/bin/env python
+"""bench.py — Mrays/s of the custom-intersector trace path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl own|reference]
+                    [--config C2] [--query closest|any] [--isect alpha_texture|...]
+
+A step is one pass of the whole hot path (ray fetch,
+root test, inner-node loop, leaf loop with the intersector, hit write) over one
+1920×1080 frame of the C2 billboard forest (BASELINE.json configs[1]): ONE
+`vsr_trace` launch.  Inputs are resident in HBM when the timed region starts;
+L2 is flushed (256 MiB write) before every timed step, outside the events.
+
+N > 1 (torchrun): weak scaling — every rank traces its own 1080p frame (camera
+shifted per rank) against a scene built once on rank 0 and broadcast with NCCL;
+the timed path has no collective (rays are independent).
+Timing: CUDA events on the launching stream, max over ranks.
+
+--impl reference: the CPU oracle (oracle S, brute force, as it stands) on the
+host cores, each step a bounded ray sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Mrays/s per B200 (alpha-mask any-hit, 1080p) at 1/2/4/8 GPUs; % HBM roofline"
+UNIT = "Mrays/s"
+ISECTS = ("none", "default", "alpha_texture", "alpha_procedural", "count", "count_alpha_texture",
+          "runtime_switch_default", "runtime_fnptr_default", "runtime_switch_alpha_texture",
+          "runtime_fnptr_alpha_texture")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="own", choices=["own", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--query", default="closest", choices=["closest", "any"])
+    ap.add_argument("--isect", default="alpha_texture")
+    ap.add_argument("--no-variants", action="store_true", help="skip the C3 intersector sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def config_desc(name):
+    import workloads as W
+    return {"workload": f"{name}: {W.CONFIGS[name]}"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML in a background thread)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, device_index=0, period=0.002):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.period = period
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "samples": len(self.samples), "reasons": names}
+
+
+# ---------------------------------------------------------------------------
+# workload
+# ---------------------------------------------------------------------------
+def make_workload(name, rank=0):
+    import workloads as W
+    if name in ("C2", "C3"):
+        sc = W.forest_scene()
+        rays = W.pinhole_rays((2.0 * rank, 4.0, -280.0), (2.0 * rank, 4.0, 0.0), (0.0, 1.0, 0.0),
+                              45.0, 1920, 1080)
+        return sc, rays
+    return W.config(name)
+
+
+def algorithmic_bytes(counts_np, isect_has_alpha):
+    """B(r) = 32 + 16 + 64*I + 48*T + 36*A, I = (boxes-1)/2."""
+    boxes = counts_np["boxes"].astype(np.int64)
+    tris = counts_np["tris"].astype(np.int64)
+    alpha = counts_np["alpha"].astype(np.int64) if isect_has_alpha else 0
+    inner = (boxes - 1) // 2
+    per_ray = 48 + 64 * inner + 48 * tris + 36 * alpha
+    return int(per_ray.sum()), {"inner_per_ray": float(inner.mean()), "tris_per_ray": float(tris.mean()),
+                                "alpha_per_ray": float(np.mean(alpha)) if isect_has_alpha else 0.0}
+
+
+# ---------------------------------------------------------------------------
+# own arm
+# ---------------------------------------------------------------------------
+def run_own(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1912_12786_b200 import _build, shard, vsr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+
+    q = vsr.CLOSEST if args.query == "closest" else vsr.ANY
+    isect = getattr(vsr, args.isect.upper())
+    sc, rays = make_workload(args.config, rank)
+    t0 = time.time()
+    if world > 1:
+        base = vsr.Scene.from_workload(sc, device=local).build() if rank == 0 else None
+        scene, _ = shard.broadcast_scene(base, local, dist)
+    else:
+        scene = vsr.Scene.from_workload(sc, device=local).build()
+    setup_s = time.time() - t0
+    stats = scene.stats()
+    n = rays.n
+    d_rays = torch.from_numpy(rays.data).cuda()
+    hits = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    counts = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20) // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    sh = stream.cuda_stream
+
+    def trace(kind, query=q):
+        scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
+                        counts.data_ptr(), sh)
+
+    def timed(kind, steps, warmup, query=q, sampler=None):
+        for _ in range(warmup):
+            flush.fill_(1.0)
+            trace(kind, query)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = vsr.launch_count()
+        ctx = sampler if sampler is not None else _Null()
+        with ctx:
+            for a, b in evs:
+                flush.fill_(1.0)
+                a.record(stream)
+                trace(kind, query)
+                b.record(stream)
+            torch.cuda.synchronize()
+        launches = vsr.launch_count() - l0
+        if world > 1:
+            dist.barrier()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        return ms, launches
+
+    # ---- headline ----
+    sampler = ClockSampler(local)
+    ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler)
+    ms_step = float(np.mean(ms))
+    if world > 1:
+        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step_max = float(t.item())
+    else:
+        ms_step_max = ms_step
+    value = world * n / (ms_step_max * 1e-3) / 1e6
+
+    # ---- algorithmic bytes from the counting intersector (untimed) ----
+    has_alpha = args.isect in ("alpha_texture", "runtime_switch_alpha_texture",
+                               "runtime_fnptr_alpha_texture")
+    cnt_kind = vsr.COUNT_ALPHA_TEXTURE if has_alpha else vsr.COUNT
+    trace(cnt_kind)
+    torch.cuda.synchronize()
+    cnp = vsr.counts_to_numpy(counts)
+    bytes_launch, work = algorithmic_bytes(cnp, has_alpha)
+    peak, peak_src = load_peaks()
+    achieved = bytes_launch / (ms_step * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": bytes_launch,
+                "bytes_per_ray": round(bytes_launch / n, 1), "work_per_ray": work,
+                "kernel": f"trace_kernel<{args.query}, {args.isect}>"}
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            tr = json.load(open(prof)).get(f"{args.config}:{args.query}:{args.isect}")
+            if tr:
+                roofline["traffic"] = tr["dram_bytes_per_launch"]
+                roofline["traffic_source"] = tr.get("source")
+        except Exception:
+            pass
+
+    # ---- variants: any-hit + the C3 zero-cost sweep (rank 0 only reports) ----
+    extra = {}
+    if not args.no_variants:
+        ms_any, _ = timed(isect, max(5, args.steps // 2), 3, query=vsr.ANY if q == vsr.CLOSEST else vsr.CLOSEST)
+        extra["other_query"] = {"query": "any" if q == vsr.CLOSEST else "closest",
+                                "value": round(n / (np.mean(ms_any) * 1e-3) / 1e6, 1),
+                                "ms": round(float(np.mean(ms_any)), 4)}
+        var = {}
+        for name in ISECTS:
+            kind = getattr(vsr, name.upper())
+            m, _ = timed(kind, max(5, args.steps // 2), 3)
+            var[name] = round(n / (np.mean(m) * 1e-3) / 1e6, 1)
+        # interleaved A/B for the zero-cost claim
+        a_ms, b_ms = [], []
+        for _ in range(max(5, args.steps // 2)):
+            a_ms += timed(vsr.NONE, 1, 1)[0]
+            b_ms += timed(vsr.DEFAULT, 1, 1)[0]
+        extra["variants_mrays"] = var
+        extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
+                              "default_ms": round(float(np.median(b_ms)), 4),
+                              "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}
+
+    # ---- end to end through vsr_trace_host (pinned host buffers) ----
+    h_rays = torch.from_numpy(rays.data).pin_memory()
+    h_hits = torch.empty((n, 4), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        scene.trace_host(h_rays, q, isect, hits=h_hits, stream=stream)
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for _ in range(max(3, args.steps // 2)):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        scene.trace_host(h_rays, q, isect, hits=h_hits, stream=stream)
+        b.record(stream)
+        b.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e_step = float(np.mean(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_step = float(t.item())
+    e2e = {"value": round(world * n / (e2e_step * 1e-3) / 1e6, 2), "unit": UNIT,
+           "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": n * 16,
+           "ms_per_step": round(e2e_step, 4), "api": "vsr_trace_host (pinned host buffers)"}
+
+    # ---- cpu baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(sc, rays, args, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        clocks = sampler.summary()
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step_max, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generators, workloads/)",
+            "config": {**config_desc(args.config), "query": args.query, "intersector": args.isect,
+                       "rays_per_gpu": n, "resolution": "1920x1080x1spp",
+                       "triangles": int(stats["num_tris"]), "bvh_nodes": int(stats["num_nodes"]),
+                       "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
+                       "l2": "flushed before every timed step (256 MiB write, outside the events)",
+                       "parallelism": f"rays sharded by frame, {world} rank(s), no data-path collective",
+                       "setup_s": round(setup_s, 2)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "ms_per_step_each": [round(x, 4) for x in ms], **extra,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (cpu_baseline and --impl reference)
+# ---------------------------------------------------------------------------
+def _oracle_kind(name):
+    import oracle
+    base = name.replace("runtime_switch_", "").replace("runtime_fnptr_", "").replace("count_", "")
+    return {"none": oracle.NONE, "default": oracle.DEFAULT, "alpha_texture": oracle.ALPHA_TEX,
+            "alpha_procedural": oracle.ALPHA_PROC, "count": oracle.DEFAULT}[base]
+
+
+def cpu_baseline(sc, rays, args, target_s=12.0):
+    """Oracle S as it stands (brute force, all host cores) on a bounded seeded sample."""
+    import oracle
+    oq = oracle.CLOSEST if args.query == "closest" else oracle.ANY
+    ok = _oracle_kind(args.isect)
+    osc = oracle.OracleScene(sc)
+    cores = host_cores()
+    rng = np.random.default_rng(12345)
+    probe = rays.data[rng.choice(rays.n, 64 * cores, replace=False)]
+    t0 = time.perf_counter()
+    oracle.trace(osc, probe, oq, ok, nthreads=cores)
+    per_ray = (time.perf_counter() - t0) / probe.shape[0]
+    m = int(min(rays.n, max(256, target_s / max(per_ray, 1e-9))))
+    sample = rays.data[np.sort(rng.choice(rays.n, m, replace=False))]
+    t0 = time.perf_counter()
+    oracle.trace(osc, sample, oq, ok, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(m / dt / 1e6, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{m} seeded rays of the {rays.n}-ray frame, brute force vs all "
+                      f"{sc.num_tris} triangles, {dt:.1f} s", "cpu": cpu_model()}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    sc, rays = make_workload(args.config, 0)
+    oq = oracle.CLOSEST if args.query == "closest" else oracle.ANY
+    ok = _oracle_kind(args.isect)
+    osc = oracle.OracleScene(sc)
+    cores = host_cores()
+    rng = np.random.default_rng(777)
+    probe = rays.data[rng.choice(rays.n, 32 * cores, replace=False)]
+    t0 = time.perf_counter()
+    oracle.trace(osc, probe, oq, ok, nthreads=cores)
+    per_ray = (time.perf_counter() - t0) / probe.shape[0]
+    budget = 150.0 / max(1, args.steps + args.warmup)       # whole run ~2.5 min
+    m = int(min(rays.n, max(128, budget / max(per_ray, 1e-9))))
+    times = []
+    for step in range(args.warmup + args.steps):
+        idx = np.sort(rng.choice(rays.n, m, replace=False))
+        sample = rays.data[idx]
+        t0 = time.perf_counter()
+        oracle.trace(osc, sample, oq, ok, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+    ms = float(np.mean(times)) * 1e3
+    value = m / (ms * 1e-3) / 1e6
+    line = {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generators, workloads/)", "impl": "reference",
+            "config": {**config_desc(args.config), "query": args.query, "intersector": args.isect,
+                       "rays_per_step": m, "triangles": sc.num_tris},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{m} seeded rays per step of the {rays.n}-ray frame, brute "
+                                       f"force vs {sc.num_tris} triangles", "cpu": cpu_model()},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_own(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,210 @@
+/*
+ * vsr.h — C ABI of the B200-native custom-intersector ray tracing path.
+ *
+ * What it implements (PAPER.md = arXiv 1912.12786, "custom intersectors"):
+ *   per-ray BVH traversal with ray–triangle intersection, where the
+ *   intersector — the user code that may veto a hit (PAPER.md:140-184
+ *   [§3.1 listings 2-3]) — is injected at COMPILE time into both call sites
+ *   of the while-while traversal (PAPER.md:228-252 [§3.2 pseudocode]).
+ *   Every (query, intersector) pair is its own kernel instantiation chosen
+ *   once on the host, so the default path carries no device-side branch or
+ *   function pointer: the paper's zero-cost claim.
+ *
+ * Conventions for every entry point:
+ *   - all functions are extern "C", return a vsr_status, and never throw;
+ *   - argument errors are detected synchronously and leave no side effect;
+ *   - on error, vsr_last_error() returns a thread-local message that stays
+ *     valid until the next vsr_* call on that thread;
+ *   - distinct scenes may be used from distinct threads concurrently; a
+ *     built scene is read-only and may be traced from several streams at
+ *     once; building while tracing the same scene is not allowed.
+ *
+ * Layouts below are little-endian and part of the ABI (DESIGN.md §"Data
+ * layout" documents each byte).
+ */
+#ifndef VSR_H
+#define VSR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSR_ABI_VERSION 1u
+
+typedef enum {
+  VSR_OK = 0,
+  VSR_ERR_INVALID_ARG = 1,  /* NULL handle/pointer, misaligned buffer, bad enum, bad size */
+  VSR_ERR_EMPTY_SCENE = 2,  /* zero triangles, or every triangle degenerate */
+  VSR_ERR_NONFINITE = 3,    /* NaN/Inf vertex or texcoord                    */
+  VSR_ERR_BVH_TOO_DEEP = 4, /* traversal stack would exceed 64 entries      */
+  VSR_ERR_NOT_BUILT = 5,    /* vsr_trace before vsr_bvh_build / vsr_scene_import         */
+  VSR_ERR_CUDA = 6,         /* a CUDA runtime call failed; message in vsr_last_error()   */
+  VSR_ERR_OOM = 7,          /* host or device allocation failed                          */
+  VSR_ERR_UNSUPPORTED = 8   /* combination not provided (e.g. > 2^26 triangles)          */
+} vsr_status;
+
+/* Visibility queries: closest-hit = min-t accepted hit;
+ * any-hit = the first accepted hit encountered during traversal. */
+typedef enum { VSR_QUERY_CLOSEST = 0, VSR_QUERY_ANY = 1 } vsr_query;
+
+/* Intersectors.  Each value selects a distinct compile-time instantiation.
+ *   NONE              the default overload without an intersector argument
+ *                     (PAPER.md:195-205): traversal calls intersect() directly.
+ *   DEFAULT           basic_intersector with no override: every
+ *                     hook forwards to intersect().  Compiles to the same SASS as NONE.
+ *   ALPHA_TEXTURE     §4 alpha-mask listing: on a geometric hit,
+ *                     look up textures[geom_texture[geom_id]] at lerp(uv0,uv1,uv2,u,v)
+ *                     (nearest, wrap) and keep the hit iff alpha >= alpha_threshold.
+ *                     A vetoed hit does not shrink tmax: traversal continues.
+ *   ALPHA_PROCEDURAL  procedural mask: keep iff
+ *                     floor(u*M) + floor(v*M) is even, M = checker_freq.
+ *   COUNT             bvh_costs: ++num_boxes per box hook,
+ *                     ++num_tris per triangle hook, default filter; writes d_counts.
+ *   COUNT_ALPHA_TEXTURE  bvh_costs stacked on ALPHA_TEXTURE (the cost of the alpha
+ *                     intersector's traversal; also counts alpha lookups).
+ *   RUNTIME_*         measurement controls for the zero-cost claim: the same
+ *                     traversal with the filter chosen at RUN time inside the loop,
+ *                     the Embree/OptiX style the paper contrasts with.
+ *                     100+k: switch on kind k; 200+k: device function pointer with a
+ *                     null check (k = DEFAULT means a null pointer). */
+typedef enum {
+  VSR_ISECT_NONE = 0,
+  VSR_ISECT_DEFAULT = 1,
+  VSR_ISECT_ALPHA_TEXTURE = 2,
+  VSR_ISECT_ALPHA_PROCEDURAL = 3,
+  VSR_ISECT_COUNT = 4,
+  VSR_ISECT_COUNT_ALPHA_TEXTURE = 5,
+  VSR_ISECT_RUNTIME_SWITCH_DEFAULT = 101,
+  VSR_ISECT_RUNTIME_SWITCH_ALPHA_TEXTURE = 102,
+  VSR_ISECT_RUNTIME_SWITCH_ALPHA_PROCEDURAL = 103,
+  VSR_ISECT_RUNTIME_FNPTR_DEFAULT = 201,
+  VSR_ISECT_RUNTIME_FNPTR_ALPHA_TEXTURE = 202,
+  VSR_ISECT_RUNTIME_FNPTR_ALPHA_PROCEDURAL = 203
+} vsr_isect;
+
+/* 32 B, 16-B aligned.  t is in units of d (d need not be normalised);
+ * the accepted interval is [tmin, tmax], inclusive. */
+typedef struct { float ox, oy, oz, tmin, dx, dy, dz, tmax; } vsr_ray;
+
+/* 16 B.  prim_id is the caller's triangle index (reordering is invisible).
+ * Miss: prim_id = 0xFFFFFFFF, t = +inf, u = v = 0 (reading A24).
+ * Barycentrics: hit point = v0 + u*(v1-v0) + v*(v2-v0). */
+typedef struct { float t, u, v; uint32_t prim_id; } vsr_hit;
+#define VSR_MISS 0xFFFFFFFFu
+
+/* 16 B per ray, written by COUNT and COUNT_ALPHA_TEXTURE only. */
+typedef struct { uint32_t num_boxes, num_tris, num_alpha, reserved; } vsr_counts;
+
+/* Row-major RGBA8, row j holds texture coordinate t in [j/H, (j+1)/H). */
+typedef struct { uint32_t width, height; const uint8_t* rgba8; } vsr_texture_desc;
+
+typedef struct {
+  uint32_t num_tris;
+  const float* vertices;          /* host, 9 floats per triangle (v0, v1, v2); copied      */
+  const uint32_t* geom_ids;       /* host, num_tris; NULL -> all 0                          */
+  const float* texcoords;         /* host, 6 floats per triangle (uv0,uv1,uv2); NULL -> 0;
+                                     |value| <= 1024                                        */
+  uint32_t num_geoms;             /* size of geom_texture (ignored if geom_texture NULL)    */
+  const uint32_t* geom_texture;   /* host, geom -> texture index; NULL -> identity          */
+  uint32_t num_textures;          /* 0 -> one implicit 1x1 opaque white texture     */
+  const vsr_texture_desc* textures; /* host; 1 <= width, height <= 65536                    */
+  int device;                     /* CUDA ordinal that owns the device copies               */
+} vsr_scene_desc;
+
+/* Binned SAH parameters.  NULL -> {4, 16, 1.0, 1.0}.
+ * 1 <= max_leaf_size <= 32, 2 <= sah_bins <= 256. */
+typedef struct {
+  uint32_t max_leaf_size, sah_bins;
+  float traversal_cost, intersection_cost;
+} vsr_build_params;
+
+/* NULL -> {0.01f, 8 (reading A4)}.  checker_freq >= 1. */
+typedef struct { float alpha_threshold; uint32_t checker_freq; } vsr_isect_params;
+
+typedef struct vsr_scene vsr_scene;
+
+/* Flattened acceleration structure in the export layout:
+ *   nodes    64 B each: float lo0[3],hi0[3],lo1[3],hi1[3]; uint32 ref[2]; uint32 pad[2]
+ *   tris     48 B each: float v0[3]; uint32 prim_id; float e1[3]; 0; float e2[3]; 0
+ *   sides    32 B each: float uv0[2],uv1[2],uv2[2]; uint32 texture; 0
+ *   texdescs 16 B each: uint64 texel_offset; uint32 width, height
+ *   texels    4 B each: RGBA8 packed little-endian (alpha = texel >> 24)
+ * ref encoding: bit31 = leaf; leaf: bits 26..30 = count-1, bits 0..25 = first tri;
+ * inner: node index.  root_ref may be a leaf (no nodes). */
+typedef struct {
+  uint32_t root_ref;
+  float root_lo[3], root_hi[3];
+  uint32_t num_nodes, num_tris, num_textures;
+  uint64_t num_texels;
+  void* nodes;
+  void* tris;
+  void* sides;
+  void* texdescs;
+  void* texels;
+} vsr_bvh_view;
+
+typedef struct {
+  uint32_t num_tris_input, num_tris, num_degenerate;
+  uint32_t num_nodes, num_leaves, max_depth, num_textures, built;
+  uint64_t num_texels, device_bytes;
+  double build_ms;
+} vsr_stats;
+
+/* Validate and copy a host scene description.  No device work.
+ * Errors: INVALID_ARG (NULL desc/out, vertices NULL with num_tris > 0, geom or texture
+ * index out of range, bad texture size, |texcoord| > 1024), NONFINITE, OOM. */
+vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out);
+
+/* Build the BVH on the host (binned SAH), flatten it to the export
+ * layout and upload everything to desc->device.  Synchronous; untimed setup.
+ * Degenerate triangles (e1 x e2 == 0) are excluded and never hit.
+ * Errors: INVALID_ARG, EMPTY_SCENE, BVH_TOO_DEEP, UNSUPPORTED, CUDA, OOM. */
+vsr_status vsr_bvh_build(vsr_scene* scene, const vsr_build_params* params);
+
+/* Enqueue one trace of n rays on `stream` (a cudaStream_t; NULL = legacy default).
+ * d_rays / d_hits / d_counts are caller-owned DEVICE buffers on the scene's device,
+ * 16-B aligned.  d_counts is required iff isect is COUNT or COUNT_ALPHA_TEXTURE.
+ * Asynchronous: results are valid once the stream is synchronised.  n = 0 is a
+ * no-op.  Errors: INVALID_ARG, NOT_BUILT, CUDA (launch failure). */
+vsr_status vsr_trace(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                     vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                     vsr_counts* d_counts, void* stream);
+
+/* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
+ * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
+ * overlap the kernel; returns after the stream work completed. */
+vsr_status vsr_trace_host(vsr_scene* scene, const vsr_ray* h_rays, uint64_t n,
+                          vsr_query query, vsr_isect isect, const vsr_isect_params* params,
+                          vsr_hit* h_hits, vsr_counts* h_counts, void* stream);
+
+/* Free a scene and all its device memory.  NULL is a no-op. */
+vsr_status vsr_destroy(vsr_scene* scene);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* vsr_last_error(void);
+
+/* Sizes (all pointers NULL in *view) or copies (non-NULL pointers, host or device,
+ * cudaMemcpyDefault) of the built structure in the export layout. */
+vsr_status vsr_bvh_export(const vsr_scene* scene, vsr_bvh_view* view);
+
+/* Create a built scene on `device` directly from export-layout buffers (host or
+ * device pointers), e.g. after a broadcast.  The structure is validated: every
+ * ref in range, every triangle referenced by exactly one leaf, depth <= 64,
+ * texture indices and texel ranges in bounds.
+ * Errors: INVALID_ARG (malformed), BVH_TOO_DEEP, CUDA, OOM. */
+vsr_status vsr_scene_import(const vsr_bvh_view* view, int device, vsr_scene** out);
+
+vsr_status vsr_scene_stats(const vsr_scene* scene, vsr_stats* out);
+
+/* Number of kernels this library has launched in this process (all scenes). */
+uint64_t vsr_launch_count(void);
+
+uint32_t vsr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSR_H */

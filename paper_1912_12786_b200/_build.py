@@ -1,0 +1,63 @@
+"""Build libvsr.so in-tree with nvcc for sm_100a (no JIT cache, no torch extension).
+
+    python -m paper_1912_12786_b200._build [--force]
+
+Flags: -gencode arch=compute_100a,code=sm_100a -lineinfo -O3, and the
+arithmetic contract of DESIGN.md (A.1-A.3): -fmad=false (no FMA contraction),
+IEEE division/sqrt (-prec-div=true -prec-sqrt=true), denormals preserved
+(-ftz=false); host code with -ffp-contract=off.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libvsr.so")
+SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu"]
+HEADERS = ["layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
+        if cand and (os.path.isabs(cand) and os.path.exists(cand) or not os.path.isabs(cand)):
+            return cand
+    return "nvcc"
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(ROOT, "include", "vsr.h"))
+    deps.append(os.path.abspath(__file__))
+    lib_t = os.path.getmtime(LIB)
+    return any(os.path.getmtime(d) > lib_t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    tmp = LIB + ".tmp"
+    cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler",
+           "-ffp-contract=off", *ARCH, "-lineinfo", "-fmad=false", "-prec-div=true",
+           "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
+           "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lcudart"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError("nvcc failed building libvsr.so")
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+        f.write(res.stderr)
+    if verbose:
+        sys.stderr.write(res.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,726 @@
+// api.cpp — the C ABI declared in include/vsr.h.
+//
+// Host-side responsibilities: argument validation, scene ingest (SPEC
+// S:433-436), BVH build + upload (untimed setup), export/import of the
+// flattened structure for multi-GPU replication, and the host dispatch that
+// maps (query, intersector) to ONE kernel instantiation per call (PAPER.md:
+// 74-78: the choice is made once, outside the innermost loop).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/vsr.h"
+#include "builder.hpp"
+#include "layout.hpp"
+#include "trace.hpp"
+
+using namespace vsr;
+
+namespace {
+thread_local std::string g_err;
+
+vsr_status fail(vsr_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+vsr_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(VSR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) err = cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+struct HostTexture {
+  uint32_t w, h;
+  std::vector<uint32_t> texels;   // packed RGBA8, alpha in the top byte
+};
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Copy `bytes` from src (host or device memory) into host memory.
+cudaError_t to_host(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;
+  cudaPointerAttributes at{};
+  cudaError_t e = cudaPointerGetAttributes(&at, src);
+  if (e != cudaSuccess || at.type == cudaMemoryTypeUnregistered || at.type == cudaMemoryTypeHost) {
+    cudaGetLastError();   // clear a sticky "no device" / invalid value from the query
+    std::memcpy(dst, src, bytes);
+    return cudaSuccess;
+  }
+  return cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+}
+
+}  // namespace
+
+struct vsr_scene {
+  int device = 0;
+  // ---- host copies (vsr_scene_create) ----
+  uint32_t num_tris_input = 0;
+  std::vector<float> vertices, texcoords;
+  std::vector<uint32_t> tri_tex;
+  std::vector<HostTexture> textures;
+  bool has_texcoords = false;
+  // ---- device state (vsr_bvh_build / vsr_scene_import) ----
+  bool built = false;
+  // host-only scenes (device == -1) keep the flattened arrays here instead
+  bool host_built = false;
+  HostBvh host_bvh;
+  std::vector<TexDesc> host_descs;
+  std::vector<uint32_t> host_pool;
+  DevScene dev{};
+  PairNode* d_nodes = nullptr;
+  Tri* d_tris = nullptr;
+  Side* d_sides = nullptr;
+  TexDesc* d_texdescs = nullptr;
+  uint32_t* d_texels = nullptr;
+  uint64_t num_texels = 0;
+  vsr_stats stats{};
+  // ---- vsr_trace_host staging ----
+  std::mutex stage_mu;
+  static constexpr int kSlots = 3;
+  uint64_t stage_cap = 0;   // rays per slot
+  float4* d_in[kSlots] = {};
+  float4* d_out[kSlots] = {};
+  uint4* d_cnt[kSlots] = {};
+  cudaStream_t streams[kSlots] = {};
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_done[kSlots] = {};
+  void* fn_cache[4] = {};
+  bool fn_cached[4] = {};
+
+  void free_device() {
+    cudaFree(d_nodes);
+    cudaFree(d_tris);
+    cudaFree(d_sides);
+    cudaFree(d_texdescs);
+    cudaFree(d_texels);
+    d_nodes = nullptr;
+    d_tris = nullptr;
+    d_sides = nullptr;
+    d_texdescs = nullptr;
+    d_texels = nullptr;
+    built = false;
+  }
+  void free_stage() {
+    for (int s = 0; s < kSlots; ++s) {
+      cudaFree(d_in[s]);
+      cudaFree(d_out[s]);
+      cudaFree(d_cnt[s]);
+      d_in[s] = nullptr;
+      d_out[s] = nullptr;
+      d_cnt[s] = nullptr;
+      if (streams[s]) cudaStreamDestroy(streams[s]);
+      if (ev_done[s]) cudaEventDestroy(ev_done[s]);
+      streams[s] = nullptr;
+      ev_done[s] = nullptr;
+    }
+    if (ev_start) cudaEventDestroy(ev_start);
+    ev_start = nullptr;
+    stage_cap = 0;
+  }
+};
+
+namespace {
+
+template <class T>
+vsr_status dev_upload(T** dst, const void* src, size_t count, const char* what) {
+  size_t bytes = count * sizeof(T);
+  if (bytes == 0) bytes = sizeof(T);   // keep a valid pointer for empty arrays
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), bytes);
+  if (e != cudaSuccess) {
+    *dst = nullptr;
+    return e == cudaErrorMemoryAllocation ? fail(VSR_ERR_OOM, std::string("cudaMalloc ") + what)
+                                          : cuda_fail(e, what);
+  }
+  if (count) {
+    e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(e, what);
+  }
+  return VSR_OK;
+}
+
+// Upload flattened arrays (host or device sources) and fill scene->dev.
+vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const float* root_hi,
+                  const void* nodes, uint32_t num_nodes, const void* tris, const void* sides,
+                  uint32_t num_tris, const void* texdescs, uint32_t num_textures,
+                  const void* texels, uint64_t num_texels) {
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  s->free_device();
+  vsr_status st;
+  if ((st = dev_upload(&s->d_nodes, nodes, num_nodes, "nodes")) != VSR_OK) return st;
+  if ((st = dev_upload(&s->d_tris, tris, num_tris, "triangles")) != VSR_OK) return st;
+  if ((st = dev_upload(&s->d_sides, sides, num_tris, "sidecars")) != VSR_OK) return st;
+  if ((st = dev_upload(&s->d_texdescs, texdescs, num_textures, "texdescs")) != VSR_OK) return st;
+  if ((st = dev_upload(&s->d_texels, texels, num_texels, "texels")) != VSR_OK) return st;
+  s->num_texels = num_texels;
+  DevScene& d = s->dev;
+  d.nodes = s->d_nodes;
+  d.tris = s->d_tris;
+  d.sides = s->d_sides;
+  d.texdescs = s->d_texdescs;
+  d.texels = s->d_texels;
+  d.root_ref = root_ref;
+  for (int a = 0; a < 3; ++a) {
+    d.root_lo[a] = root_lo[a];
+    d.root_hi[a] = root_hi[a];
+  }
+  d.num_nodes = num_nodes;
+  d.num_tris = num_tris;
+  d.num_textures = num_textures;
+  s->stats.num_nodes = num_nodes;
+  s->stats.num_tris = num_tris;
+  s->stats.num_textures = num_textures;
+  s->stats.num_texels = num_texels;
+  s->stats.device_bytes = (uint64_t)num_nodes * 64 + (uint64_t)num_tris * 80 +
+                          (uint64_t)num_textures * 16 + num_texels * 4;
+  s->built = true;
+  s->stats.built = 1;
+  return VSR_OK;
+}
+
+// smallest a8 in [0,255] with (float)a8 / 255.0f >= thr, evaluated with the
+// exact fp32 expression of the listing (reading A7); 256 = none.
+uint32_t alpha_min_a8(float thr) {
+  for (uint32_t a = 0; a < 256; ++a)
+    if ((float)a / 255.0f >= thr) return a;
+  return 256;
+}
+
+bool valid_isect(int k) {
+  switch (k) {
+    case VSR_ISECT_NONE:
+    case VSR_ISECT_DEFAULT:
+    case VSR_ISECT_ALPHA_TEXTURE:
+    case VSR_ISECT_ALPHA_PROCEDURAL:
+    case VSR_ISECT_COUNT:
+    case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+    case VSR_ISECT_RUNTIME_SWITCH_DEFAULT:
+    case VSR_ISECT_RUNTIME_SWITCH_ALPHA_TEXTURE:
+    case VSR_ISECT_RUNTIME_SWITCH_ALPHA_PROCEDURAL:
+    case VSR_ISECT_RUNTIME_FNPTR_DEFAULT:
+    case VSR_ISECT_RUNTIME_FNPTR_ALPHA_TEXTURE:
+    case VSR_ISECT_RUNTIME_FNPTR_ALPHA_PROCEDURAL: return true;
+    default: return false;
+  }
+}
+
+bool needs_counts(int k) { return k == VSR_ISECT_COUNT || k == VSR_ISECT_COUNT_ALPHA_TEXTURE; }
+
+vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
+                       const vsr_isect_params* params, TraceParams& p) {
+  if (query != VSR_QUERY_CLOSEST && query != VSR_QUERY_ANY)
+    return fail(VSR_ERR_INVALID_ARG, "invalid query");
+  if (!valid_isect(isect)) return fail(VSR_ERR_INVALID_ARG, "invalid intersector kind");
+  vsr_isect_params ip{0.01f, 8u};
+  if (params) ip = *params;
+  if (std::isnan(ip.alpha_threshold)) return fail(VSR_ERR_INVALID_ARG, "alpha_threshold is NaN");
+  if (ip.checker_freq < 1u || ip.checker_freq > (1u << 24))
+    return fail(VSR_ERR_INVALID_ARG, "checker_freq must be in [1, 2^24]");
+  std::memset(&p, 0, sizeof p);
+  p.scene = s->dev;
+  p.data.sides = s->d_sides;
+  p.data.descs = s->d_texdescs;
+  p.data.texels = s->d_texels;
+  p.data.a_min = alpha_min_a8(ip.alpha_threshold);
+  p.data.fm = (float)ip.checker_freq;
+  int kind = 0;
+  if (isect >= 200) kind = isect - 200;
+  else if (isect >= 100) kind = isect - 100;
+  p.runtime_kind = kind;
+  if (isect >= 200 && kind != 1) {
+    if (!s->fn_cached[kind]) {
+      DeviceGuard g(s->device);
+      cudaError_t e = filter_fn_pointer(kind, &s->fn_cache[kind]);
+      if (e != cudaSuccess) return cuda_fail(e, "filter function pointer");
+      s->fn_cached[kind] = true;
+    }
+    p.filter_fn = s->fn_cache[kind];
+  }
+  return VSR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+uint32_t vsr_abi_version(void) { return VSR_ABI_VERSION; }
+
+const char* vsr_last_error(void) { return g_err.c_str(); }
+
+uint64_t vsr_launch_count(void) { return launch_count(); }
+
+vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out) {
+  g_err.clear();
+  if (!desc || !out) return fail(VSR_ERR_INVALID_ARG, "NULL desc or out");
+  *out = nullptr;
+  const uint32_t n = desc->num_tris;
+  if (n > 0 && !desc->vertices) return fail(VSR_ERR_INVALID_ARG, "vertices is NULL");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 &&
+      (desc->device < -1 || desc->device >= ndev))
+    return fail(VSR_ERR_INVALID_ARG, "device ordinal out of range");
+  for (size_t i = 0; i < (size_t)n * 9; ++i)
+    if (!std::isfinite(desc->vertices[i]))
+      return fail(VSR_ERR_NONFINITE, "non-finite vertex coordinate at triangle " +
+                                         std::to_string(i / 9));
+  if (desc->texcoords) {
+    for (size_t i = 0; i < (size_t)n * 6; ++i) {
+      float v = desc->texcoords[i];
+      if (!std::isfinite(v))
+        return fail(VSR_ERR_NONFINITE, "non-finite texcoord at triangle " + std::to_string(i / 6));
+      if (std::fabs(v) > 1024.0f)
+        return fail(VSR_ERR_INVALID_ARG, "|texcoord| > 1024 at triangle " + std::to_string(i / 6));
+    }
+  }
+  const uint32_t ntex = desc->num_textures;
+  if (ntex > 0 && !desc->textures) return fail(VSR_ERR_INVALID_ARG, "textures is NULL");
+  for (uint32_t k = 0; k < ntex; ++k) {
+    const vsr_texture_desc& t = desc->textures[k];
+    if (t.width < 1 || t.height < 1 || t.width > 65536 || t.height > 65536 || !t.rgba8)
+      return fail(VSR_ERR_INVALID_ARG, "texture " + std::to_string(k) + " has a bad size/pointer");
+  }
+  const uint32_t eff_tex = ntex ? ntex : 1u;
+  if (desc->geom_texture) {
+    for (uint32_t g = 0; g < desc->num_geoms; ++g)
+      if (desc->geom_texture[g] >= eff_tex)
+        return fail(VSR_ERR_INVALID_ARG, "geom_texture[" + std::to_string(g) + "] out of range");
+  }
+  vsr_scene* s = new (std::nothrow) vsr_scene();
+  if (!s) return fail(VSR_ERR_OOM, "scene allocation");
+  try {
+    s->device = desc->device;
+    s->num_tris_input = n;
+    s->vertices.assign(desc->vertices, desc->vertices + (size_t)n * 9);
+    s->has_texcoords = desc->texcoords != nullptr;
+    if (desc->texcoords) s->texcoords.assign(desc->texcoords, desc->texcoords + (size_t)n * 6);
+    s->tri_tex.resize(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      uint32_t g = desc->geom_ids ? desc->geom_ids[i] : 0u;
+      uint32_t t;
+      if (desc->geom_texture) {
+        if (g >= desc->num_geoms) {
+          delete s;
+          return fail(VSR_ERR_INVALID_ARG, "geom_id of triangle " + std::to_string(i) +
+                                               " >= num_geoms");
+        }
+        t = desc->geom_texture[g];
+      } else {
+        t = ntex ? g : 0u;
+      }
+      if (t >= eff_tex) {
+        delete s;
+        return fail(VSR_ERR_INVALID_ARG, "texture index of triangle " + std::to_string(i) +
+                                             " out of range");
+      }
+      s->tri_tex[i] = t;
+    }
+    if (ntex == 0) {
+      s->textures.push_back(HostTexture{1, 1, {0xFFFFFFFFu}});   // implicit opaque white
+    } else {
+      s->textures.resize(ntex);
+      for (uint32_t k = 0; k < ntex; ++k) {
+        const vsr_texture_desc& t = desc->textures[k];
+        HostTexture& h = s->textures[k];
+        h.w = t.width;
+        h.h = t.height;
+        size_t cnt = (size_t)t.width * t.height;
+        h.texels.resize(cnt);
+        const uint8_t* p = t.rgba8;
+        for (size_t q = 0; q < cnt; ++q)
+          h.texels[q] = (uint32_t)p[4 * q] | ((uint32_t)p[4 * q + 1] << 8) |
+                        ((uint32_t)p[4 * q + 2] << 16) | ((uint32_t)p[4 * q + 3] << 24);
+      }
+    }
+  } catch (const std::bad_alloc&) {
+    delete s;
+    return fail(VSR_ERR_OOM, "host copy of the scene");
+  }
+  s->stats.num_tris_input = n;
+  *out = s;
+  return VSR_OK;
+}
+
+vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  if (s->vertices.empty() && s->num_tris_input == 0 && s->built)
+    return fail(VSR_ERR_INVALID_ARG, "imported scenes cannot be rebuilt");
+  vsr_build_params prm{4u, 16u, 1.0f, 1.0f};
+  if (params) prm = *params;
+  if (prm.max_leaf_size < 1 || prm.max_leaf_size > kMaxLeafSize)
+    return fail(VSR_ERR_INVALID_ARG, "max_leaf_size must be in [1, 32]");
+  if (prm.sah_bins < 2 || prm.sah_bins > 256)
+    return fail(VSR_ERR_INVALID_ARG, "sah_bins must be in [2, 256]");
+  if (!(prm.traversal_cost >= 0.0f) || !(prm.intersection_cost > 0.0f))
+    return fail(VSR_ERR_INVALID_ARG, "costs must be finite, intersection_cost > 0");
+  if (s->num_tris_input == 0) return fail(VSR_ERR_EMPTY_SCENE, "empty scene: zero triangles");
+  auto t0 = std::chrono::steady_clock::now();
+  HostBvh hb;
+  std::string err;
+  BuildInput in{s->vertices.data(), s->num_tris_input,
+                s->has_texcoords ? s->texcoords.data() : nullptr, s->tri_tex.data()};
+  vsr_status st;
+  try {
+    st = build_bvh(in, prm, hb, err);
+  } catch (const std::bad_alloc&) {
+    return fail(VSR_ERR_OOM, "host BVH build");
+  }
+  if (st != VSR_OK) return fail(st, err);
+  // texture pool
+  std::vector<TexDesc> descs(s->textures.size());
+  uint64_t total = 0;
+  for (size_t k = 0; k < s->textures.size(); ++k) {
+    descs[k].offset = total;
+    descs[k].w = s->textures[k].w;
+    descs[k].h = s->textures[k].h;
+    total += (uint64_t)descs[k].w * descs[k].h;
+  }
+  std::vector<uint32_t> pool(total);
+  for (size_t k = 0; k < s->textures.size(); ++k)
+    std::memcpy(pool.data() + descs[k].offset, s->textures[k].texels.data(),
+                s->textures[k].texels.size() * 4);
+  if (s->device < 0) {
+    // host-only scene: keep the flattened arrays for export (no device copy)
+    s->free_device();
+    s->stats.num_nodes = (uint32_t)hb.nodes.size();
+    s->stats.num_tris = (uint32_t)hb.tris.size();
+    s->stats.num_textures = (uint32_t)descs.size();
+    s->stats.num_texels = total;
+    s->stats.device_bytes = 0;
+    s->stats.built = 1;
+    s->dev.root_ref = hb.root_ref;
+    for (int a = 0; a < 3; ++a) {
+      s->dev.root_lo[a] = hb.root_lo[a];
+      s->dev.root_hi[a] = hb.root_hi[a];
+    }
+    s->dev.num_nodes = s->stats.num_nodes;
+    s->dev.num_tris = s->stats.num_tris;
+    s->dev.num_textures = s->stats.num_textures;
+    s->num_texels = total;
+    s->host_bvh = std::move(hb);
+    s->host_descs = std::move(descs);
+    s->host_pool = std::move(pool);
+    s->host_built = true;
+  } else {
+    st = upload(s, hb.root_ref, hb.root_lo, hb.root_hi, hb.nodes.data(),
+                (uint32_t)hb.nodes.size(), hb.tris.data(), hb.sides.data(),
+                (uint32_t)hb.tris.size(), descs.data(), (uint32_t)descs.size(), pool.data(), total);
+    if (st != VSR_OK) return st;
+  }
+  s->stats.num_degenerate = hb.num_degenerate;
+  s->stats.num_leaves = hb.num_leaves;
+  s->stats.max_depth = hb.max_depth;
+  s->stats.build_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return VSR_OK;
+}
+
+vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                     vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                     vsr_counts* d_counts, void* stream) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  TraceParams p;
+  vsr_status st = make_params(s, query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
+  if (n == 0) return VSR_OK;
+  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  if (!aligned16(d_rays) || !aligned16(d_hits))
+    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  p.rays = reinterpret_cast<const float4*>(d_rays);
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "trace kernel launch");
+  return VSR_OK;
+}
+
+vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_query query,
+                          vsr_isect isect, const vsr_isect_params* params, vsr_hit* h_hits,
+                          vsr_counts* h_counts, void* stream) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  TraceParams p;
+  vsr_status st = make_params(s, query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
+  if (n == 0) return VSR_OK;
+  if (!h_rays || !h_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  const bool cnt = needs_counts(isect);
+  if (cnt && !h_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs counts");
+  std::lock_guard<std::mutex> lk(s->stage_mu);
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  // Chunked pipeline over kSlots streams: chunk c's H2D copy, kernel and D2H
+  // copy run on stream c % kSlots, so copies of one chunk overlap the kernel
+  // of another (copy engines and SMs work concurrently).
+  const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(65536, (n + 7) / 8));
+  cudaError_t e;
+  if (s->stage_cap < chunk || (cnt && !s->d_cnt[0])) {
+    s->free_stage();
+    for (int k = 0; k < vsr_scene::kSlots; ++k) {
+      if ((e = cudaMalloc(&s->d_in[k], chunk * 32)) != cudaSuccess ||
+          (e = cudaMalloc(&s->d_out[k], chunk * 16)) != cudaSuccess ||
+          (e = cudaMalloc(&s->d_cnt[k], chunk * 16)) != cudaSuccess ||
+          (e = cudaStreamCreateWithFlags(&s->streams[k], cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&s->ev_done[k], cudaEventDisableTiming)) != cudaSuccess) {
+        s->free_stage();
+        return cuda_fail(e, "staging allocation");
+      }
+    }
+    if ((e = cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_fail(e, "event");
+    s->stage_cap = chunk;
+  }
+  cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
+  if ((e = cudaEventRecord(s->ev_start, user)) != cudaSuccess) return cuda_fail(e, "event");
+  for (int k = 0; k < vsr_scene::kSlots; ++k)
+    if ((e = cudaStreamWaitEvent(s->streams[k], s->ev_start, 0)) != cudaSuccess)
+      return cuda_fail(e, "stream wait");
+  const char* src = reinterpret_cast<const char*>(h_rays);
+  char* dst = reinterpret_cast<char*>(h_hits);
+  char* cdst = reinterpret_cast<char*>(h_counts);
+  uint64_t c = 0;
+  for (uint64_t b = 0; b < n; b += chunk, ++c) {
+    const int k = (int)(c % vsr_scene::kSlots);
+    const uint64_t m = std::min(chunk, n - b);
+    cudaStream_t ss = s->streams[k];
+    if ((e = cudaMemcpyAsync(s->d_in[k], src + b * 32, m * 32, cudaMemcpyHostToDevice, ss)) !=
+        cudaSuccess)
+      return cuda_fail(e, "H2D rays");
+    p.rays = s->d_in[k];
+    p.hits = s->d_out[k];
+    p.counts = s->d_cnt[k];
+    p.n = m;
+    if ((e = launch_trace(query, isect, p, ss)) != cudaSuccess) return cuda_fail(e, "trace launch");
+    if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
+        cudaSuccess)
+      return cuda_fail(e, "D2H hits");
+    if (cnt && (e = cudaMemcpyAsync(cdst + b * 16, s->d_cnt[k], m * 16, cudaMemcpyDeviceToHost,
+                                    ss)) != cudaSuccess)
+      return cuda_fail(e, "D2H counts");
+  }
+  for (int k = 0; k < vsr_scene::kSlots; ++k) {
+    if ((e = cudaEventRecord(s->ev_done[k], s->streams[k])) != cudaSuccess)
+      return cuda_fail(e, "event");
+    if ((e = cudaStreamWaitEvent(user, s->ev_done[k], 0)) != cudaSuccess)
+      return cuda_fail(e, "stream wait");
+  }
+  if ((e = cudaStreamSynchronize(user)) != cudaSuccess) return cuda_fail(e, "trace (host)");
+  return VSR_OK;
+}
+
+vsr_status vsr_destroy(vsr_scene* s) {
+  g_err.clear();
+  if (!s) return VSR_OK;
+  if (s->device >= 0) {
+    DeviceGuard g(s->device);
+    s->free_stage();
+    s->free_device();
+  }
+  delete s;
+  return VSR_OK;
+}
+
+vsr_status vsr_bvh_export(const vsr_scene* s, vsr_bvh_view* view) {
+  g_err.clear();
+  if (!s || !view) return fail(VSR_ERR_INVALID_ARG, "NULL scene or view");
+  if (!s->built && !s->host_built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH");
+  const DevScene& d = s->dev;
+  view->root_ref = d.root_ref;
+  for (int a = 0; a < 3; ++a) {
+    view->root_lo[a] = d.root_lo[a];
+    view->root_hi[a] = d.root_hi[a];
+  }
+  view->num_nodes = d.num_nodes;
+  view->num_tris = d.num_tris;
+  view->num_textures = d.num_textures;
+  view->num_texels = s->num_texels;
+  struct Item { void* dst; const void* src; size_t bytes; };
+  if (s->host_built) {
+    // host-only scene: plain host copies (destinations must be host memory)
+    const HostBvh& h = s->host_bvh;
+    const Item items[] = {{view->nodes, h.nodes.data(), (size_t)d.num_nodes * 64},
+                          {view->tris, h.tris.data(), (size_t)d.num_tris * 48},
+                          {view->sides, h.sides.data(), (size_t)d.num_tris * 32},
+                          {view->texdescs, s->host_descs.data(), (size_t)d.num_textures * 16},
+                          {view->texels, s->host_pool.data(), (size_t)s->num_texels * 4}};
+    for (const Item& it : items)
+      if (it.dst && it.bytes) std::memcpy(it.dst, it.src, it.bytes);
+    return VSR_OK;
+  }
+  DeviceGuard g(s->device);
+  const Item items[] = {{view->nodes, s->d_nodes, (size_t)d.num_nodes * 64},
+                        {view->tris, s->d_tris, (size_t)d.num_tris * 48},
+                        {view->sides, s->d_sides, (size_t)d.num_tris * 32},
+                        {view->texdescs, s->d_texdescs, (size_t)d.num_textures * 16},
+                        {view->texels, s->d_texels, (size_t)s->num_texels * 4}};
+  for (const Item& it : items) {
+    if (!it.dst || it.bytes == 0) continue;
+    cudaError_t e = cudaMemcpy(it.dst, it.src, it.bytes, cudaMemcpyDefault);
+    if (e != cudaSuccess) return cuda_fail(e, "export copy");
+  }
+  return VSR_OK;
+}
+
+vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) {
+  g_err.clear();
+  if (!v || !out) return fail(VSR_ERR_INVALID_ARG, "NULL view or out");
+  *out = nullptr;
+  if (v->num_tris == 0) return fail(VSR_ERR_EMPTY_SCENE, "imported BVH has no triangles");
+  if (v->num_tris > kMaxTris) return fail(VSR_ERR_UNSUPPORTED, "more than 2^26 triangles");
+  if (!v->tris || !v->sides || (v->num_nodes && !v->nodes) || !v->texdescs || !v->texels ||
+      v->num_textures == 0)
+    return fail(VSR_ERR_INVALID_ARG, "NULL array in view (or zero textures)");
+  int ndev = 0;
+  if (device < -1) return fail(VSR_ERR_INVALID_ARG, "device ordinal out of range");
+  if (device >= 0 && cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0 && device >= ndev)
+    return fail(VSR_ERR_INVALID_ARG, "device ordinal out of range");
+  // Host copies for validation (the source may be device memory).
+  std::vector<PairNode> nodes(v->num_nodes);
+  std::vector<Side> sides(v->num_tris);
+  std::vector<TexDesc> descs(v->num_textures);
+  {
+    cudaError_t e;
+    if (v->num_nodes && (e = to_host(nodes.data(), v->nodes, nodes.size() * 64)) != cudaSuccess)
+      return cuda_fail(e, "import nodes");
+    if ((e = to_host(sides.data(), v->sides, sides.size() * 32)) != cudaSuccess)
+      return cuda_fail(e, "import sidecars");
+    if ((e = to_host(descs.data(), v->texdescs, descs.size() * 16)) != cudaSuccess)
+      return cuda_fail(e, "import texdescs");
+  }
+  for (uint32_t k = 0; k < v->num_textures; ++k) {
+    const TexDesc& t = descs[k];
+    if (t.w < 1 || t.h < 1 || t.w > 65536 || t.h > 65536 ||
+        t.offset + (uint64_t)t.w * t.h > v->num_texels)
+      return fail(VSR_ERR_INVALID_ARG, "texture descriptor " + std::to_string(k) + " out of range");
+  }
+  for (uint32_t k = 0; k < v->num_tris; ++k)
+    if (sides[k].tex >= v->num_textures)
+      return fail(VSR_ERR_INVALID_ARG, "sidecar " + std::to_string(k) + " texture out of range");
+  // Structure: reachable refs in range, every triangle in exactly one leaf, depth <= 64.
+  std::vector<uint8_t> seen_tri(v->num_tris, 0), seen_node(v->num_nodes, 0);
+  struct Item { uint32_t ref; uint32_t depth; };
+  std::vector<Item> st{{v->root_ref, 0}};
+  uint32_t max_depth = 0, leaves = 0;
+  while (!st.empty()) {
+    Item it = st.back();
+    st.pop_back();
+    if (it.depth > (uint32_t)kMaxStack)
+      return fail(VSR_ERR_BVH_TOO_DEEP, "imported BVH deeper than 64 levels");
+    max_depth = std::max(max_depth, it.depth);
+    if (it.ref & kLeafBit) {
+      uint32_t first = it.ref & kLeafFirstMask;
+      uint32_t cnt = ((it.ref >> kLeafCountShift) & 31u) + 1u;
+      if ((uint64_t)first + cnt > v->num_tris)
+        return fail(VSR_ERR_INVALID_ARG, "leaf range out of bounds");
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        if (seen_tri[k]) return fail(VSR_ERR_INVALID_ARG, "triangle referenced by two leaves");
+        seen_tri[k] = 1;
+      }
+      ++leaves;
+      continue;
+    }
+    if (it.ref >= v->num_nodes) return fail(VSR_ERR_INVALID_ARG, "node ref out of range");
+    if (seen_node[it.ref]) return fail(VSR_ERR_INVALID_ARG, "node reachable twice (not a tree)");
+    seen_node[it.ref] = 1;
+    st.push_back({nodes[it.ref].ref[1], it.depth + 1});
+    st.push_back({nodes[it.ref].ref[0], it.depth + 1});
+  }
+  for (uint32_t k = 0; k < v->num_tris; ++k)
+    if (!seen_tri[k]) return fail(VSR_ERR_INVALID_ARG, "triangle not referenced by any leaf");
+  vsr_scene* s = new (std::nothrow) vsr_scene();
+  if (!s) return fail(VSR_ERR_OOM, "scene allocation");
+  s->device = device;
+  if (device < 0) {
+    // host-only import (e.g. a CPU rank relaying a broadcast): keep host copies
+    try {
+      HostBvh& h = s->host_bvh;
+      h.nodes = std::move(nodes);
+      h.tris.resize(v->num_tris);
+      h.sides = std::move(sides);
+      s->host_descs = std::move(descs);
+      s->host_pool.resize(v->num_texels);
+      cudaError_t e;
+      if ((e = to_host(h.tris.data(), v->tris, (size_t)v->num_tris * 48)) != cudaSuccess ||
+          (e = to_host(s->host_pool.data(), v->texels, (size_t)v->num_texels * 4)) != cudaSuccess) {
+        delete s;
+        return cuda_fail(e, "import copy");
+      }
+    } catch (const std::bad_alloc&) {
+      delete s;
+      return fail(VSR_ERR_OOM, "host import");
+    }
+    DevScene& d = s->dev;
+    d.root_ref = v->root_ref;
+    for (int a = 0; a < 3; ++a) {
+      d.root_lo[a] = v->root_lo[a];
+      d.root_hi[a] = v->root_hi[a];
+    }
+    d.num_nodes = v->num_nodes;
+    d.num_tris = v->num_tris;
+    d.num_textures = v->num_textures;
+    s->num_texels = v->num_texels;
+    s->host_built = true;
+    s->stats.built = 1;
+    s->stats.num_nodes = v->num_nodes;
+    s->stats.num_tris = v->num_tris;
+    s->stats.num_textures = v->num_textures;
+    s->stats.num_texels = v->num_texels;
+    s->stats.num_tris_input = v->num_tris;
+    s->stats.num_leaves = leaves;
+    s->stats.max_depth = max_depth;
+    *out = s;
+    return VSR_OK;
+  }
+  vsr_status rc = upload(s, v->root_ref, v->root_lo, v->root_hi, v->nodes, v->num_nodes, v->tris,
+                         v->sides, v->num_tris, v->texdescs, v->num_textures, v->texels,
+                         v->num_texels);
+  if (rc != VSR_OK) {
+    vsr_destroy(s);
+    return rc;
+  }
+  s->stats.num_tris_input = v->num_tris;
+  s->stats.num_leaves = leaves;
+  s->stats.max_depth = max_depth;
+  *out = s;
+  return VSR_OK;
+}
+
+vsr_status vsr_scene_stats(const vsr_scene* s, vsr_stats* out) {
+  g_err.clear();
+  if (!s || !out) return fail(VSR_ERR_INVALID_ARG, "NULL scene or out");
+  *out = s->stats;
+  return VSR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,31 @@
+// builder.hpp — host BVH builder interface (product side).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/vsr.h"
+#include "layout.hpp"
+
+namespace vsr {
+
+struct BuildInput {
+  const float* vertices;    // 9 per triangle
+  uint32_t num_tris;
+  const float* texcoords;   // 6 per triangle or nullptr
+  const uint32_t* tri_tex;  // resolved texture index per triangle
+};
+
+struct HostBvh {
+  uint32_t root_ref = 0;
+  float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
+  std::vector<PairNode> nodes;
+  std::vector<Tri> tris;
+  std::vector<Side> sides;
+  uint32_t max_depth = 0, num_leaves = 0, num_degenerate = 0;
+};
+
+vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
+                     std::string& err);
+
+}  // namespace vsr

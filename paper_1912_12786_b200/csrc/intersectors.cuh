@@ -1,0 +1,252 @@
+// intersectors.cuh — the paper's intersector API on the device.
+//
+// PAPER.md §3.1: the customization point `intersect(ray, prim) -> hit_record`
+// is the default behaviour; a custom intersector derives
+// from `basic_intersector<Derived>` (CRTP), re-exports the
+// base operator() and overrides the hook it wants.  The
+// traversal calls the intersector at both call sites — box and primitive —
+// (PAPER.md:248-260), and extra box arguments such as the inverse ray
+// direction are forwarded untouched (PAPER.md:337-376 variadic pass-through).
+//
+// Everything here is resolved at compile time: a kernel instantiated with an
+// intersector contains exactly that intersector's code and nothing else
+// (PAPER.md:83-89), and the default intersector inlines to the same
+// instructions as calling `intersect` directly.
+//
+// Arithmetic follows DESIGN.md §"Arithmetic contract" (IEEE fp32, no FMA: the
+// translation unit is compiled with -fmad=false, IEEE division).
+#pragma once
+#include <cstdint>
+#include <type_traits>
+
+#include "layout.hpp"
+
+namespace vsr {
+
+struct RayCtx {
+  float ox, oy, oz, tmin;
+  float dx, dy, dz;
+  float ix, iy, iz;   // guarded reciprocal direction (reading A20)
+};
+
+struct Aabb {
+  float lx, ly, lz, hx, hy, hz;
+};
+
+// Triangle as loaded: v0 (+prim id bits in w), e1, e2 (SPEC S:47 v0/e1/e2).
+struct TriData {
+  float4 a, b, c;
+};
+
+// hit_record<Ray, primitive<unsigned>>: hit flag, t, barycentrics
+// and the primitive's position k in the leaf-ordered arrays (the sidecar index;
+// PAPER.md:306-308 reads tex_coords[prim_id*3 + i], reading A9).
+struct hit_record {
+  bool hit;
+  float t, u, v;
+  uint32_t k;
+};
+
+__device__ __forceinline__ float4 ldg4(const void* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// ---------------------------------------------------------------------------
+// Default primitive tests (the `intersect` customization points).
+// ---------------------------------------------------------------------------
+
+// Ray/AABB slab test with the caller-supplied inverse direction (the "special
+// interface" of PAPER.md:371-376), clipped to [tmin, best_t]; tf widened by
+// (1 + 2*gamma_3) (reading A23).  min/max are exact, so their order is free.
+__device__ __forceinline__ bool intersect(const RayCtx& r, const Aabb& b, float best_t,
+                                          float& tn) {
+  const float t0x = (b.lx - r.ox) * r.ix, t1x = (b.hx - r.ox) * r.ix;
+  const float t0y = (b.ly - r.oy) * r.iy, t1y = (b.hy - r.oy) * r.iy;
+  const float t0z = (b.lz - r.oz) * r.iz, t1z = (b.hz - r.oz) * r.iz;
+  const float n = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), r.tmin));
+  float f = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
+  f = fminf(f, best_t);
+  tn = n;
+  return n <= f;
+}
+
+// Ray/triangle: Möller–Trumbore in textbook order (DESIGN.md
+// A.1), no culling, |det| < 1e-12 -> miss, t in [tmin, tmax_cur] inclusive.
+__device__ __forceinline__ hit_record intersect(const RayCtx& r, const TriData& tri, uint32_t k,
+                                                float tmax_cur) {
+  hit_record hr;
+  hr.k = k;
+  const float e1x = tri.b.x, e1y = tri.b.y, e1z = tri.b.z;
+  const float e2x = tri.c.x, e2y = tri.c.y, e2z = tri.c.z;
+  // p = cross(d, e2)
+  const float px = r.dy * e2z - r.dz * e2y;
+  const float py = r.dz * e2x - r.dx * e2z;
+  const float pz = r.dx * e2y - r.dy * e2x;
+  const float det = (e1x * px + e1y * py) + e1z * pz;
+  const float inv = 1.0f / det;
+  const float sx = r.ox - tri.a.x, sy = r.oy - tri.a.y, sz = r.oz - tri.a.z;
+  const float u = ((sx * px + sy * py) + sz * pz) * inv;
+  // q = cross(s, e1)
+  const float qx = sy * e1z - sz * e1y;
+  const float qy = sz * e1x - sx * e1z;
+  const float qz = sx * e1y - sy * e1x;
+  const float v = ((r.dx * qx + r.dy * qy) + r.dz * qz) * inv;
+  const float t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
+  hr.t = t;
+  hr.u = u;
+  hr.v = v;
+  hr.hit = (fabsf(det) >= 1e-12f) && (u >= 0.0f) && (u <= 1.0f) && (v >= 0.0f) &&
+           (u + v <= 1.0f) && (t >= r.tmin) && (t <= tmax_cur);
+  return hr;
+}
+
+// ---------------------------------------------------------------------------
+// basic_intersector<Derived>: both hooks forward.
+// ---------------------------------------------------------------------------
+template <class Derived>
+struct basic_intersector {
+  static constexpr bool kCounts = false;
+  template <class... Args>
+  __device__ __forceinline__ bool operator()(const RayCtx& r, const Aabb& b, Args&&... args) {
+    return intersect(r, b, static_cast<Args&&>(args)...);
+  }
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    return intersect(r, t, k, tmax_cur);
+  }
+  __device__ __forceinline__ uint32_t lookups() const { return 0u; }
+};
+
+// Tag for the default overload without an intersector:
+// the traversal calls `intersect` itself.
+struct no_intersector {
+  static constexpr bool kCounts = false;
+  __device__ __forceinline__ uint32_t lookups() const { return 0u; }
+};
+
+// DEFAULT: a user intersector that overrides nothing.
+struct default_intersector : basic_intersector<default_intersector> {
+  using basic_intersector<default_intersector>::operator();
+};
+
+// nearest + wrap addressing on the integer texel index (reading A6)
+__device__ __forceinline__ uint32_t wrap_texel(float x, uint32_t n) {
+  const int i = (int)floorf(x * (float)n);
+  if ((n & (n - 1u)) == 0u) return (uint32_t)i & (n - 1u);
+  const int m = (int)n;
+  return (uint32_t)(((i % m) + m) % m);
+}
+
+// The §4 alpha-mask filter body: lerp the three texcoords with (u, v), tex2D,
+// test alpha against the threshold.
+__device__ __forceinline__ bool alpha_keep(const IsectData& d, uint32_t k, float u, float v) {
+  const float4 s0 = ldg4(d.sides + k);
+  const float4 s1 = ldg4(reinterpret_cast<const float4*>(d.sides + k) + 1);
+  const float w = (1.0f - u) - v;
+  const float s = (w * s0.x + u * s0.z) + v * s1.x;
+  const float t = (w * s0.y + u * s0.w) + v * s1.y;
+  const uint4 td = __ldg(reinterpret_cast<const uint4*>(d.descs + __float_as_uint(s1.z)));
+  const uint64_t off = (uint64_t)td.x | ((uint64_t)td.y << 32);
+  const uint32_t i = wrap_texel(s, td.z);
+  const uint32_t j = wrap_texel(t, td.w);
+  const uint32_t texel = __ldg(d.texels + off + (uint64_t)j * td.z + i);
+  return (texel >> 24) >= d.a_min;
+}
+
+// §4 procedural mask, read as a barycentric checkerboard (readings A4/A5).
+__device__ __forceinline__ bool checker_keep(float fm, float u, float v) {
+  const int cu = (int)floorf(u * fm);
+  const int cv = (int)floorf(v * fm);
+  return ((cu + cv) & 1) == 0;
+}
+
+// ALPHA_TEXTURE: the §4 listing.  Only the triangle hook is
+// overridden; the box hook is inherited (SPEC S:226 design decision).
+struct alpha_texture_intersector : basic_intersector<alpha_texture_intersector> {
+  using basic_intersector<alpha_texture_intersector>::operator();
+  IsectData d;
+  uint32_t n_lookups = 0;
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) {   // look up only on a geometric hit (reading A3)
+      ++n_lookups;
+      hr.hit &= alpha_keep(d, hr.k, hr.u, hr.v);
+    }
+    return hr;
+  }
+  __device__ __forceinline__ uint32_t lookups() const { return n_lookups; }
+};
+
+// ALPHA_PROCEDURAL.
+struct alpha_procedural_intersector : basic_intersector<alpha_procedural_intersector> {
+  using basic_intersector<alpha_procedural_intersector>::operator();
+  float fm;
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) hr.hit &= checker_keep(fm, hr.u, hr.v);
+    return hr;
+  }
+};
+
+// bvh_costs: intercept and count both hooks, then forward.
+// Stacked on any other intersector (Inner), the counts are those of Inner's
+// traversal; COUNT uses the default one, as in the listing.
+template <class Inner>
+struct cost_intersector : Inner {
+  static constexpr bool kCounts = true;
+  uint32_t num_boxes = 0;
+  uint32_t num_tris = 0;
+  template <class... Args>
+  __device__ __forceinline__ bool operator()(const RayCtx& r, const Aabb& b, Args&&... args) {
+    ++num_boxes;
+    return Inner::operator()(r, b, static_cast<Args&&>(args)...);
+  }
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    ++num_tris;
+    return Inner::operator()(r, t, k, tmax_cur);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Measurement controls (never a default path): the run-time alternatives the
+// paper contrasts with (Embree intersection filter / OptiX
+// any-hit program).  Same traversal; the filter is chosen while tracing.
+// ---------------------------------------------------------------------------
+enum : int { kFilterDefault = 1, kFilterAlphaTex = 2, kFilterAlphaProc = 3 };
+
+struct runtime_switch_intersector : basic_intersector<runtime_switch_intersector> {
+  using basic_intersector<runtime_switch_intersector>::operator();
+  IsectData d;
+  int kind;
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) {
+      switch (kind) {
+        case kFilterAlphaTex: hr.hit &= alpha_keep(d, hr.k, hr.u, hr.v); break;
+        case kFilterAlphaProc: hr.hit &= checker_keep(d.fm, hr.u, hr.v); break;
+        default: break;
+      }
+    }
+    return hr;
+  }
+};
+
+typedef bool (*filter_fn_t)(const IsectData*, uint32_t, float, float);
+
+struct runtime_fnptr_intersector : basic_intersector<runtime_fnptr_intersector> {
+  using basic_intersector<runtime_fnptr_intersector>::operator();
+  IsectData d;
+  filter_fn_t fn;   // nullptr == no filter registered
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit && fn != nullptr) hr.hit &= fn(&d, hr.k, hr.u, hr.v);
+    return hr;
+  }
+};
+
+}  // namespace vsr

@@ -1,0 +1,80 @@
+// layout.hpp — device/export data layout shared by the host builder, the C ABI
+// and the trace kernels (product side only; the oracle re-declares it from
+// DESIGN.md and never includes this file).
+//
+// All arrays are 16-B aligned AoS records sized for 128-bit loads:
+//   PairNode 64 B  = 4 x LDG.128   (both children's boxes + refs: one node
+//                                   visit tests two boxes)
+//   Tri      48 B  = 3 x LDG.128   (v0 + precomputed edges)
+//   Side     32 B  = 2 x LDG.128   (alpha sidecar)
+//   TexDesc  16 B
+#pragma once
+#include <cstdint>
+
+namespace vsr {
+
+constexpr uint32_t kLeafBit = 0x80000000u;
+constexpr uint32_t kLeafFirstMask = 0x03FFFFFFu;  // 26 bits
+constexpr uint32_t kLeafCountShift = 26;
+constexpr uint32_t kMaxLeafSize = 32;
+constexpr uint32_t kMaxTris = 1u << 26;
+constexpr int kMaxStack = 64;
+
+struct alignas(16) PairNode {
+  float lo0[3], hi0[3], lo1[3], hi1[3];
+  uint32_t ref[2];
+  uint32_t pad[2];
+};
+static_assert(sizeof(PairNode) == 64, "PairNode must be 64 B");
+
+struct alignas(16) Tri {
+  float v0[3];
+  uint32_t prim;
+  float e1[3];
+  uint32_t pad1;
+  float e2[3];
+  uint32_t pad2;
+};
+static_assert(sizeof(Tri) == 48, "Tri must be 48 B");
+
+struct alignas(16) Side {
+  float uv[6];
+  uint32_t tex;
+  uint32_t pad;
+};
+static_assert(sizeof(Side) == 32, "Side must be 32 B");
+
+struct alignas(16) TexDesc {
+  uint64_t offset;
+  uint32_t w, h;
+};
+static_assert(sizeof(TexDesc) == 16, "TexDesc must be 16 B");
+
+inline uint32_t make_leaf(uint32_t first, uint32_t count) {
+  return kLeafBit | ((count - 1u) << kLeafCountShift) | first;
+}
+
+// Device view of a built scene, passed by value in the kernel parameter space.
+struct DevScene {
+  const PairNode* nodes;
+  const Tri* tris;
+  const Side* sides;
+  const TexDesc* texdescs;
+  const uint32_t* texels;
+  uint32_t root_ref;
+  float root_lo[3], root_hi[3];
+  uint32_t num_nodes, num_tris, num_textures;
+};
+
+// Scene data the mask intersectors read (their "member variables",
+// PAPER.md:286-288 "stores a pointer to the texture and texture coordinate
+// lists").
+struct IsectData {
+  const Side* sides;
+  const TexDesc* descs;
+  const uint32_t* texels;
+  uint32_t a_min;   // smallest a8 with (float)a8/255.0f >= threshold (exact, host-derived)
+  float fm;         // checker frequency M as float
+};
+
+}  // namespace vsr

@@ -1,0 +1,28 @@
+// trace.hpp — host-visible launch interface of the trace kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/vsr.h"
+#include "layout.hpp"
+
+namespace vsr {
+
+// Kernel parameters (passed by value: they live in the constant parameter bank).
+struct TraceParams {
+  DevScene scene;
+  IsectData data;
+  const float4* rays;
+  float4* hits;
+  uint4* counts;
+  uint64_t n;
+  int runtime_kind;
+  void* filter_fn;
+};
+
+cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);
+cudaError_t filter_fn_pointer(int kind, void** out);
+uint64_t launch_count();
+
+}  // namespace vsr

@@ -1,0 +1,303 @@
+"""Thin ctypes binding over libvsr.so (include/vsr.h) — argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind ``vsr_trace``; this
+module only converts Python/numpy/torch arguments into the C ABI's plain
+pointers and sizes.  There is no CPU fallback: if ``libvsr.so`` is missing the
+import of :func:`lib` raises.  PyTorch is used for device memory and streams
+only (``torch.Tensor.data_ptr()``, ``torch.cuda.current_stream().cuda_stream``).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvsr.so")
+
+# vsr_status
+OK, ERR_INVALID_ARG, ERR_EMPTY_SCENE, ERR_NONFINITE, ERR_BVH_TOO_DEEP, ERR_NOT_BUILT, \
+    ERR_CUDA, ERR_OOM, ERR_UNSUPPORTED = range(9)
+STATUS_NAMES = ["VSR_OK", "VSR_ERR_INVALID_ARG", "VSR_ERR_EMPTY_SCENE", "VSR_ERR_NONFINITE",
+                "VSR_ERR_BVH_TOO_DEEP", "VSR_ERR_NOT_BUILT", "VSR_ERR_CUDA", "VSR_ERR_OOM",
+                "VSR_ERR_UNSUPPORTED"]
+# vsr_query
+CLOSEST, ANY = 0, 1
+# vsr_isect
+NONE, DEFAULT, ALPHA_TEXTURE, ALPHA_PROCEDURAL, COUNT, COUNT_ALPHA_TEXTURE = range(6)
+RUNTIME_SWITCH_DEFAULT, RUNTIME_SWITCH_ALPHA_TEXTURE, RUNTIME_SWITCH_ALPHA_PROCEDURAL = 101, 102, 103
+RUNTIME_FNPTR_DEFAULT, RUNTIME_FNPTR_ALPHA_TEXTURE, RUNTIME_FNPTR_ALPHA_PROCEDURAL = 201, 202, 203
+ISECT_NAMES = {NONE: "none", DEFAULT: "default", ALPHA_TEXTURE: "alpha_texture",
+               ALPHA_PROCEDURAL: "alpha_procedural", COUNT: "count",
+               COUNT_ALPHA_TEXTURE: "count_alpha_texture",
+               RUNTIME_SWITCH_DEFAULT: "runtime_switch_default",
+               RUNTIME_SWITCH_ALPHA_TEXTURE: "runtime_switch_alpha_texture",
+               RUNTIME_SWITCH_ALPHA_PROCEDURAL: "runtime_switch_alpha_procedural",
+               RUNTIME_FNPTR_DEFAULT: "runtime_fnptr_default",
+               RUNTIME_FNPTR_ALPHA_TEXTURE: "runtime_fnptr_alpha_texture",
+               RUNTIME_FNPTR_ALPHA_PROCEDURAL: "runtime_fnptr_alpha_procedural"}
+MISS = 0xFFFFFFFF
+
+HIT_DTYPE = np.dtype([("t", "<f4"), ("u", "<f4"), ("v", "<f4"), ("prim", "<u4")])
+COUNTS_DTYPE = np.dtype([("boxes", "<u4"), ("tris", "<u4"), ("alpha", "<u4"), ("reserved", "<u4")])
+
+EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_host",
+                    "vsr_destroy", "vsr_last_error", "vsr_bvh_export", "vsr_scene_import",
+                    "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version"]
+
+
+class VsrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{name}: {msg}")
+
+
+class TextureDesc(C.Structure):
+    _fields_ = [("width", C.c_uint32), ("height", C.c_uint32), ("rgba8", C.c_void_p)]
+
+
+class SceneDesc(C.Structure):
+    _fields_ = [("num_tris", C.c_uint32), ("vertices", C.c_void_p), ("geom_ids", C.c_void_p),
+                ("texcoords", C.c_void_p), ("num_geoms", C.c_uint32),
+                ("geom_texture", C.c_void_p), ("num_textures", C.c_uint32),
+                ("textures", C.c_void_p), ("device", C.c_int)]
+
+
+class BuildParams(C.Structure):
+    _fields_ = [("max_leaf_size", C.c_uint32), ("sah_bins", C.c_uint32),
+                ("traversal_cost", C.c_float), ("intersection_cost", C.c_float)]
+
+
+class IsectParams(C.Structure):
+    _fields_ = [("alpha_threshold", C.c_float), ("checker_freq", C.c_uint32)]
+
+
+class BvhView(C.Structure):
+    _fields_ = [("root_ref", C.c_uint32), ("root_lo", C.c_float * 3), ("root_hi", C.c_float * 3),
+                ("num_nodes", C.c_uint32), ("num_tris", C.c_uint32), ("num_textures", C.c_uint32),
+                ("num_texels", C.c_uint64), ("nodes", C.c_void_p), ("tris", C.c_void_p),
+                ("sides", C.c_void_p), ("texdescs", C.c_void_p), ("texels", C.c_void_p)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("num_tris_input", C.c_uint32), ("num_tris", C.c_uint32),
+                ("num_degenerate", C.c_uint32), ("num_nodes", C.c_uint32),
+                ("num_leaves", C.c_uint32), ("max_depth", C.c_uint32),
+                ("num_textures", C.c_uint32), ("built", C.c_uint32), ("num_texels", C.c_uint64),
+                ("device_bytes", C.c_uint64), ("build_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libvsr.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                              "g.build()'` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.vsr_scene_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(P)]
+        L.vsr_bvh_build.argtypes = [P, C.POINTER(BuildParams)]
+        L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
+        L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
+                                     P, P, P]
+        L.vsr_destroy.argtypes = [P]
+        L.vsr_last_error.restype = C.c_char_p
+        L.vsr_bvh_export.argtypes = [P, C.POINTER(BvhView)]
+        L.vsr_scene_import.argtypes = [C.POINTER(BvhView), C.c_int, C.POINTER(P)]
+        L.vsr_scene_stats.argtypes = [P, C.POINTER(Stats)]
+        L.vsr_launch_count.restype = C.c_uint64
+        L.vsr_abi_version.restype = C.c_uint32
+        for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_host",
+                     "vsr_destroy", "vsr_bvh_export", "vsr_scene_import", "vsr_scene_stats"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        raise VsrError(status, lib().vsr_last_error().decode())
+
+
+def launch_count() -> int:
+    return int(lib().vsr_launch_count())
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    return a.ctypes.data
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Scene:
+    """A scene on one device: vsr_scene_create + vsr_bvh_build, then vsr_trace."""
+
+    def __init__(self, vertices=None, geom_ids=None, texcoords=None, geom_texture=None,
+                 textures=None, device: int = 0, _handle=None):
+        self.device = device
+        self._h = C.c_void_p()
+        if _handle is not None:
+            self._h = _handle
+            return
+        v = np.ascontiguousarray(vertices, dtype=np.float32).reshape(-1, 9)
+        keep = [v]
+        g = None if geom_ids is None else np.ascontiguousarray(geom_ids, dtype=np.uint32)
+        tc = None if texcoords is None else np.ascontiguousarray(texcoords, dtype=np.float32)
+        gt = None if geom_texture is None else np.ascontiguousarray(geom_texture, dtype=np.uint32)
+        keep += [g, tc, gt]
+        texs = [np.ascontiguousarray(t, dtype=np.uint8) for t in (textures or [])]
+        tarr = (TextureDesc * max(1, len(texs)))()
+        for k, t in enumerate(texs):
+            assert t.ndim == 3 and t.shape[2] == 4, "textures are [H, W, 4] RGBA8"
+            tarr[k] = TextureDesc(t.shape[1], t.shape[0], t.ctypes.data)
+        desc = SceneDesc(v.shape[0], _ptr(v), _ptr(g), _ptr(tc),
+                         0 if gt is None else gt.shape[0], _ptr(gt), len(texs),
+                         C.cast(tarr, C.c_void_p) if texs else None, device)
+        _check(lib().vsr_scene_create(C.byref(desc), C.byref(self._h)))
+        del keep, texs
+
+    @classmethod
+    def from_workload(cls, scene, device: int = 0):
+        return cls(scene.vertices, scene.geom_ids, scene.texcoords, scene.geom_texture,
+                   scene.textures, device)
+
+    # -- lifecycle ------------------------------------------------------------
+    def close(self):
+        if self._h:
+            lib().vsr_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- setup ----------------------------------------------------------------
+    def build(self, max_leaf_size=4, sah_bins=16, traversal_cost=1.0, intersection_cost=1.0):
+        prm = BuildParams(max_leaf_size, sah_bins, traversal_cost, intersection_cost)
+        _check(lib().vsr_bvh_build(self._h, C.byref(prm)))
+        return self
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().vsr_scene_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    # -- hot path ---------------------------------------------------------------
+    def trace(self, rays, query=CLOSEST, isect=DEFAULT, hits=None, counts=None, stream=None,
+              alpha_threshold=0.01, checker_freq=8, n=None):
+        """Enqueue vsr_trace on device tensors; returns (hits, counts) tensors.
+
+        rays: torch float32 CUDA tensor [n, 8]; hits: [n, 4] float32 (allocated if None);
+        counts: [n, 4] int32 for COUNT kinds (allocated if None)."""
+        import torch
+        n = rays.shape[0] if n is None else n
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace(self._h, _ptr(rays), n, query, isect, C.byref(prm), _ptr(hits),
+                               _ptr(counts), _stream_handle(stream)))
+        return hits, counts
+
+    def trace_raw(self, rays_ptr, n, query, isect, hits_ptr, counts_ptr=None, stream=0,
+                  alpha_threshold=0.01, checker_freq=8):
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace(self._h, rays_ptr, n, query, isect, C.byref(prm), hits_ptr,
+                               counts_ptr, stream))
+
+    def trace_host(self, rays, query=CLOSEST, isect=DEFAULT, hits=None, counts=None, stream=None,
+                   alpha_threshold=0.01, checker_freq=8):
+        """vsr_trace_host over host buffers (numpy arrays or pinned CPU tensors)."""
+        n = rays.shape[0]
+        if hits is None:
+            hits = np.empty(n, dtype=HIT_DTYPE)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = np.empty(n, dtype=COUNTS_DTYPE)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_host(self._h, _ptr(rays), n, query, isect, C.byref(prm),
+                                    _ptr(hits), _ptr(counts),
+                                    0 if stream is None else _stream_handle(stream)))
+        return hits, counts
+
+    # -- replication (multi-GPU) ------------------------------------------------
+    def export(self) -> dict:
+        """Host copies of the flattened structure in the export layout."""
+        v = BvhView()
+        _check(lib().vsr_bvh_export(self._h, C.byref(v)))
+        arrs = {
+            "nodes": np.zeros((v.num_nodes, 16), np.uint32),
+            "tris": np.zeros((v.num_tris, 12), np.uint32),
+            "sides": np.zeros((v.num_tris, 8), np.uint32),
+            "texdescs": np.zeros((v.num_textures, 4), np.uint32),
+            "texels": np.zeros(v.num_texels, np.uint32),
+        }
+        v.nodes, v.tris, v.sides, v.texdescs, v.texels = (
+            _ptr(arrs["nodes"]) if v.num_nodes else None, _ptr(arrs["tris"]), _ptr(arrs["sides"]),
+            _ptr(arrs["texdescs"]), _ptr(arrs["texels"]))
+        _check(lib().vsr_bvh_export(self._h, C.byref(v)))
+        arrs["root_ref"] = int(v.root_ref)
+        arrs["root_lo"] = np.array(v.root_lo, np.float32)
+        arrs["root_hi"] = np.array(v.root_hi, np.float32)
+        return arrs
+
+    @classmethod
+    def import_arrays(cls, arrs: dict, device: int = 0):
+        """vsr_scene_import from host numpy arrays or device tensors (export layout)."""
+        v = BvhView()
+        v.root_ref = int(arrs["root_ref"])
+        v.root_lo = (C.c_float * 3)(*[float(x) for x in arrs["root_lo"]])
+        v.root_hi = (C.c_float * 3)(*[float(x) for x in arrs["root_hi"]])
+        v.num_nodes = arrs["nodes"].shape[0]
+        v.num_tris = arrs["tris"].shape[0]
+        v.num_textures = arrs["texdescs"].shape[0]
+        v.num_texels = arrs["texels"].shape[0]
+        v.nodes = _ptr(arrs["nodes"]) if v.num_nodes else None
+        v.tris = _ptr(arrs["tris"])
+        v.sides = _ptr(arrs["sides"])
+        v.texdescs = _ptr(arrs["texdescs"])
+        v.texels = _ptr(arrs["texels"])
+        h = C.c_void_p()
+        _check(lib().vsr_scene_import(C.byref(v), device, C.byref(h)))
+        return cls(device=device, _handle=h)
+
+
+def hits_to_numpy(hits) -> np.ndarray:
+    """[n,4] float32 tensor/array -> structured HIT_DTYPE array (prim as uint32 bits)."""
+    if hasattr(hits, "detach"):
+        hits = hits.detach().cpu().numpy()
+    return np.ascontiguousarray(hits, dtype=np.float32).view(HIT_DTYPE).reshape(-1)
+
+
+def counts_to_numpy(counts) -> np.ndarray:
+    if hasattr(counts, "detach"):
+        counts = counts.detach().cpu().numpy()
+    return np.ascontiguousarray(counts).view(np.uint32).view(COUNTS_DTYPE).reshape(-1)
