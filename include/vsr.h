@@ -127,7 +127,9 @@ typedef struct { float alpha_threshold; uint32_t checker_freq; } vsr_isect_param
 typedef struct vsr_scene vsr_scene;
 
 /* Flattened acceleration structure in the export layout:
- *   nodes    64 B each: float lo0[3],hi0[3],lo1[3],hi1[3]; uint32 ref[2]; uint32 pad[2]
+ *   nodes    64 B each: float x[4], y[4], z[4]; uint32 ref[2]; uint32 pad[2], where axis
+ *            k holds (lo0.k, lo1.k, hi0.k, hi1.k) — child 0 / child 1 slab planes side by
+ *            side; every child box must be finite with lo <= hi
  *   tris     48 B each: float v0[3]; uint32 prim_id; float e1[3]; 0; float e2[3]; 0
  *   sides    32 B each: float uv0[2],uv1[2],uv2[2]; uint32 texture; 0
  *   texdescs 16 B each: uint64 texel_offset; uint32 width, height

@@ -79,8 +79,8 @@ void oracle_lerp2(const float* a, const float* b, const float* c, float u, float
                   float* out);
 
 /* ---------------- export layout (re-declared from DESIGN.md) -------------- */
-typedef struct {          /* 64 B pair node */
-  float lo0[3], hi0[3], lo1[3], hi1[3];
+typedef struct {          /* 64 B pair node; per axis k: lo0.k, lo1.k, hi0.k, hi1.k */
+  float x[4], y[4], z[4];
   uint32_t ref[2];
   uint32_t pad[2];
 } or_node;

@@ -87,6 +87,22 @@ static void pad_box(float* lo, float* hi) {
   }
 }
 
+/* export layout: per axis k the node stores (lo0.k, lo1.k, hi0.k, hi1.k) */
+static void put_child_box(or_node* nd, int c, const float* lo, const float* hi) {
+  float* ax[3] = {nd->x, nd->y, nd->z};
+  for (int a = 0; a < 3; ++a) {
+    ax[a][c] = lo[a];
+    ax[a][2 + c] = hi[a];
+  }
+}
+static void get_child_box(const or_node* nd, int c, float* lo, float* hi) {
+  const float* ax[3] = {nd->x, nd->y, nd->z};
+  for (int a = 0; a < 3; ++a) {
+    lo[a] = ax[a][c];
+    hi[a] = ax[a][2 + c];
+  }
+}
+
 static uint32_t emit_leaf(bld_t* b, uint32_t beg, uint32_t end) {
   uint32_t first = b->num_out;
   for (uint32_t k = beg; k < end; ++k) b->leaf_order[b->num_out++] = b->idx[k];
@@ -117,15 +133,13 @@ static uint32_t build_rec(bld_t* b, uint32_t beg, uint32_t end, int depth) {
   if (me >= b->cap_nodes) return 0xFFFFFFFFu;
   or_node* nd = &b->nodes[me];
   memset(nd, 0, sizeof *nd);
-  float lo[3], hi[3];
-  range_bounds(b, beg, mid, lo, hi);
-  pad_box(lo, hi);
-  memcpy(b->nodes[me].lo0, lo, sizeof lo);
-  memcpy(b->nodes[me].hi0, hi, sizeof hi);
-  range_bounds(b, mid, end, lo, hi);
-  pad_box(lo, hi);
-  memcpy(b->nodes[me].lo1, lo, sizeof lo);
-  memcpy(b->nodes[me].hi1, hi, sizeof hi);
+  for (int c = 0; c < 2; ++c) {
+    float lo[3], hi[3];
+    if (c == 0) range_bounds(b, beg, mid, lo, hi);
+    else range_bounds(b, mid, end, lo, hi);
+    pad_box(lo, hi);
+    put_child_box(&b->nodes[me], c, lo, hi);
+  }
   uint32_t r0 = build_rec(b, beg, mid, depth + 1);
   uint32_t r1 = build_rec(b, mid, end, depth + 1);
   b->nodes[me].ref[0] = r0;
@@ -350,8 +364,11 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
       const or_node* nd = &b->nodes[cur];
       float tn0, tn1;
       c.boxes += 2;
-      int h0 = slab(nd->lo0, nd->hi0, o, inv, tmin, best_t, &tn0);
-      int h1 = slab(nd->lo1, nd->hi1, o, inv, tmin, best_t, &tn1);
+      float lo0[3], hi0[3], lo1[3], hi1[3];
+      get_child_box(nd, 0, lo0, hi0);
+      get_child_box(nd, 1, lo1, hi1);
+      int h0 = slab(lo0, hi0, o, inv, tmin, best_t, &tn0);
+      int h1 = slab(lo1, hi1, o, inv, tmin, best_t, &tn1);
       if (h0 && h1) {
         uint32_t nearr, farr;
         float ftn;

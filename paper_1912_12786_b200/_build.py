@@ -39,25 +39,34 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > lib_t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Build libvsr.so (or a tuning variant at `out` with extra -D`defines`)."""
+    target = out or LIB
+    if out is None and not force and not _stale():
         return LIB
-    tmp = LIB + ".tmp"
+    tmp = target + ".tmp"
     cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler",
            "-ffp-contract=off", *ARCH, "-lineinfo", "-fmad=false", "-prec-div=true",
            "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
+           *[f"-D{d}" for d in defines],
            "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libvsr.so")
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+    info = os.path.join(HERE, "ptxas_info.txt" if out is None else
+                        os.path.basename(target) + ".ptxas.txt")
+    with open(info, "w") as f:
         f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = [a for a in sys.argv[1:] if not a.startswith("-")]
+    defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                out=args[0] if args else None, defines=defs))

@@ -10,6 +10,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <atomic>
+#include <cstdlib>
 #include <mutex>
 #include <new>
 #include <string>
@@ -91,6 +93,8 @@ struct vsr_scene {
   Side* d_sides = nullptr;
   TexDesc* d_texdescs = nullptr;
   uint32_t* d_texels = nullptr;
+  unsigned long long* d_counters = nullptr;   // persistent-kernel work counters
+  std::atomic<uint32_t> launch_seq{0};
   uint64_t num_texels = 0;
   vsr_stats stats{};
   // ---- vsr_trace_host staging ----
@@ -112,11 +116,13 @@ struct vsr_scene {
     cudaFree(d_sides);
     cudaFree(d_texdescs);
     cudaFree(d_texels);
+    cudaFree(d_counters);
     d_nodes = nullptr;
     d_tris = nullptr;
     d_sides = nullptr;
     d_texdescs = nullptr;
     d_texels = nullptr;
+    d_counters = nullptr;
     built = false;
   }
   void free_stage() {
@@ -171,8 +177,15 @@ vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const f
   if ((st = dev_upload(&s->d_sides, sides, num_tris, "sidecars")) != VSR_OK) return st;
   if ((st = dev_upload(&s->d_texdescs, texdescs, num_textures, "texdescs")) != VSR_OK) return st;
   if ((st = dev_upload(&s->d_texels, texels, num_texels, "texels")) != VSR_OK) return st;
+  {
+    const size_t cbytes = sizeof(unsigned long long) * 2 * kCounterSlots;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s->d_counters), cbytes);
+    if (e != cudaSuccess) return cuda_fail(e, "counters");
+    if ((e = cudaMemset(s->d_counters, 0, cbytes)) != cudaSuccess) return cuda_fail(e, "counters");
+  }
   s->num_texels = num_texels;
   DevScene& d = s->dev;
+  d.counters = s->d_counters;
   d.nodes = s->d_nodes;
   d.tris = s->d_tris;
   d.sides = s->d_sides;
@@ -255,7 +268,20 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
     }
     p.filter_fn = s->fn_cache[kind];
   }
+  // Scheduling knobs (read per call; defaults are the measured best):
+  // VSR_SCHED=persistent selects the persistent kernel, VSR_REFILL its refill threshold.
+  const char* ev = std::getenv("VSR_REFILL");
+  const int refill = ev ? std::atoi(ev) : 32;
+  p.refill = refill < 1 ? 1 : (refill > 32 ? 32 : refill);
+  const char* es = std::getenv("VSR_SCHED");
+  p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent : kSchedDirect;
   return VSR_OK;
+}
+
+// A fresh work-counter slot per launch (self-reset by the launch's last warp).
+unsigned long long* next_counter(vsr_scene* s) {
+  const uint32_t slot = s->launch_seq.fetch_add(1, std::memory_order_relaxed) % kCounterSlots;
+  return s->d_counters + 2 * (size_t)slot;
 }
 
 }  // namespace
@@ -458,6 +484,7 @@ vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query 
   p.n = n;
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  p.counter = next_counter(s);
   cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "trace kernel launch");
   return VSR_OK;
@@ -521,6 +548,7 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
     p.hits = s->d_out[k];
     p.counts = s->d_cnt[k];
     p.n = m;
+    p.counter = next_counter(s);
     if ((e = launch_trace(query, isect, p, ss)) != cudaSuccess) return cuda_fail(e, "trace launch");
     if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
         cudaSuccess)
@@ -652,6 +680,15 @@ vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) 
     }
     if (it.ref >= v->num_nodes) return fail(VSR_ERR_INVALID_ARG, "node ref out of range");
     if (seen_node[it.ref]) return fail(VSR_ERR_INVALID_ARG, "node reachable twice (not a tree)");
+    {
+      const PairNode& nd = nodes[it.ref];
+      const float* ax[3] = {nd.x, nd.y, nd.z};
+      for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 2; ++c)
+          if (!std::isfinite(ax[a][c]) || !std::isfinite(ax[a][2 + c]) || !(ax[a][c] <= ax[a][2 + c]))
+            return fail(VSR_ERR_INVALID_ARG, "node " + std::to_string(it.ref) +
+                                                 " has a non-finite or inverted child box");
+    }
     seen_node[it.ref] = 1;
     st.push_back({nodes[it.ref].ref[1], it.depth + 1});
     st.push_back({nodes[it.ref].ref[0], it.depth + 1});

@@ -302,8 +302,16 @@ vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh&
       if (it.patch_node >= 0) out.nodes[it.patch_node].ref[it.patch_child] = me;
       const TmpNode& tn = c.nodes[it.tmp];
       PairNode& pn = out.nodes[me];
-      pad_out(tn.box[0], pn.lo0, pn.hi0);
-      pad_out(tn.box[1], pn.lo1, pn.hi1);
+      float lo[2][3], hi[2][3];
+      pad_out(tn.box[0], lo[0], hi[0]);
+      pad_out(tn.box[1], lo[1], hi[1]);
+      float* axis[3] = {pn.x, pn.y, pn.z};
+      for (int a = 0; a < 3; ++a) {
+        axis[a][0] = lo[0][a];
+        axis[a][1] = lo[1][a];
+        axis[a][2] = hi[0][a];
+        axis[a][3] = hi[1][a];
+      }
       pn.pad[0] = pn.pad[1] = 0;
       for (int k = 1; k >= 0; --k) {       // push child 1 first so child 0 is emitted next
         int32_t ch = tn.child[k];

@@ -13,8 +13,13 @@
 // (PAPER.md:83-89), and the default intersector inlines to the same
 // instructions as calling `intersect` directly.
 //
-// Arithmetic follows DESIGN.md §"Arithmetic contract" (IEEE fp32, no FMA: the
-// translation unit is compiled with -fmad=false, IEEE division).
+// Box tests come in two shapes: a single `Aabb` (the root) and an `AabbPair`
+// (both children of a 64-B pair node, tested together with Blackwell's packed
+// f32x2 add/mul — one instruction computes the same IEEE result for both
+// boxes).  A box hook on an AabbPair stands for two box-hook calls.
+//
+// Arithmetic follows DESIGN.md §3 "Arithmetic contract" (IEEE fp32 RN, no FMA:
+// the translation unit is compiled with -fmad=false and IEEE division).
 #pragma once
 #include <cstdint>
 #include <type_traits>
@@ -23,14 +28,56 @@
 
 namespace vsr {
 
+// ---------------------------------------------------------------------------
+// packed fp32x2 helpers (sm_100a FADD2 / FMUL2; each lane is an IEEE RN op)
+// ---------------------------------------------------------------------------
+typedef unsigned long long f2_t;
+
+__device__ __forceinline__ f2_t pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void upk(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t sub2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
 struct RayCtx {
   float ox, oy, oz, tmin;
   float dx, dy, dz;
-  float ix, iy, iz;   // guarded reciprocal direction (reading A20)
+  float ix, iy, iz;          // guarded reciprocal direction (reading A20)
 };
+
+__device__ __forceinline__ void make_ray(RayCtx& r, float4 a, float4 b) {
+  r.ox = a.x; r.oy = a.y; r.oz = a.z; r.tmin = a.w;
+  r.dx = b.x; r.dy = b.y; r.dz = b.z;
+  r.ix = 1.0f / (fabsf(b.x) > 0x1p-80f ? b.x : copysignf(0x1p-80f, b.x));
+  r.iy = 1.0f / (fabsf(b.y) > 0x1p-80f ? b.y : copysignf(0x1p-80f, b.y));
+  r.iz = 1.0f / (fabsf(b.z) > 0x1p-80f ? b.z : copysignf(0x1p-80f, b.z));
+}
 
 struct Aabb {
   float lx, ly, lz, hx, hy, hz;
+};
+
+// Both children of a pair node, as stored: per axis (lo0, lo1, hi0, hi1).
+struct AabbPair {
+  float4 x, y, z;
+};
+
+struct BoxPairHit {
+  bool h0, h1;
+  float tn0, tn1;
 };
 
 // Triangle as loaded: v0 (+prim id bits in w), e1, e2 (SPEC S:47 v0/e1/e2).
@@ -68,6 +115,32 @@ __device__ __forceinline__ bool intersect(const RayCtx& r, const Aabb& b, float 
   f = fminf(f, best_t);
   tn = n;
   return n <= f;
+}
+
+// The same test on both children of a pair node at once: every sub/mul is the
+// scalar contract's operation, done two at a time (FADD2/FMUL2).
+__device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair& b,
+                                                float best_t) {
+  float t0x0, t0x1, t1x0, t1x1, t0y0, t0y1, t1y0, t1y1, t0z0, t0z1, t1z0, t1z1;
+  // (o.k, o.k) and (inv.k, inv.k) are broadcast operands (SASS ".F32" form)
+  const f2_t ox2 = pk(r.ox, r.ox), oy2 = pk(r.oy, r.oy), oz2 = pk(r.oz, r.oz);
+  const f2_t ix2 = pk(r.ix, r.ix), iy2 = pk(r.iy, r.iy), iz2 = pk(r.iz, r.iz);
+  upk(mul2(sub2(pk(b.x.x, b.x.y), ox2), ix2), t0x0, t0x1);
+  upk(mul2(sub2(pk(b.x.z, b.x.w), ox2), ix2), t1x0, t1x1);
+  upk(mul2(sub2(pk(b.y.x, b.y.y), oy2), iy2), t0y0, t0y1);
+  upk(mul2(sub2(pk(b.y.z, b.y.w), oy2), iy2), t1y0, t1y1);
+  upk(mul2(sub2(pk(b.z.x, b.z.y), oz2), iz2), t0z0, t0z1);
+  upk(mul2(sub2(pk(b.z.z, b.z.w), oz2), iz2), t1z0, t1z1);
+  BoxPairHit h;
+  h.tn0 = fmaxf(fmaxf(fminf(t0x0, t1x0), fminf(t0y0, t1y0)), fmaxf(fminf(t0z0, t1z0), r.tmin));
+  h.tn1 = fmaxf(fmaxf(fminf(t0x1, t1x1), fminf(t0y1, t1y1)), fmaxf(fminf(t0z1, t1z1), r.tmin));
+  const float f0 = fminf(fminf(fmaxf(t0x0, t1x0), fmaxf(t0y0, t1y0)), fmaxf(t0z0, t1z0));
+  const float f1 = fminf(fminf(fmaxf(t0x1, t1x1), fmaxf(t0y1, t1y1)), fmaxf(t0z1, t1z1));
+  float g0, g1;
+  upk(mul2(pk(f0, f1), pk(1.0000003576f, 1.0000003576f)), g0, g1);
+  h.h0 = h.tn0 <= fminf(g0, best_t);
+  h.h1 = h.tn1 <= fminf(g1, best_t);
+  return h;
 }
 
 // Ray/triangle: Möller–Trumbore in textbook order (DESIGN.md
@@ -110,10 +183,16 @@ struct basic_intersector {
   __device__ __forceinline__ bool operator()(const RayCtx& r, const Aabb& b, Args&&... args) {
     return intersect(r, b, static_cast<Args&&>(args)...);
   }
+  template <class... Args>
+  __device__ __forceinline__ BoxPairHit operator()(const RayCtx& r, const AabbPair& b,
+                                                   Args&&... args) {
+    return intersect(r, b, static_cast<Args&&>(args)...);
+  }
   __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
                                                    float tmax_cur) {
     return intersect(r, t, k, tmax_cur);
   }
+  __device__ __forceinline__ void reset() {}
   __device__ __forceinline__ uint32_t lookups() const { return 0u; }
 };
 
@@ -121,6 +200,7 @@ struct basic_intersector {
 // the traversal calls `intersect` itself.
 struct no_intersector {
   static constexpr bool kCounts = false;
+  __device__ __forceinline__ void reset() {}
   __device__ __forceinline__ uint32_t lookups() const { return 0u; }
 };
 
@@ -161,7 +241,7 @@ __device__ __forceinline__ bool checker_keep(float fm, float u, float v) {
 }
 
 // ALPHA_TEXTURE: the §4 listing.  Only the triangle hook is
-// overridden; the box hook is inherited (SPEC S:226 design decision).
+// overridden; the box hooks are inherited (SPEC S:226 design decision).
 struct alpha_texture_intersector : basic_intersector<alpha_texture_intersector> {
   using basic_intersector<alpha_texture_intersector>::operator();
   IsectData d;
@@ -175,6 +255,7 @@ struct alpha_texture_intersector : basic_intersector<alpha_texture_intersector> 
     }
     return hr;
   }
+  __device__ __forceinline__ void reset() { n_lookups = 0; }
   __device__ __forceinline__ uint32_t lookups() const { return n_lookups; }
 };
 
@@ -203,10 +284,21 @@ struct cost_intersector : Inner {
     ++num_boxes;
     return Inner::operator()(r, b, static_cast<Args&&>(args)...);
   }
+  template <class... Args>
+  __device__ __forceinline__ BoxPairHit operator()(const RayCtx& r, const AabbPair& b,
+                                                   Args&&... args) {
+    num_boxes += 2;   // two box tests: one per child
+    return Inner::operator()(r, b, static_cast<Args&&>(args)...);
+  }
   __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
                                                    float tmax_cur) {
     ++num_tris;
     return Inner::operator()(r, t, k, tmax_cur);
+  }
+  __device__ __forceinline__ void reset() {
+    num_boxes = 0;
+    num_tris = 0;
+    Inner::reset();
   }
 };
 

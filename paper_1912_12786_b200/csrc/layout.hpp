@@ -20,8 +20,12 @@ constexpr uint32_t kMaxLeafSize = 32;
 constexpr uint32_t kMaxTris = 1u << 26;
 constexpr int kMaxStack = 64;
 
+// Per axis k: (lo0.k, lo1.k, hi0.k, hi1.k) — the two children's slab planes
+// side by side, so one packed f32x2 op works on both children.
 struct alignas(16) PairNode {
-  float lo0[3], hi0[3], lo1[3], hi1[3];
+  float x[4];
+  float y[4];
+  float z[4];
   uint32_t ref[2];
   uint32_t pad[2];
 };
@@ -64,7 +68,12 @@ struct DevScene {
   uint32_t root_ref;
   float root_lo[3], root_hi[3];
   uint32_t num_nodes, num_tris, num_textures;
+  unsigned long long* counters;   // kCounterSlots x 2, zero-initialised
 };
+
+// Work-distribution counters for the persistent trace kernel: slot s holds
+// {next ray, warps finished}; the last warp of a launch resets its slot.
+constexpr uint32_t kCounterSlots = 256;
 
 // Scene data the mask intersectors read (their "member variables",
 // PAPER.md:286-288 "stores a pointer to the texture and texture coordinate

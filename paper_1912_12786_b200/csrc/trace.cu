@@ -1,16 +1,23 @@
 // trace.cu — the hot path: per-ray BVH traversal + ray/triangle intersection
 // with a compile-time intersector (§3.2).
 //
-// One thread per ray.  The traversal is the while-while scheme of Aila &
-// Laine cited by the paper: an inner-node loop that calls
-// the intersector's box hook on both children of a 64-B pair node, then a
-// leaf loop that calls its triangle hook on each primitive.  Every decision
-// is a function of the ray alone (no warp-voted speculation), so the
-// counting intersector's numbers are deterministic and match the CPU walker
-// bit for bit.
+// Traversal: the while-while scheme of Aila & Laine cited by the paper
+// (PAPER.md:228-247): an inner-node loop that calls the intersector's box
+// hook on both children of a 64-B pair node, then a leaf loop that calls its
+// triangle hook on each primitive.  Every decision is a function of the ray
+// alone (no warp-voted speculation), so results and the counting
+// intersector's numbers do not depend on which lanes share a warp — they are
+// deterministic and match the CPU walker bit for bit.
+//
+// Scheduling (B200): persistent warps.  The grid is sized to the occupancy
+// limit (148 SMs x resident blocks); every warp repeatedly claims rays from a
+// global counter (one atomicAdd per refill, ballot/popc compaction) and keeps
+// tracing.  A warp refills its idle lanes after each processed leaf as soon
+// as `refill` lanes are idle ("dynamic fetch"), so short rays (sky) do not
+// leave lanes idle behind long ones (forest) and there is no last-wave tail.
 //
 // Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (IEEE fp32
-// contract; see DESIGN.md A.1-A.3).
+// contract).
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -24,6 +31,7 @@ namespace vsr {
 
 constexpr int kBlock = 128;
 constexpr uint32_t kMissPrim = 0xFFFFFFFFu;
+constexpr unsigned kFull = 0xFFFFFFFFu;
 enum : int { kClosest = 0, kAny = 1 };
 
 template <class I>
@@ -34,89 +42,123 @@ __device__ __forceinline__ bool box_hook(I& isect, const RayCtx& r, const Aabb& 
 }
 
 template <class I>
+__device__ __forceinline__ BoxPairHit box_pair_hook(I& isect, const RayCtx& r, const AabbPair& b,
+                                                    float best_t) {
+  if constexpr (std::is_same<I, no_intersector>::value) return intersect(r, b, best_t);
+  else return isect(r, b, best_t);
+}
+
+template <class I>
 __device__ __forceinline__ hit_record tri_hook(I& isect, const RayCtx& r, const TriData& t,
                                                uint32_t k, float tmax_cur) {
   if constexpr (std::is_same<I, no_intersector>::value) return intersect(r, t, k, tmax_cur);
   else return isect(r, t, k, tmax_cur);
 }
 
-struct Result {
+// Per-lane traversal state of one ray.
+struct Trav {
+  RayCtx r;
+  float best_t;
+  bool have;
   float t, u, v;
   uint32_t prim;
+  uint32_t cur;
+  int sp;
+  uint64_t id;
 };
 
-// intersect(ray, BVH, isect) — PAPER.md:228-247, both call sites hooked
-// (PAPER.md:248-252).
-template <int Q, class I>
-__device__ __forceinline__ Result traverse(const DevScene& S, const RayCtx& r, float tmax,
-                                           I& isect) {
-  Result res{__int_as_float(0x7f800000), 0.0f, 0.0f, kMissPrim};
-  float best_t = tmax;
-  bool have = false;
-  float tn;
-  const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2],
-                  S.root_hi[0], S.root_hi[1], S.root_hi[2]};
-  // The root box is tested (and counted) once before the loop (reading A11).
-  if (!box_hook(isect, r, root, best_t, tn)) return res;
+// Pop the next entry not farther than the current best (reading A14).
+__device__ __forceinline__ bool pop(Trav& T, const float2* stack) {
+  while (T.sp > 0) {
+    --T.sp;
+    const float2 e = stack[T.sp];
+    if (e.y <= T.best_t) {
+      T.cur = __float_as_uint(e.x);
+      return true;
+    }
+  }
+  return false;
+}
 
-  float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by the build
-  int sp = 0;
-  uint32_t cur = S.root_ref;
-  for (;;) {
-    // ---- inner-node loop: "while node is inner" ----
-    while (!(cur & kLeafBit)) {
-      const float4* np = reinterpret_cast<const float4*>(S.nodes + cur);
-      const float4 n0 = __ldg(np), n1 = __ldg(np + 1), n2 = __ldg(np + 2), n3 = __ldg(np + 3);
-      const Aabb b0{n0.x, n0.y, n0.z, n0.w, n1.x, n1.y};
-      const Aabb b1{n1.z, n1.w, n2.x, n2.y, n2.z, n2.w};
-      float tn0, tn1;
-      const bool h0 = box_hook(isect, r, b0, best_t, tn0);
-      const bool h1 = box_hook(isect, r, b1, best_t, tn1);
-      const uint32_t r0 = __float_as_uint(n3.x), r1 = __float_as_uint(n3.y);
-      if (h0 && h1) {
-        const bool swap = tn1 < tn0;   // nearer child first, ties -> child 0 (reading A13)
-        stack[sp] = make_float2(__uint_as_float(swap ? r0 : r1), swap ? tn0 : tn1);
-        ++sp;
-        cur = swap ? r1 : r0;
-      } else if (h0) {
-        cur = r0;
-      } else if (h1) {
-        cur = r1;
-      } else {
-        goto pop;
-      }
+// Load ray `id`, test the root box once (counted, reading A11).
+// Returns true if the ray needs traversal.
+template <class I>
+__device__ __forceinline__ bool start_ray(const TraceParams& p, Trav& T, I& isect, uint64_t id) {
+  const float4 a = __ldg(p.rays + 2 * id);
+  const float4 b = __ldg(p.rays + 2 * id + 1);
+  make_ray(T.r, a, b);
+  T.best_t = b.w;
+  T.have = false;
+  T.t = __int_as_float(0x7f800000);
+  T.u = 0.0f;
+  T.v = 0.0f;
+  T.prim = kMissPrim;
+  T.sp = 0;
+  T.id = id;
+  T.cur = p.scene.root_ref;
+  isect.reset();
+  const Aabb root{p.scene.root_lo[0], p.scene.root_lo[1], p.scene.root_lo[2],
+                  p.scene.root_hi[0], p.scene.root_hi[1], p.scene.root_hi[2]};
+  float tn;
+  return box_hook(isect, T.r, root, T.best_t, tn);
+}
+
+// One outer iteration of "while ray not terminated": descend
+// to the next leaf, run its primitives, pop.  Returns true when the ray is done.
+template <int Q, class I>
+__device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, float2* stack) {
+  // ---- inner-node loop: "while node is inner" ----
+  while (!(T.cur & kLeafBit)) {
+    const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
+    const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2), nr = __ldg(np + 3);
+    const BoxPairHit h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
+    const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
+    if (h.h0 && h.h1) {
+      const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
+      stack[T.sp] = make_float2(__uint_as_float(swap ? r0 : r1), swap ? h.tn0 : h.tn1);
+      ++T.sp;
+      T.cur = swap ? r1 : r0;
+    } else if (h.h0) {
+      T.cur = r0;
+    } else if (h.h1) {
+      T.cur = r1;
+    } else if (!pop(T, stack)) {
+      return true;
     }
-    // ---- leaf loop: "while node contains untested primitives" ----
-    {
-      const uint32_t first = cur & kLeafFirstMask;
-      const uint32_t end = first + ((cur >> kLeafCountShift) & 31u) + 1u;
-      for (uint32_t k = first; k < end; ++k) {
-        const float4* tp = reinterpret_cast<const float4*>(S.tris + k);
-        const TriData td{__ldg(tp), __ldg(tp + 1), __ldg(tp + 2)};
-        const hit_record hr = tri_hook(isect, r, td, k, best_t);
-        if (Q == kAny) {
-          if (hr.hit) {   // any-hit: the first accepted hit ends the query
-            res = Result{hr.t, hr.u, hr.v, __float_as_uint(td.a.w)};
-            return res;
-          }
-        } else if (hr.hit && (!have || hr.t < best_t)) {
-          // closest-hit: accepted hits shrink tmax; vetoed ones do not
-          best_t = hr.t;
-          have = true;
-          res = Result{hr.t, hr.u, hr.v, __float_as_uint(td.a.w)};
-        }
+  }
+  // ---- leaf loop: "while node contains untested primitives" ----
+  const uint32_t first = T.cur & kLeafFirstMask;
+  const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
+  for (uint32_t k = first; k < end; ++k) {
+    const float4* tp = reinterpret_cast<const float4*>(S.tris + k);
+    const TriData td{__ldg(tp), __ldg(tp + 1), __ldg(tp + 2)};
+    const hit_record hr = tri_hook(isect, T.r, td, k, T.best_t);
+    if (Q == kAny) {
+      if (hr.hit) {   // any-hit: the first accepted hit ends the query
+        T.t = hr.t;
+        T.u = hr.u;
+        T.v = hr.v;
+        T.prim = __float_as_uint(td.a.w);
+        return true;
       }
+    } else if (hr.hit && (!T.have || hr.t < T.best_t)) {
+      // closest-hit: accepted hits shrink tmax; vetoed ones do not
+      T.best_t = hr.t;
+      T.have = true;
+      T.t = hr.t;
+      T.u = hr.u;
+      T.v = hr.v;
+      T.prim = __float_as_uint(td.a.w);
     }
-  pop:
-    for (;;) {   // entries farther than the current best are dropped unhooked (A14)
-      if (sp == 0) return res;
-      --sp;
-      const float2 e = stack[sp];
-      if (e.y <= best_t) {
-        cur = __float_as_uint(e.x);
-        break;
-      }
-    }
+  }
+  return !pop(T, stack);
+}
+
+template <class I>
+__device__ __forceinline__ void finish(const TraceParams& p, const Trav& T, const I& isect) {
+  p.hits[T.id] = make_float4(T.t, T.u, T.v, __uint_as_float(T.prim));
+  if constexpr (I::kCounts) {
+    p.counts[T.id] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
   }
 }
 
@@ -137,24 +179,106 @@ __device__ __forceinline__ I make_isect(const TraceParams& p) {
   return isect;
 }
 
+#ifndef VSR_MINB
+#define VSR_MINB 0
+#endif
+#ifndef VSR_CHUNK
+#define VSR_CHUNK 32
+#endif
+constexpr unsigned kChunk = VSR_CHUNK;   // rays a warp claims per atomicAdd
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Direct schedule (default): one thread per ray, blocks in ray order; the
+// hardware block scheduler balances the blocks across the 148 SMs.
 template <int Q, class I>
-__global__ void __launch_bounds__(kBlock) trace_kernel(const TraceParams p) {
-  const uint64_t i = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
-  if (i >= p.n) return;
-  const float4 a = __ldg(p.rays + 2 * i);
-  const float4 b = __ldg(p.rays + 2 * i + 1);
-  RayCtx r;
-  r.ox = a.x; r.oy = a.y; r.oz = a.z; r.tmin = a.w;
-  r.dx = b.x; r.dy = b.y; r.dz = b.z;
-  // guarded reciprocal (reading A20): no 0*inf NaN in the slab test
-  r.ix = 1.0f / (fabsf(b.x) > 0x1p-80f ? b.x : copysignf(0x1p-80f, b.x));
-  r.iy = 1.0f / (fabsf(b.y) > 0x1p-80f ? b.y : copysignf(0x1p-80f, b.y));
-  r.iz = 1.0f / (fabsf(b.z) > 0x1p-80f ? b.z : copysignf(0x1p-80f, b.z));
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TraceParams p) {
+#ifdef VSR_TIMELINE
+  const uint64_t t0 = global_ns();
+#endif
+  const uint64_t id = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+  if (id < p.n) {
+    I isect = make_isect<I>(p);
+    Trav T;
+    float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
+    if (start_ray(p, T, isect, id)) {
+      while (!advance<Q>(p.scene, T, isect, stack)) {
+      }
+    }
+    finish(p, T, isect);
+  }
+#ifdef VSR_TIMELINE
+  // diagnostic build only: per-warp (SM id, start ns, end ns) into counts[warp]
+  __syncwarp();
+  if ((threadIdx.x & 31u) == 0 && !I::kCounts) {
+    unsigned smid;
+    asm("mov.u32 %0, %%smid;" : "=r"(smid));
+    const uint64_t t1 = global_ns();
+    p.counts[id / 32] = make_uint4(smid, (unsigned)t0, (unsigned)t1, (unsigned)(t0 >> 32));
+  }
+#endif
+}
+
+// Persistent schedule (VSR_SCHED=persistent): grid sized to residency; warps
+// claim kChunk rays per atomicAdd and refill idle lanes after each leaf once
+// `refill` lanes are idle.  Measured slower than the direct schedule on the
+// coherent primary rays of C2 (profiles/r01_tuning.md); kept for incoherent
+// workloads and as a measured alternative.
+template <int Q, class I>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(const TraceParams p) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned below = (1u << lane) - 1u;
+  unsigned long long* ctr = p.counter;
   I isect = make_isect<I>(p);
-  const Result res = traverse<Q>(p.scene, r, b.w, isect);
-  p.hits[i] = make_float4(res.t, res.u, res.v, __uint_as_float(res.prim));
-  if constexpr (I::kCounts) {
-    p.counts[i] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
+  Trav T;
+  float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
+  bool active = false;
+  // warp-uniform work queue: [next, next + left) of the warp's claimed chunk
+  unsigned long long next = 0;
+  unsigned left = 0;
+  bool drained = false;      // the global counter ran past n
+  for (;;) {
+    // converged refill point: ballot/popc compaction of the idle lanes
+    const unsigned idle = __ballot_sync(kFull, !active);
+    if (idle != 0u && (idle == kFull || __popc(idle) >= p.refill) && !(drained && left == 0)) {
+      if (left == 0) {   // claim a new chunk: one atomicAdd per kChunk rays
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(ctr, (unsigned long long)kChunk);
+        base = __shfl_sync(kFull, base, 0);
+        next = base;
+        left = base >= p.n ? 0u : (unsigned)min((unsigned long long)kChunk, p.n - base);
+        drained = base + kChunk >= p.n;
+      }
+      const unsigned take = min((unsigned)__popc(idle), left);
+      if (!active) {
+        const unsigned rank = __popc(idle & below);
+        if (rank < take) {
+          active = start_ray(p, T, isect, next + rank);
+          if (!active) finish(p, T, isect);   // missed the root box: a miss record
+        }
+      }
+      next += take;
+      left -= take;
+    } else if (idle == kFull && drained && left == 0) {
+      break;
+    }
+    if (active && advance<Q>(p.scene, T, isect, stack)) {
+      finish(p, T, isect);
+      active = false;
+    }
+  }
+  // The launch's last warp resets the counter slot for a later launch.
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long warps = (unsigned long long)gridDim.x * (kBlock / 32);
+    if (atomicAdd(ctr + 1, 1ull) == warps - 1ull) {
+      atomicExch(ctr, 0ull);
+      atomicExch(ctr + 1, 0ull);
+    }
   }
 }
 
@@ -171,10 +295,38 @@ __device__ filter_fn_t g_fn_alpha_proc = fn_alpha_proc;
 namespace {
 std::atomic<uint64_t> g_launches{0};
 
+int sm_count() {
+  static int cache[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cache[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev] = n > 0 ? n : 148;
+  }
+  return cache[dev];
+}
+
 template <int Q, class I>
 cudaError_t launch(const TraceParams& p, cudaStream_t st) {
-  const uint64_t blocks = (p.n + kBlock - 1) / kBlock;
-  trace_kernel<Q, I><<<(unsigned)blocks, kBlock, 0, st>>>(p);
+  const uint64_t need = (p.n + kBlock - 1) / kBlock;
+  if (p.sched == kSchedPersistent) {
+    static int per_sm = 0;   // resident blocks per SM for this instantiation
+    if (per_sm == 0) {
+      int nb = 0;
+      cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &nb, trace_kernel_persistent<Q, I>, kBlock, 0);
+      if (e != cudaSuccess) return e;
+      per_sm = nb > 0 ? nb : 1;
+    }
+    const uint64_t full = (uint64_t)per_sm * sm_count();
+    const unsigned blocks = (unsigned)(need < full ? need : full);
+    trace_kernel_persistent<Q, I><<<blocks, kBlock, 0, st>>>(p);
+  } else {
+    if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+    trace_kernel<Q, I><<<(unsigned)need, kBlock, 0, st>>>(p);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -9,6 +9,8 @@
 
 namespace vsr {
 
+enum : int { kSchedDirect = 0, kSchedPersistent = 1 };
+
 // Kernel parameters (passed by value: they live in the constant parameter bank).
 struct TraceParams {
   DevScene scene;
@@ -17,6 +19,9 @@ struct TraceParams {
   float4* hits;
   uint4* counts;
   uint64_t n;
+  unsigned long long* counter;   // {next ray, warps done}: this launch's slot
+  int refill;                    // refill a warp once this many lanes are idle
+  int sched;                     // kSchedDirect (default) or kSchedPersistent
   int runtime_kind;
   void* filter_fn;
 };

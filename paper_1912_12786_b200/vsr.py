@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvsr.so")
+LIB_PATH = os.environ.get("VSR_LIB") or os.path.join(_HERE, "libvsr.so")   # VSR_LIB: tuning builds
 
 # vsr_status
 OK, ERR_INVALID_ARG, ERR_EMPTY_SCENE, ERR_NONFINITE, ERR_BVH_TOO_DEEP, ERR_NOT_BUILT, \

@@ -59,8 +59,9 @@ def validate(b, vertices=None, max_leaf=None, slack=1e-5):
         assert 0 <= ref < nodes.shape[0]
         seen_node[ref] += 1
         for c in range(2):
-            clo = nf[ref, 6 * c:6 * c + 3]
-            chi = nf[ref, 6 * c + 3:6 * c + 6]
+            # per axis k the node stores (lo0.k, lo1.k, hi0.k, hi1.k)
+            clo = nf[ref, [0 + c, 4 + c, 8 + c]]
+            chi = nf[ref, [2 + c, 6 + c, 10 + c]]
             assert np.all(clo <= chi)
             assert np.all(clo >= lo - slack * np.maximum(1, np.abs(lo)))
             assert np.all(chi <= hi + slack * np.maximum(1, np.abs(hi)))

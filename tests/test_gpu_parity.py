@@ -128,6 +128,33 @@ def test_edge_rays(V, oracle_lib):
             check_against_oracle(V, oracle_lib, sc, s, rays, q, k)
 
 
+@pytest.mark.parametrize("refill", ["32", "8"])
+def test_persistent_schedule(V, oracle_lib, monkeypatch, refill):
+    """The persistent dynamic-fetch kernel gives the same bytes as the direct one;
+    its self-resetting work counters survive > 256 launches (slot reuse)."""
+    sc = W.random_soup(1500, seed=5)
+    rays = W.random_rays(5003, seed=6)
+    s = V.Scene.from_workload(sc).build()
+    ref = {}
+    for q in (V.CLOSEST, V.ANY):
+        for k in (V.DEFAULT, V.ALPHA_TEXTURE, V.COUNT_ALPHA_TEXTURE):
+            ref[(q, k)] = gpu_trace(V, s, rays.data, q, k)
+    monkeypatch.setenv("VSR_SCHED", "persistent")
+    monkeypatch.setenv("VSR_REFILL", refill)
+    for q in (V.CLOSEST, V.ANY):
+        for k in (V.DEFAULT, V.ALPHA_TEXTURE, V.COUNT_ALPHA_TEXTURE):
+            h, c = check_against_oracle(V, oracle_lib, sc, s, rays.data, q, k)[:2]
+            assert h.tobytes() == ref[(q, k)][0].tobytes()
+            if c is not None:
+                assert c.tobytes() == ref[(q, k)][1].tobytes()
+    r = torch.from_numpy(rays.data).cuda()
+    hits = torch.empty((rays.n, 4), device="cuda")
+    for _ in range(300):
+        s.trace(r, V.CLOSEST, V.ALPHA_TEXTURE, hits=hits)
+    torch.cuda.synchronize()
+    assert V.hits_to_numpy(hits).tobytes() == ref[(V.CLOSEST, V.ALPHA_TEXTURE)][0].tobytes()
+
+
 def test_imported_oracle_bvh_counts(V, oracle_lib):
     """Counts bit-exact on a tree the product did NOT build (oracle median BVH)."""
     o = oracle_lib

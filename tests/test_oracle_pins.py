@@ -411,45 +411,13 @@ def test_slab_worked_examples(oracle_lib):
     assert not hit
 
 
-def _validate_bvh(b, n_tris_expected):
-    """Independent structural check of an export-layout BVH."""
-    LEAF = 0x80000000
-    nodes = b.nodes.view(np.float32)
-    refs = b.nodes[:, 12:14]
-    seen = np.zeros(b.tris.shape[0], dtype=np.int64)
-    vt = b.tris.view(np.float32)
-    v0 = vt[:, 0:3]
-    v1 = v0 + vt[:, 4:7]
-    v2 = v0 + vt[:, 8:11]
-    tlo = np.minimum(np.minimum(v0, v1), v2)
-    thi = np.maximum(np.maximum(v0, v1), v2)
-
-    def visit(ref, lo, hi, depth):
-        assert depth <= 64
-        if ref & LEAF:
-            first = ref & 0x03FFFFFF
-            cnt = ((ref >> 26) & 31) + 1
-            for k in range(first, first + cnt):
-                seen[k] += 1
-                assert np.all(tlo[k] >= lo - 1e-5) and np.all(thi[k] <= hi + 1e-5)
-            return
-        nd = nodes[ref]
-        for c in range(2):
-            clo, chi = nd[6 * c:6 * c + 3], nd[6 * c + 3:6 * c + 6]
-            assert np.all(clo >= lo - 1e-5) and np.all(chi <= hi + 1e-5)
-            visit(int(refs[ref, c]), clo, chi, depth + 1)
-
-    visit(int(b.root_ref), b.root_lo, b.root_hi, 0)
-    assert np.all(seen == 1)
-    assert b.tris.shape[0] == n_tris_expected
-    assert sorted(b.tris[:, 3].tolist()) == sorted(set(b.tris[:, 3].tolist()))
-
-
 @pytest.mark.parametrize("max_leaf", [1, 4, 16])
 def test_oracle_bvh_valid(oracle_lib, max_leaf):
+    from tests import bvh_check
     sc = W.random_soup(777, seed=51)
     b = oracle_lib.build_bvh(sc, max_leaf)
-    _validate_bvh(b, 777)
+    bvh_check.validate(b, sc.vertices, max_leaf)
+    assert b.tris.shape[0] == 777
 
 
 def _hand_bvh(z_left=1.0, z_right=3.0, transparent_left=False):
@@ -458,8 +426,10 @@ def _hand_bvh(z_left=1.0, z_right=3.0, transparent_left=False):
     f = np.float32
     nodes = np.zeros((1, 16), np.uint32)
     nf = nodes.view(np.float32)
-    nf[0, 0:6] = [0, 0, z_left, 1, 1, z_left]       # child 0 box (flat in z)
-    nf[0, 6:12] = [0, 0, z_right, 1, 1, z_right]    # child 1 box
+    # per axis k: (lo0.k, lo1.k, hi0.k, hi1.k); child 0 at z_left, child 1 at z_right (flat in z)
+    nf[0, 0:4] = [0, 0, 1, 1]
+    nf[0, 4:8] = [0, 0, 1, 1]
+    nf[0, 8:12] = [z_left, z_right, z_left, z_right]
     LEAF = 0x80000000
     nodes[0, 12] = LEAF | (1 << 26) | 0           # leaf: 2 tris from 0
     nodes[0, 13] = LEAF | (1 << 26) | 2           # leaf: 2 tris from 2
