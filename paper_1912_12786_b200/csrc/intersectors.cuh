@@ -143,6 +143,50 @@ __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair&
   return h;
 }
 
+// Ray octant (sign bits of inv.x, inv.y, inv.z) known at compile time: an
+// extra box-hook argument, forwarded like the paper's inverse direction
+// (PAPER.md:371-376).
+template <int OCT>
+struct octant {};
+
+// Octant-specialised pair slab test.  With lo <= hi (validated on import) and
+// inv never 0 or NaN (guarded reciprocal), IEEE rounding is monotone, so
+// min((lo-o)*inv, (hi-o)*inv) is exactly the near-plane term and max the far
+// one: selecting the planes at compile time gives bit-identical tn/tf to the
+// generic test above without its 12 per-axis min/max.
+template <int OCT>
+__device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair& b, float best_t,
+                                                octant<OCT>) {
+  constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
+  const f2_t ox2 = pk(r.ox, r.ox), oy2 = pk(r.oy, r.oy), oz2 = pk(r.oz, r.oz);
+  const f2_t ix2 = pk(r.ix, r.ix), iy2 = pk(r.iy, r.iy), iz2 = pk(r.iz, r.iz);
+  const f2_t lox = pk(b.x.x, b.x.y), hix = pk(b.x.z, b.x.w);
+  const f2_t loy = pk(b.y.x, b.y.y), hiy = pk(b.y.z, b.y.w);
+  const f2_t loz = pk(b.z.x, b.z.y), hiz = pk(b.z.z, b.z.w);
+  float nx0, nx1, fx0, fx1, ny0, ny1, fy0, fy1, nz0, nz1, fz0, fz1;
+  upk(mul2(sub2(sx ? hix : lox, ox2), ix2), nx0, nx1);
+  upk(mul2(sub2(sx ? lox : hix, ox2), ix2), fx0, fx1);
+  upk(mul2(sub2(sy ? hiy : loy, oy2), iy2), ny0, ny1);
+  upk(mul2(sub2(sy ? loy : hiy, oy2), iy2), fy0, fy1);
+  upk(mul2(sub2(sz ? hiz : loz, oz2), iz2), nz0, nz1);
+  upk(mul2(sub2(sz ? loz : hiz, oz2), iz2), fz0, fz1);
+  BoxPairHit h;
+  h.tn0 = fmaxf(fmaxf(nx0, ny0), fmaxf(nz0, r.tmin));
+  h.tn1 = fmaxf(fmaxf(nx1, ny1), fmaxf(nz1, r.tmin));
+  float g0, g1;
+  upk(mul2(pk(fminf(fminf(fx0, fy0), fz0), fminf(fminf(fx1, fy1), fz1)),
+           pk(1.0000003576f, 1.0000003576f)),
+      g0, g1);
+  h.h0 = h.tn0 <= fminf(g0, best_t);
+  h.h1 = h.tn1 <= fminf(g1, best_t);
+  return h;
+}
+
+__device__ __forceinline__ int ray_octant(const RayCtx& r) {
+  return (int)(__float_as_uint(r.ix) >> 31) | (int)((__float_as_uint(r.iy) >> 31) << 1) |
+         (int)((__float_as_uint(r.iz) >> 31) << 2);
+}
+
 // Ray/triangle: Möller–Trumbore in textbook order (DESIGN.md
 // A.1), no culling, |det| < 1e-12 -> miss, t in [tmin, tmax_cur] inclusive.
 __device__ __forceinline__ hit_record intersect(const RayCtx& r, const TriData& tri, uint32_t k,

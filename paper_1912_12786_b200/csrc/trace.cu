@@ -41,11 +41,11 @@ __device__ __forceinline__ bool box_hook(I& isect, const RayCtx& r, const Aabb& 
   else return isect(r, b, best_t, tn);
 }
 
-template <class I>
+template <class I, class... Args>
 __device__ __forceinline__ BoxPairHit box_pair_hook(I& isect, const RayCtx& r, const AabbPair& b,
-                                                    float best_t) {
-  if constexpr (std::is_same<I, no_intersector>::value) return intersect(r, b, best_t);
-  else return isect(r, b, best_t);
+                                                    float best_t, Args... args) {
+  if constexpr (std::is_same<I, no_intersector>::value) return intersect(r, b, best_t, args...);
+  else return isect(r, b, best_t, args...);
 }
 
 template <class I>
@@ -103,15 +103,18 @@ __device__ __forceinline__ bool start_ray(const TraceParams& p, Trav& T, I& isec
   return box_hook(isect, T.r, root, T.best_t, tn);
 }
 
-// One outer iteration of "while ray not terminated" (PAPER.md:235): descend
-// to the next leaf, run its primitives, pop.  Returns true when the ray is done.
-template <int Q, class I>
-__device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, float2* stack) {
-  // ---- inner-node loop: "while node is inner" ----
+// ---- inner-node loop: "while node is inner" ----
+// OCT >= 0: the warp's rays all share octant OCT (specialised slab test);
+// OCT < 0: generic min/max slab test.  Returns false when the ray is done
+// (nothing left to visit), true when T.cur is a leaf.
+template <int OCT, class I>
+__device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, float2* stack) {
   while (!(T.cur & kLeafBit)) {
     const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
     const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2), nr = __ldg(np + 3);
-    const BoxPairHit h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
+    BoxPairHit h;
+    if constexpr (OCT >= 0) h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t, octant<OCT>{});
+    else h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
     const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
     if (h.h0 && h.h1) {
       const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
@@ -123,10 +126,16 @@ __device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, fl
     } else if (h.h1) {
       T.cur = r1;
     } else if (!pop(T, stack)) {
-      return true;
+      return false;
     }
   }
-  // ---- leaf loop: "while node contains untested primitives" ----
+  return true;
+}
+
+// ---- leaf loop: "while node contains untested primitives" ----
+// Returns true when the query is finished (any-hit accepted a primitive).
+template <int Q, class I>
+__device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect) {
   const uint32_t first = T.cur & kLeafFirstMask;
   const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
   for (uint32_t k = first; k < end; ++k) {
@@ -151,7 +160,39 @@ __device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, fl
       T.prim = __float_as_uint(td.a.w);
     }
   }
+  return false;
+}
+
+// One outer iteration of "while ray not terminated" (PAPER.md:235): descend
+// to the next leaf, run its primitives, pop.  Returns true when the ray is done.
+template <int Q, int OCT, class I>
+__device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, float2* stack) {
+  if (!descend<OCT>(S, T, isect, stack)) return true;
+  if (leaf<Q>(S, T, isect)) return true;
   return !pop(T, stack);
+}
+
+// Whole traversal of one ray.  `oct` is warp-uniform: 0..7 if every lane of
+// the warp has that octant (primary rays: all but the centre row/column
+// tiles), 8 otherwise; the switch is taken once per leaf, uniformly.
+template <int Q, class I>
+__device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, float2* stack,
+                                         int oct) {
+  for (;;) {
+    bool at_leaf;
+    switch (oct) {
+      case 0: at_leaf = descend<0>(S, T, isect, stack); break;
+      case 1: at_leaf = descend<1>(S, T, isect, stack); break;
+      case 2: at_leaf = descend<2>(S, T, isect, stack); break;
+      case 3: at_leaf = descend<3>(S, T, isect, stack); break;
+      case 4: at_leaf = descend<4>(S, T, isect, stack); break;
+      case 5: at_leaf = descend<5>(S, T, isect, stack); break;
+      case 6: at_leaf = descend<6>(S, T, isect, stack); break;
+      case 7: at_leaf = descend<7>(S, T, isect, stack); break;
+      default: at_leaf = descend<-1>(S, T, isect, stack); break;
+    }
+    if (!at_leaf || leaf<Q>(S, T, isect) || !pop(T, stack)) return;
+  }
 }
 
 template <class I>
@@ -205,10 +246,12 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
     I isect = make_isect<I>(p);
     Trav T;
     float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
-    if (start_ray(p, T, isect, id)) {
-      while (!advance<Q>(p.scene, T, isect, stack)) {
-      }
-    }
+    const bool go = start_ray(p, T, isect, id);
+    // warp-uniform octant: specialised slab test when all live lanes agree
+    const unsigned live = __activemask();
+    const int oct = ray_octant(T.r);
+    const int woct = __match_any_sync(live, oct) == live ? oct : 8;
+    if (go) traverse<Q>(p.scene, T, isect, stack, woct);
     finish(p, T, isect);
   }
 #ifdef VSR_TIMELINE
@@ -266,7 +309,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(cons
     } else if (idle == kFull && drained && left == 0) {
       break;
     }
-    if (active && advance<Q>(p.scene, T, isect, stack)) {
+    if (active && advance<Q, -1>(p.scene, T, isect, stack)) {
       finish(p, T, isect);
       active = false;
     }
