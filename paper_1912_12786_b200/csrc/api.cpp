@@ -275,6 +275,8 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.refill = refill < 1 ? 1 : (refill > 32 ? 32 : refill);
   const char* es = std::getenv("VSR_SCHED");
   p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent : kSchedDirect;
+  const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
+  p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
   return VSR_OK;
 }
 

@@ -234,14 +234,92 @@ __device__ __forceinline__ uint64_t global_ns() {
   return t;
 }
 
-// Direct schedule (default): one thread per ray, blocks in ray order; the
+// ---------------------------------------------------------------------------
+// Longest-first block order (scheduling only; results do not depend on it).
+// The last rays to start bound a launch's tail by their own latency, so the
+// blocks whose rays cross the most of the scene are launched first.  Cost
+// proxy per 128-ray block: the longest segment of 4 sample rays inside the
+// padded root box, in 32 buckets of the root diagonal; a counting sort
+// (histogram + scatter, most expensive bucket first) gives the permutation.
+// ---------------------------------------------------------------------------
+constexpr int kOrderBuckets = 32;
+
+__global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
+                                                         uint32_t* hist, uint32_t* slot) {
+  const uint32_t t = blockIdx.x * 256 + threadIdx.x;   // 4 sample rays per 128-ray block
+  const uint32_t b = t >> 2;
+  float len = 0.0f;
+  if (b < nblocks) {
+    const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * 42u + ((t & 3u) == 3u ? 1u : 0u);
+    if (id < p.n) {
+      const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
+      RayCtx r;
+      make_ray(r, a, d);
+      const float t0x = (p.scene.root_lo[0] - r.ox) * r.ix, t1x = (p.scene.root_hi[0] - r.ox) * r.ix;
+      const float t0y = (p.scene.root_lo[1] - r.oy) * r.iy, t1y = (p.scene.root_hi[1] - r.oy) * r.iy;
+      const float t0z = (p.scene.root_lo[2] - r.oz) * r.iz, t1z = (p.scene.root_hi[2] - r.oz) * r.iz;
+      const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
+      const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
+      if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+    }
+  }
+  len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 1));
+  len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 2));
+  // CTA-local histogram first: a handful of buckets take almost all blocks,
+  // so per-block global atomics would serialise on a few addresses.
+  __shared__ uint32_t lh[kOrderBuckets], lbase[kOrderBuckets];
+  if (threadIdx.x < kOrderBuckets) lh[threadIdx.x] = 0;
+  __syncthreads();
+  const bool leader = (t & 3u) == 0u && b < nblocks;
+  int q = 0;
+  uint32_t lpos = 0;
+  if (leader) {
+    const float dx = p.scene.root_hi[0] - p.scene.root_lo[0];
+    const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
+    const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
+    const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
+    q = diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
+    q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
+    lpos = atomicAdd(lh + q, 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < kOrderBuckets && lh[threadIdx.x])
+    lbase[threadIdx.x] = atomicAdd(hist + threadIdx.x, lh[threadIdx.x]);
+  __syncthreads();
+  if (leader) slot[b] = ((uint32_t)q << 24) | (lbase[q] + lpos);
+}
+
+__global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, const uint32_t* hist,
+                                                            const uint32_t* slot, uint32_t* perm) {
+  __shared__ uint32_t start[kOrderBuckets];
+  if (threadIdx.x < 32) {   // exclusive scan over buckets, most expensive first
+    const unsigned lane = threadIdx.x;
+    const int q = kOrderBuckets - 1 - (int)lane;
+    const uint32_t cnt = hist[q];
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    start[q] = incl - cnt;
+  }
+  __syncthreads();
+  const uint32_t b = blockIdx.x * 256 + threadIdx.x;
+  if (b >= nblocks) return;
+  const uint32_t s = slot[b];
+  perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
+}
+
+// Direct schedule (default): one thread per ray; launch slot i traces the 128
+// rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
 template <int Q, class I>
 __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TraceParams p) {
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
 #endif
-  const uint64_t id = (uint64_t)blockIdx.x * kBlock + threadIdx.x;
+  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t id = blk * kBlock + threadIdx.x;
   if (id < p.n) {
     I isect = make_isect<I>(p);
     Trav T;
@@ -406,9 +484,49 @@ cudaError_t filter_fn_pointer(int kind, void** out) {
   return e;
 }
 
-cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st) {
-  if (p.n == 0) return cudaSuccess;
-  return query == kAny ? dispatch_isect<kAny>(isect, p, st) : dispatch_isect<kClosest>(isect, p, st);
+cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStream_t st) {
+  if (p_in.n == 0) return cudaSuccess;
+  TraceParams p = p_in;
+  p.perm = nullptr;
+  const uint64_t nblocks = (p.n + kBlock - 1) / kBlock;
+  void* scratch = nullptr;
+  if (p.order && p.sched == kSchedDirect && nblocks >= 2ull * sm_count() && nblocks < (1u << 24)) {
+    // stream-ordered scratch: safe for concurrent launches on other streams.
+    // Keep freed blocks in the device's default pool (release threshold = max)
+    // so steady-state launches never map memory.
+    static bool pool_set[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !pool_set[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      pool_set[dev] = true;
+    }
+    const size_t bytes = sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks);
+    cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
+    if (e != cudaSuccess) return e;
+    uint32_t* hist = static_cast<uint32_t*>(scratch);
+    uint32_t* slot = hist + kOrderBuckets;
+    uint32_t* perm = slot + nblocks;
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess) return e;
+    order_cost_kernel<<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(p, (uint32_t)nblocks,
+                                                                             hist, slot);
+    order_scatter_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, st>>>((uint32_t)nblocks, hist,
+                                                                            slot, perm);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    p.perm = perm;
+  }
+  cudaError_t e = query == kAny ? dispatch_isect<kAny>(isect, p, st)
+                                : dispatch_isect<kClosest>(isect, p, st);
+  if (scratch) {
+    cudaError_t f = cudaFreeAsync(scratch, st);
+    if (e == cudaSuccess) e = f;
+  }
+  return e;
 }
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }

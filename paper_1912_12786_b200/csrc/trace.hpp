@@ -22,6 +22,8 @@ struct TraceParams {
   unsigned long long* counter;   // {next ray, warps done}: this launch's slot
   int refill;                    // refill a warp once this many lanes are idle
   int sched;                     // kSchedDirect (default) or kSchedPersistent
+  int order;                     // 1: launch blocks longest-first (direct schedule)
+  const uint32_t* perm;          // longest-first block permutation (set by launch_trace)
   int runtime_kind;
   void* filter_fn;
 };
