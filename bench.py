@@ -182,9 +182,18 @@ def run_own(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    # VSR_DIST_BACKEND=gloo: plumbing test of the N-rank path on fewer GPUs
+    # (ranks share devices; no kernel waits on another rank's kernel).
+    backend = os.environ.get("VSR_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
+    cdev = "cuda" if backend == "nccl" else "cpu"   # device of collective tensors
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     if rank == 0:
         _build.build()
     if world > 1:
@@ -196,7 +205,8 @@ def run_own(args):
     t0 = time.time()
     if world > 1:
         base = vsr.Scene.from_workload(sc, device=local).build() if rank == 0 else None
-        scene, _ = shard.broadcast_scene(base, local, dist)
+        scene, _ = shard.broadcast_scene(base, local, dist,
+                                         tensor_device=None if backend == "nccl" else "cpu")
     else:
         scene = vsr.Scene.from_workload(sc, device=local).build()
     setup_s = time.time() - t0
@@ -252,7 +262,7 @@ def run_own(args):
     ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler)
     ms_step = float(np.mean(ms))
     if world > 1:
-        t = torch.tensor([ms_step], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms_step], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step_max = float(t.item())
     else:
@@ -323,7 +333,7 @@ def run_own(args):
         e2e_ms.append(a.elapsed_time(b))
     e2e_step = float(np.mean(e2e_ms))
     if world > 1:
-        t = torch.tensor([e2e_step], dtype=torch.float64, device="cuda")
+        t = torch.tensor([e2e_step], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_step = float(t.item())
     e2e = {"value": round(world * n / (e2e_step * 1e-3) / 1e6, 2), "unit": UNIT,
@@ -384,7 +394,7 @@ def cpu_baseline(sc, rays, args, target_s=12.0):
     osc = oracle.OracleScene(sc)
     cores = host_cores()
     rng = np.random.default_rng(12345)
-    probe = rays.data[rng.choice(rays.n, 64 * cores, replace=False)]
+    probe = rays.data[rng.choice(rays.n, min(rays.n, 1024 * cores), replace=False)]  # oracle hands out 1024-ray chunks
     t0 = time.perf_counter()
     oracle.trace(osc, probe, oq, ok, nthreads=cores)
     per_ray = (time.perf_counter() - t0) / probe.shape[0]
@@ -414,7 +424,7 @@ def run_reference(args):
     osc = oracle.OracleScene(sc)
     cores = host_cores()
     rng = np.random.default_rng(777)
-    probe = rays.data[rng.choice(rays.n, 32 * cores, replace=False)]
+    probe = rays.data[rng.choice(rays.n, min(rays.n, 1024 * cores), replace=False)]  # oracle hands out 1024-ray chunks
     t0 = time.perf_counter()
     oracle.trace(osc, probe, oq, ok, nthreads=cores)
     per_ray = (time.perf_counter() - t0) / probe.shape[0]
