@@ -148,13 +148,9 @@ class ClockSampler:
 # workload
 # ---------------------------------------------------------------------------
 def make_workload(name, rank=0):
+    """Scene + this rank's frame (camera shifted 2 m sideways per rank)."""
     import workloads as W
-    if name in ("C2", "C3"):
-        sc = W.forest_scene()
-        rays = W.pinhole_rays((2.0 * rank, 4.0, -280.0), (2.0 * rank, 4.0, 0.0), (0.0, 1.0, 0.0),
-                              45.0, 1920, 1080)
-        return sc, rays
-    return W.config(name)
+    return W.scene(name), W.rays_for(name, shift_x=2.0 * rank)
 
 
 def algorithmic_bytes(counts_np, isect_has_alpha):

@@ -179,7 +179,8 @@ typedef struct {
   or_hit* hits;
   uint32_t* flags;
   uint32_t* ntie;
-  uint64_t next; /* atomic chunk counter */
+  uint64_t chunk; /* rays per claim */
+  uint64_t next;  /* atomic chunk counter */
 } job_t;
 
 static void trace_one(const job_t* jb, uint64_t r) {
@@ -260,7 +261,7 @@ static void trace_one(const job_t* jb, uint64_t r) {
 
 static void* worker(void* arg) {
   job_t* jb = (job_t*)arg;
-  const uint64_t chunk = 1024;
+  const uint64_t chunk = jb->chunk;
   for (;;) {
     uint64_t b = __atomic_fetch_add(&jb->next, chunk, __ATOMIC_RELAXED);
     if (b >= jb->n) break;
@@ -282,6 +283,10 @@ int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, in
   jb.s = s; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect;
   jb.thr = thr; jb.M = M; jb.hits = hits; jb.flags = flags; jb.ntie = ntie; jb.next = 0;
   if (nthreads < 1) nthreads = 1;
+  /* up to 1024 rays per claim, fewer for small inputs so every thread gets work */
+  jb.chunk = n / ((uint64_t)nthreads * 4);
+  if (jb.chunk < 1) jb.chunk = 1;
+  if (jb.chunk > 1024) jb.chunk = 1024;
   if (nthreads == 1) {
     worker(&jb);
     return 0;

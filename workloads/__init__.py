@@ -24,6 +24,9 @@ from .gen import (  # noqa: F401
     c5_scene,
     pinhole_rays,
     config,
+    scene,
+    rays_for,
+    CAMERAS,
     CONFIGS,
     random_soup,
     random_rays,

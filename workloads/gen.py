@@ -424,21 +424,39 @@ CONFIGS = {
 }
 
 
+CAMERAS = {
+    # eye, look_at, up, vfov, width, height, spp
+    "C2": ((0.0, 4.0, -280.0), (0.0, 4.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
+    "C3": ((0.0, 4.0, -280.0), (0.0, 4.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
+    "C4": ((0.0, 40.0, -300.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
+    "C5": ((0.0, 60.0, -1100.0), (0.0, 10.0, 0.0), (0.0, 1.0, 0.0), 45.0, 3840, 2160, 4),
+}
+
+
+def scene(name: str, textures=None) -> Scene:
+    if name == "C1":
+        return quad_pair_scene()
+    if name in ("C2", "C3"):
+        return forest_scene(textures=textures)
+    if name == "C4":
+        return c4_scene(textures=textures)
+    if name == "C5":
+        return c5_scene(textures=textures)
+    raise KeyError(name)
+
+
+def rays_for(name: str, width: int | None = None, height: int | None = None,
+             spp: int | None = None, shift_x: float = 0.0) -> Rays:
+    """The config's primary rays; `shift_x` moves the camera sideways (per-rank frames)."""
+    if name == "C1":
+        return quad_pair_rays(width or 64)
+    eye, look, up, fov, w, h, s = CAMERAS[name]
+    eye = (eye[0] + shift_x, eye[1], eye[2])
+    look = (look[0] + shift_x, look[1], look[2])
+    return pinhole_rays(eye, look, up, fov, width or w, height or h, spp or s)
+
+
 def config(name: str, width: int | None = None, height: int | None = None, spp: int | None = None,
            textures=None):
     """Return (scene, rays) for a named config; width/height/spp may be reduced for tests."""
-    if name == "C1":
-        return quad_pair_scene(), quad_pair_rays(width or 64)
-    if name in ("C2", "C3"):
-        sc = forest_scene(textures=textures)
-        return sc, pinhole_rays((0.0, 4.0, -280.0), (0.0, 4.0, 0.0), (0.0, 1.0, 0.0), 45.0,
-                                width or 1920, height or 1080, spp or 1)
-    if name == "C4":
-        sc = c4_scene(textures=textures)
-        return sc, pinhole_rays((0.0, 40.0, -300.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 45.0,
-                                width or 1920, height or 1080, spp or 1)
-    if name == "C5":
-        sc = c5_scene(textures=textures)
-        return sc, pinhole_rays((0.0, 60.0, -1100.0), (0.0, 10.0, 0.0), (0.0, 1.0, 0.0), 45.0,
-                                width or 3840, height or 2160, spp or 4)
-    raise KeyError(name)
+    return scene(name, textures), rays_for(name, width, height, spp)
