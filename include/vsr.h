@@ -114,7 +114,8 @@ typedef struct {
   int device;                     /* CUDA ordinal that owns the device copies               */
 } vsr_scene_desc;
 
-/* Binned SAH parameters.  NULL -> {4, 16, 1.0, 1.0}.
+/* Binned SAH parameters.  NULL -> {2, 16, 1.0, 1.0} (max_leaf 2 measured
+ * fastest on C2 and C5; SPEC's CPU program uses 4; reading A22).
  * 1 <= max_leaf_size <= 32, 2 <= sah_bins <= 256. */
 typedef struct {
   uint32_t max_leaf_size, sah_bins;

@@ -392,7 +392,7 @@ vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
   if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
   if (s->vertices.empty() && s->num_tris_input == 0 && s->built)
     return fail(VSR_ERR_INVALID_ARG, "imported scenes cannot be rebuilt");
-  vsr_build_params prm{4u, 16u, 1.0f, 1.0f};
+  vsr_build_params prm{2u, 16u, 1.0f, 1.0f};   // max_leaf 2: measured best (A22)
   if (params) prm = *params;
   if (prm.max_leaf_size < 1 || prm.max_leaf_size > kMaxLeafSize)
     return fail(VSR_ERR_INVALID_ARG, "max_leaf_size must be in [1, 32]");

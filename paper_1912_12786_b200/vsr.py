@@ -200,7 +200,7 @@ class Scene:
         self.close()
 
     # -- setup ----------------------------------------------------------------
-    def build(self, max_leaf_size=4, sah_bins=16, traversal_cost=1.0, intersection_cost=1.0):
+    def build(self, max_leaf_size=2, sah_bins=16, traversal_cost=1.0, intersection_cost=1.0):
         prm = BuildParams(max_leaf_size, sah_bins, traversal_cost, intersection_cost)
         _check(lib().vsr_bvh_build(self._h, C.byref(prm)))
         return self
