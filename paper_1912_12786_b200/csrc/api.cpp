@@ -109,6 +109,24 @@ struct vsr_scene {
   cudaEvent_t ev_done[kSlots] = {};
   void* fn_cache[4] = {};
   bool fn_cached[4] = {};
+  // ---- per-stream scratch of the longest-first order pass ----
+  struct OrderScratch {
+    cudaStream_t st;
+    void* ptr;
+    size_t cap;
+    cudaEvent_t ev;   // last use; the next use waits on it (stream-ordered reuse)
+  };
+  std::mutex order_mu;
+  std::vector<OrderScratch> order_scratch;
+
+  void free_order_scratch() {
+    for (OrderScratch& o : order_scratch) {
+      cudaEventSynchronize(o.ev);
+      cudaFree(o.ptr);
+      cudaEventDestroy(o.ev);
+    }
+    order_scratch.clear();
+  }
 
   void free_device() {
     cudaFree(d_nodes);
@@ -278,6 +296,43 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
   return VSR_OK;
+}
+
+// Launch with the scene's scratch for stream `st` (created or grown on first
+// use; the launch waits for the scratch's previous use, then records its own).
+// Caller holds no lock; n must be the launch's ray count.
+cudaError_t launch_with_scratch(vsr_scene* s, int query, int isect, TraceParams& p,
+                                cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(s->order_mu);
+  const size_t bytes = order_scratch_bytes(p.n);
+  vsr_scene::OrderScratch* o = nullptr;
+  for (auto& e : s->order_scratch)
+    if (e.st == st) o = &e;
+  cudaError_t e = cudaSuccess;
+  if (!o && s->order_scratch.size() < 16) {
+    vsr_scene::OrderScratch n{st, nullptr, 0, nullptr};
+    if ((e = cudaEventCreateWithFlags(&n.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+    s->order_scratch.push_back(n);
+    o = &s->order_scratch.back();
+  }
+  p.order_scratch = nullptr;
+  p.order_scratch_bytes = 0;
+  if (o) {
+    if (o->cap < bytes) {
+      cudaEventSynchronize(o->ev);
+      cudaFree(o->ptr);
+      o->ptr = nullptr;
+      o->cap = 0;
+      if ((e = cudaMalloc(&o->ptr, bytes)) != cudaSuccess) return e;
+      o->cap = bytes;
+    }
+    if ((e = cudaStreamWaitEvent(st, o->ev, 0)) != cudaSuccess) return e;
+    p.order_scratch = o->ptr;
+    p.order_scratch_bytes = o->cap;
+  }
+  e = launch_trace(query, isect, p, st);
+  if (e == cudaSuccess && o) e = cudaEventRecord(o->ev, st);
+  return e;
 }
 
 // A fresh work-counter slot per launch (self-reset by the launch's last warp).
@@ -487,7 +542,7 @@ vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query 
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   p.counter = next_counter(s);
-  cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "trace kernel launch");
   return VSR_OK;
 }
@@ -551,7 +606,8 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
     p.counts = s->d_cnt[k];
     p.n = m;
     p.counter = next_counter(s);
-    if ((e = launch_trace(query, isect, p, ss)) != cudaSuccess) return cuda_fail(e, "trace launch");
+    if ((e = launch_with_scratch(s, query, isect, p, ss)) != cudaSuccess)
+      return cuda_fail(e, "trace launch");
     if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
         cudaSuccess)
       return cuda_fail(e, "D2H hits");
@@ -575,6 +631,7 @@ vsr_status vsr_destroy(vsr_scene* s) {
   if (s->device >= 0) {
     DeviceGuard g(s->device);
     s->free_stage();
+    s->free_order_scratch();
     s->free_device();
   }
   delete s;

@@ -107,11 +107,28 @@ __device__ __forceinline__ bool start_ray(const TraceParams& p, Trav& T, I& isec
 // OCT >= 0: the warp's rays all share octant OCT (specialised slab test);
 // OCT < 0: generic min/max slab test.  Returns false when the ray is done
 // (nothing left to visit), true when T.cur is a leaf.
+__device__ __forceinline__ void prefetch_ref(const DevScene& S, uint32_t ref) {
+  const void* ptr = (ref & kLeafBit) ? static_cast<const void*>(S.tris + (ref & kLeafFirstMask))
+                                     : static_cast<const void*>(S.nodes + ref);
+#if VSR_PREFETCH == 1
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(ptr));
+#elif VSR_PREFETCH == 2
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+#else
+  (void)ptr;
+#endif
+}
+
 template <int OCT, class I>
 __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, float2* stack) {
   while (!(T.cur & kLeafBit)) {
     const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
     const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2), nr = __ldg(np + 3);
+#if VSR_PREFETCH
+    // both children towards L1 while the box tests run (scheduling only)
+    prefetch_ref(S, __float_as_uint(nr.x));
+    prefetch_ref(S, __float_as_uint(nr.y));
+#endif
     BoxPairHit h;
     if constexpr (OCT >= 0) h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t, octant<OCT>{});
     else h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
@@ -484,12 +501,18 @@ cudaError_t filter_fn_pointer(int kind, void** out) {
   return e;
 }
 
+size_t order_scratch_bytes(uint64_t n) {
+  const uint64_t nblocks = (n + kBlock - 1) / kBlock;
+  return sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks);
+}
+
 cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStream_t st) {
   if (p_in.n == 0) return cudaSuccess;
   TraceParams p = p_in;
   p.perm = nullptr;
   const uint64_t nblocks = (p.n + kBlock - 1) / kBlock;
   void* scratch = nullptr;
+  bool owned = false;
   if (p.order && p.sched == kSchedDirect && nblocks >= 2ull * sm_count() && nblocks < (1u << 24)) {
     // stream-ordered scratch: safe for concurrent launches on other streams.
     // Keep freed blocks in the device's default pool (release threshold = max)
@@ -505,9 +528,14 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
       }
       pool_set[dev] = true;
     }
-    const size_t bytes = sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks);
-    cudaError_t e = cudaMallocAsync(&scratch, bytes, st);
-    if (e != cudaSuccess) return e;
+    const size_t bytes = order_scratch_bytes(p.n);
+    cudaError_t e = cudaSuccess;
+    if (p.order_scratch && p.order_scratch_bytes >= bytes) {
+      scratch = p.order_scratch;   // caller-provided, stream-ordered (per-stream scene scratch)
+    } else {
+      if ((e = cudaMallocAsync(&scratch, bytes, st)) != cudaSuccess) return e;
+      owned = true;
+    }
     uint32_t* hist = static_cast<uint32_t*>(scratch);
     uint32_t* slot = hist + kOrderBuckets;
     uint32_t* perm = slot + nblocks;
@@ -522,7 +550,7 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
   }
   cudaError_t e = query == kAny ? dispatch_isect<kAny>(isect, p, st)
                                 : dispatch_isect<kClosest>(isect, p, st);
-  if (scratch) {
+  if (owned) {
     cudaError_t f = cudaFreeAsync(scratch, st);
     if (e == cudaSuccess) e = f;
   }

@@ -24,11 +24,14 @@ struct TraceParams {
   int sched;                     // kSchedDirect (default) or kSchedPersistent
   int order;                     // 1: launch blocks longest-first (direct schedule)
   const uint32_t* perm;          // longest-first block permutation (set by launch_trace)
+  void* order_scratch;           // optional stream-ordered scratch for the order pass
+  size_t order_scratch_bytes;
   int runtime_kind;
   void* filter_fn;
 };
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);
+size_t order_scratch_bytes(uint64_t n);
 cudaError_t filter_fn_pointer(int kind, void** out);
 uint64_t launch_count();
 
