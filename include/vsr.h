@@ -176,6 +176,16 @@ vsr_status vsr_trace(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_qu
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream);
 
+/* Multi-hit query ("the first N hit points"): per ray the
+ * max_hits (1..16) smallest-t ACCEPTED hits in ascending t (equal t: the order traversal found
+ * them).  Once max_hits hits are held, tmax shrinks to the worst kept t.
+ * d_hits: n*max_hits vsr_hit, ray-major (ray i's j-th hit at i*max_hits+j); unused slots hold
+ * the miss record.  d_num_hits: optional, n uint32 (hits kept).  d_counts as in vsr_trace.
+ * The RUNTIME_* controls are not provided for this query (VSR_ERR_UNSUPPORTED). */
+vsr_status vsr_trace_multi(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, uint32_t max_hits,
+                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                           uint32_t* d_num_hits, vsr_counts* d_counts, void* stream);
+
 /* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
  * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
  * overlap the kernel; returns after the stream work completed. */

@@ -88,6 +88,12 @@ def lib():
                                    C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_int]
         L.walker_slab.argtypes = [C.c_void_p] * 3 + [C.c_float, C.POINTER(C.c_float),
                                                        C.POINTER(C.c_float)]
+        L.oracle_trace_multi.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_uint64, C.c_uint32,
+                                         C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int]
+        L.walker_trace_multi.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_uint64, C.c_uint32,
+                                         C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -151,6 +157,23 @@ def trace(scene, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01, check
     if ties:
         out.append(nt)
     return out[0] if len(out) == 1 else tuple(out)
+
+
+def trace_multi(scene, rays, k, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,
+                nthreads=None):
+    """Brute-force multi-hit: (hits [n, k] HIT_DTYPE, nhits uint32[n], ncut uint32[n])."""
+    sc = _as_scene(scene)
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty((n, k), dtype=HIT_DTYPE)
+    nh = np.zeros(n, dtype=np.uint32)
+    nc = np.zeros(n, dtype=np.uint32)
+    rc = lib().oracle_trace_multi(C.byref(sc.c), _ptr(r), n, k, isect, alpha_threshold,
+                                  checker_freq, _ptr(hits), _ptr(nh), _ptr(nc),
+                                  nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"oracle_trace_multi failed ({rc})")
+    return hits, nh, nc
 
 
 def eval_pair(scene, ray, prim, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8):
@@ -260,3 +283,19 @@ def walk(bvh: BvhArrays, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.0
     if rc != 0:
         raise ValueError(f"walker_trace failed ({rc})")
     return hits, counts
+
+
+def walk_multi(bvh: BvhArrays, rays, k, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,
+               nthreads=None):
+    """Contract walker C, multi-hit query: (hits [n, k], nhits, counts)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty((n, k), dtype=HIT_DTYPE)
+    nh = np.zeros(n, dtype=np.uint32)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    cb = bvh.c_struct()
+    rc = lib().walker_trace_multi(C.byref(cb), _ptr(r), n, k, isect, alpha_threshold, checker_freq,
+                                  _ptr(hits), _ptr(nh), _ptr(counts), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_multi failed ({rc})")
+    return hits, nh, counts

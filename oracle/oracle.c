@@ -179,9 +179,60 @@ typedef struct {
   or_hit* hits;
   uint32_t* flags;
   uint32_t* ntie;
+  uint32_t K;       /* multi-hit query: hits per ray (0 = closest/any) */
+  uint32_t* nhits;  /* multi-hit: accepted hits kept per ray (may be NULL) */
   uint64_t chunk; /* rays per claim */
   uint64_t next;  /* atomic chunk counter */
 } job_t;
+
+/* Multi-hit query, plain definition ("the first N hit
+ * points"): all accepted candidates of the ray (same test as
+ * above, tmax = ray.tmax), sorted ascending by t (equal t: lower index
+ * first), the first K kept; remaining slots hold the miss record. */
+typedef struct { float t, u, v; uint32_t prim; } cand_t;
+static int cmp_cand(const void* a, const void* b) {
+  const cand_t* x = (const cand_t*)a;
+  const cand_t* y = (const cand_t*)b;
+  if (x->t < y->t) return -1;
+  if (x->t > y->t) return 1;
+  return x->prim < y->prim ? -1 : (x->prim > y->prim ? 1 : 0);
+}
+
+static void trace_one_multi(const job_t* jb, uint64_t r) {
+  const or_scene* s = jb->s;
+  const float* ray = jb->rays + r * 8;
+  size_t cap = 64, cnt = 0;
+  cand_t* c = (cand_t*)malloc(sizeof(cand_t) * cap);
+  for (uint32_t i = 0; i < s->num_tris; ++i) {
+    const float* vt = s->vertices + (size_t)i * 9;
+    float t, u, v;
+    if (!oracle_mt(ray, vt, vt + 3, vt + 6, ray[7], &t, &u, &v)) continue;
+    if (degenerate(vt)) continue;
+    if (!filter(s, i, jb->isect, u, v, jb->thr, jb->M)) continue;
+    if (cnt == cap) {
+      cap *= 2;
+      c = (cand_t*)realloc(c, sizeof(cand_t) * cap);
+    }
+    c[cnt].t = t; c[cnt].u = u; c[cnt].v = v; c[cnt].prim = i;
+    cnt++;
+  }
+  qsort(c, cnt, sizeof(cand_t), cmp_cand);
+  const uint32_t K = jb->K;
+  for (uint32_t j = 0; j < K; ++j) {
+    or_hit* h = &jb->hits[r * K + j];
+    if (j < cnt) { h->t = c[j].t; h->u = c[j].u; h->v = c[j].v; h->prim = c[j].prim; }
+    else { h->t = INFINITY; h->u = 0.0f; h->v = 0.0f; h->prim = 0xFFFFFFFFu; }
+  }
+  if (jb->nhits) jb->nhits[r] = (uint32_t)(cnt < K ? cnt : K);
+  /* ties at the cut: how many accepted candidates share the K-th t (for parity) */
+  if (jb->ntie) {
+    uint32_t ties = 0;
+    if (cnt > K && K > 0)
+      for (size_t q = 0; q < cnt; ++q) ties += (c[q].t == c[K - 1].t);
+    jb->ntie[r] = ties;
+  }
+  free(c);
+}
 
 static void trace_one(const job_t* jb, uint64_t r) {
   const or_scene* s = jb->s;
@@ -266,10 +317,15 @@ static void* worker(void* arg) {
     uint64_t b = __atomic_fetch_add(&jb->next, chunk, __ATOMIC_RELAXED);
     if (b >= jb->n) break;
     uint64_t e = b + chunk < jb->n ? b + chunk : jb->n;
-    for (uint64_t r = b; r < e; ++r) trace_one(jb, r);
+    for (uint64_t r = b; r < e; ++r) {
+      if (jb->K) trace_one_multi(jb, r);
+      else trace_one(jb, r);
+    }
   }
   return NULL;
 }
+
+static int run_job(job_t* jb, int nthreads);
 
 int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, int isect,
                  float thr, uint32_t M, or_hit* hits, uint32_t* flags, uint32_t* ntie,
@@ -282,9 +338,27 @@ int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, in
   memset(&jb, 0, sizeof jb);
   jb.s = s; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect;
   jb.thr = thr; jb.M = M; jb.hits = hits; jb.flags = flags; jb.ntie = ntie; jb.next = 0;
+  return run_job(&jb, nthreads);
+}
+
+int oracle_trace_multi(const or_scene* s, const float* rays, uint64_t n, uint32_t K, int isect,
+                       float thr, uint32_t M, or_hit* hits, uint32_t* nhits, uint32_t* ncut,
+                       int nthreads) {
+  if (!s || !rays || !hits || K < 1) return -1;
+  if (isect < OR_NONE || isect > OR_COUNT) return -1;
+  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  job_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.s = s; jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect;
+  jb.thr = thr; jb.M = M; jb.hits = hits; jb.K = K; jb.nhits = nhits; jb.ntie = ncut;
+  return run_job(&jb, nthreads);
+}
+
+static int run_job(job_t* jbp, int nthreads) {
+  job_t jb = *jbp;
   if (nthreads < 1) nthreads = 1;
   /* up to 1024 rays per claim, fewer for small inputs so every thread gets work */
-  jb.chunk = n / ((uint64_t)nthreads * 4);
+  jb.chunk = jb.n / ((uint64_t)nthreads * 4);
   if (jb.chunk < 1) jb.chunk = 1;
   if (jb.chunk > 1024) jb.chunk = 1024;
   if (nthreads == 1) {

@@ -65,6 +65,14 @@ int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, in
                  float alpha_threshold, uint32_t checker_freq, or_hit* hits,
                  uint32_t* flags, uint32_t* ntie, int nthreads);
 
+/* Multi-hit query by brute force: the K smallest-t accepted hits per ray, ascending t,
+ * equal t by caller index; hits has n*K records (miss record in unused slots).
+ * nhits (optional): hits kept per ray; ncut (optional): number of accepted candidates
+ * whose t equals the K-th kept t when more than K were accepted (0 otherwise). */
+int oracle_trace_multi(const or_scene* s, const float* rays, uint64_t n, uint32_t K, int isect,
+                       float alpha_threshold, uint32_t checker_freq, or_hit* hits,
+                       uint32_t* nhits, uint32_t* ncut, int nthreads);
+
 /* One ray against one triangle (caller index) with the intersector's filter.
  * Returns 1 iff accepted (geometric hit and filter); fills *out either way
  * with the geometric t,u,v. */
@@ -120,6 +128,12 @@ void oracle_bvh_free(or_bvh* b);
 int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int isect,
                  float alpha_threshold, uint32_t checker_freq, or_hit* hits,
                  or_counts* counts, int nthreads);
+
+/* Walker C for the multi-hit query (GPU acceptance rule: stable insertion by t,
+ * a full buffer only takes t < its worst, tmax shrinks to the worst once full). */
+int walker_trace_multi(const or_bvh* b, const float* rays, uint64_t n, uint32_t K, int isect,
+                       float alpha_threshold, uint32_t checker_freq, or_hit* hits,
+                       uint32_t* nhits, or_counts* counts, int nthreads);
 
 /* Slab test of the walker (exposed for pins). Returns box hit; *tn entry
  * clipped to tmin, *tf exit times (1+2*gamma_3) before the best_t clip. */

@@ -327,11 +327,15 @@ typedef struct {
   int query, isect;
   float thr;
   uint32_t M;
-  or_hit* hits;
+  or_hit* hits;     /* K == 0: one per ray; K > 0: K per ray (multi-hit) */
   or_counts* counts;
+  uint32_t K;       /* multi-hit query: hits kept per ray (0 = closest/any) */
+  uint32_t* nhits;  /* multi-hit: hits kept per ray (may be NULL) */
   uint64_t next;
   int err;
 } wjob_t;
+
+#define MAX_MULTI 64
 
 static int walk_one(const wjob_t* jb, uint64_t r) {
   const or_bvh* b = jb->b;
@@ -353,6 +357,11 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
   int sp = 0;
   int bad = 0;
   float tn;
+  /* multi-hit buffer: ascending t, equal t in the order found; a full buffer
+     drops its worst and tmax shrinks to its last entry */
+  or_hit mb[MAX_MULTI];
+  uint32_t nk = 0;
+  const uint32_t K = jb->K;
 
   c.boxes++;
   if (!slab(b->root_lo, b->root_hi, o, inv, tmin, best_t, &tn)) goto done;
@@ -397,6 +406,19 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
         if (!mt_tri(tr, o, d, tmin, best_t, &t, &u, &v)) continue;
         if (jb->isect == OR_ALPHA_TEX) c.alpha++;
         if (!walk_filter(b, k, jb->isect, u, v, jb->thr, jb->M)) continue;
+        if (K) {
+          if (nk < K || t < best_t) {
+            uint32_t pos = nk < K ? nk : K - 1;
+            while (pos > 0 && mb[pos - 1].t > t) {
+              mb[pos] = mb[pos - 1];
+              pos--;
+            }
+            mb[pos].t = t; mb[pos].u = u; mb[pos].v = v; mb[pos].prim = tr->prim;
+            if (nk < K) nk++;
+            if (nk == K) best_t = mb[K - 1].t;
+          }
+          continue;
+        }
         if (jb->query == OR_ANY) {
           best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
           goto done;
@@ -418,7 +440,13 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
     }
   }
 done:
-  jb->hits[r] = best;
+  if (K) {
+    const or_hit miss = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
+    for (uint32_t j = 0; j < K; ++j) jb->hits[r * K + j] = j < nk ? mb[j] : miss;
+    if (jb->nhits) jb->nhits[r] = nk;
+  } else {
+    jb->hits[r] = best;
+  }
   if (jb->counts) jb->counts[r] = c;
   return bad;
 }
@@ -436,6 +464,8 @@ static void* wworker(void* arg) {
   return NULL;
 }
 
+static int walker_run(wjob_t* jb, int nthreads);
+
 int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int isect,
                  float thr, uint32_t M, or_hit* hits, or_counts* counts, int nthreads) {
   if (!b || !rays || !hits) return -1;
@@ -446,14 +476,31 @@ int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int 
   memset(&jb, 0, sizeof jb);
   jb.b = b; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr;
   jb.M = M; jb.hits = hits; jb.counts = counts;
+  return walker_run(&jb, nthreads);
+}
+
+int walker_trace_multi(const or_bvh* b, const float* rays, uint64_t n, uint32_t K, int isect,
+                       float thr, uint32_t M, or_hit* hits, uint32_t* nhits, or_counts* counts,
+                       int nthreads) {
+  if (!b || !rays || !hits || K < 1 || K > MAX_MULTI) return -1;
+  if (isect < OR_NONE || isect > OR_COUNT) return -1;
+  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  wjob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.b = b; jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect; jb.thr = thr;
+  jb.M = M; jb.hits = hits; jb.counts = counts; jb.K = K; jb.nhits = nhits;
+  return walker_run(&jb, nthreads);
+}
+
+static int walker_run(wjob_t* jb, int nthreads) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) {
-    wworker(&jb);
+    wworker(jb);
   } else {
     pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
-    for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, wworker, &jb);
+    for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, wworker, jb);
     for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
     free(th);
   }
-  return jb.err ? -1 : 0;
+  return jb->err ? -1 : 0;
 }

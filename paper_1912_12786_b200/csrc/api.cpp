@@ -547,6 +547,43 @@ vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query 
   return VSR_OK;
 }
 
+vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint32_t max_hits,
+                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                           uint32_t* d_num_hits, vsr_counts* d_counts, void* stream) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  if (max_hits < 1 || max_hits > 16) return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
+  if ((int)isect >= 100 && valid_isect(isect))
+    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for the multi-hit query");
+  TraceParams p;
+  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
+  if (n == 0) return VSR_OK;
+  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  if (!aligned16(d_rays) || !aligned16(d_hits))
+    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
+  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
+    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  p.rays = reinterpret_cast<const float4*>(d_rays);
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  p.max_hits = (int)max_hits;
+  p.num_hits = d_num_hits;
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  p.counter = next_counter(s);
+  cudaError_t e = launch_with_scratch(s, 2 /* multi */, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "multi-hit trace launch");
+  return VSR_OK;
+}
+
 vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_query query,
                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* h_hits,
                           vsr_counts* h_counts, void* stream) {

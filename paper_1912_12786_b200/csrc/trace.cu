@@ -32,7 +32,7 @@ namespace vsr {
 constexpr int kBlock = 128;
 constexpr uint32_t kMissPrim = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
-enum : int { kClosest = 0, kAny = 1 };
+enum : int { kClosest = 0, kAny = 1, kMulti = 2 };
 
 template <class I>
 __device__ __forceinline__ bool box_hook(I& isect, const RayCtx& r, const Aabb& b, float best_t,
@@ -149,17 +149,46 @@ __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, fl
   return true;
 }
 
+// Multi-hit accumulator ("the first N hit points"; SPEC
+// S:285-293): the maxk smallest-t accepted hits, ascending t, equal t in
+// discovery order; once full, tmax shrinks to the worst kept t.
+struct NoMulti {};
+template <int K>
+struct MultiBuf {
+  float t[K], u[K], v[K];
+  uint32_t prim[K];
+  int n;
+  int maxk;
+};
+
 // ---- leaf loop: "while node contains untested primitives" ----
 // Returns true when the query is finished (any-hit accepted a primitive).
-template <int Q, class I>
-__device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect) {
+template <int Q, class I, class M>
+__device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb) {
   const uint32_t first = T.cur & kLeafFirstMask;
   const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
   for (uint32_t k = first; k < end; ++k) {
     const float4* tp = reinterpret_cast<const float4*>(S.tris + k);
     const TriData td{__ldg(tp), __ldg(tp + 1), __ldg(tp + 2)};
     const hit_record hr = tri_hook(isect, T.r, td, k, T.best_t);
-    if (Q == kAny) {
+    if constexpr (Q == kMulti) {
+      if (hr.hit && (mb.n < mb.maxk || hr.t < T.best_t)) {
+        int pos = mb.n < mb.maxk ? mb.n : mb.maxk - 1;   // a full buffer drops its worst
+        while (pos > 0 && mb.t[pos - 1] > hr.t) {       // stable insertion by t
+          mb.t[pos] = mb.t[pos - 1];
+          mb.u[pos] = mb.u[pos - 1];
+          mb.v[pos] = mb.v[pos - 1];
+          mb.prim[pos] = mb.prim[pos - 1];
+          --pos;
+        }
+        mb.t[pos] = hr.t;
+        mb.u[pos] = hr.u;
+        mb.v[pos] = hr.v;
+        mb.prim[pos] = __float_as_uint(td.a.w);
+        if (mb.n < mb.maxk) ++mb.n;
+        if (mb.n == mb.maxk) T.best_t = mb.t[mb.maxk - 1];
+      }
+    } else if (Q == kAny) {
       if (hr.hit) {   // any-hit: the first accepted hit ends the query
         T.t = hr.t;
         T.u = hr.u;
@@ -184,17 +213,18 @@ __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect) {
 // to the next leaf, run its primitives, pop.  Returns true when the ray is done.
 template <int Q, int OCT, class I>
 __device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, float2* stack) {
+  NoMulti none;
   if (!descend<OCT>(S, T, isect, stack)) return true;
-  if (leaf<Q>(S, T, isect)) return true;
+  if (leaf<Q>(S, T, isect, none)) return true;
   return !pop(T, stack);
 }
 
 // Whole traversal of one ray.  `oct` is warp-uniform: 0..7 if every lane of
 // the warp has that octant (primary rays: all but the centre row/column
 // tiles), 8 otherwise; the switch is taken once per leaf, uniformly.
-template <int Q, class I>
+template <int Q, class I, class M = NoMulti>
 __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, float2* stack,
-                                         int oct) {
+                                         int oct, M& mb) {
   for (;;) {
     bool at_leaf;
     switch (oct) {
@@ -208,7 +238,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, f
       case 7: at_leaf = descend<7>(S, T, isect, stack); break;
       default: at_leaf = descend<-1>(S, T, isect, stack); break;
     }
-    if (!at_leaf || leaf<Q>(S, T, isect) || !pop(T, stack)) return;
+    if (!at_leaf || leaf<Q>(S, T, isect, mb) || !pop(T, stack)) return;
   }
 }
 
@@ -346,7 +376,8 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
     const unsigned live = __activemask();
     const int oct = ray_octant(T.r);
     const int woct = __match_any_sync(live, oct) == live ? oct : 8;
-    if (go) traverse<Q>(p.scene, T, isect, stack, woct);
+    NoMulti none;
+    if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
     finish(p, T, isect);
   }
 #ifdef VSR_TIMELINE
@@ -359,6 +390,36 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
     p.counts[id / 32] = make_uint4(smid, (unsigned)t0, (unsigned)t1, (unsigned)(t0 >> 32));
   }
 #endif
+}
+
+// Multi-hit query: same traversal, the leaf accepts into a K-entry sorted
+// buffer (runtime max_hits <= K).  Output ray-major: hits[id*max_hits + j].
+template <class I, int K>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_multi_kernel(const TraceParams p) {
+  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t id = blk * kBlock + threadIdx.x;
+  if (id >= p.n) return;
+  I isect = make_isect<I>(p);
+  Trav T;
+  float2 stack[kMaxStack];
+  MultiBuf<K> mb;
+  mb.n = 0;
+  mb.maxk = p.max_hits;
+  const bool go = start_ray(p, T, isect, id);
+  const unsigned live = __activemask();
+  const int oct = ray_octant(T.r);
+  const int woct = __match_any_sync(live, oct) == live ? oct : 8;
+  if (go) traverse<kMulti>(p.scene, T, isect, stack, woct, mb);
+  float4* out = p.hits + id * (uint64_t)p.max_hits;
+  for (int j = 0; j < mb.maxk; ++j) {
+    out[j] = j < mb.n ? make_float4(mb.t[j], mb.u[j], mb.v[j], __uint_as_float(mb.prim[j]))
+                      : make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                    __uint_as_float(kMissPrim));
+  }
+  if (p.num_hits) p.num_hits[id] = (uint32_t)mb.n;
+  if constexpr (I::kCounts) {
+    p.counts[id] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
+  }
 }
 
 // Persistent schedule (VSR_SCHED=persistent): grid sized to residency; warps
@@ -469,6 +530,29 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <class I>
+cudaError_t launch_multi(const TraceParams& p, cudaStream_t st) {
+  const uint64_t need = (p.n + kBlock - 1) / kBlock;
+  if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  if (p.max_hits <= 4) trace_multi_kernel<I, 4><<<(unsigned)need, kBlock, 0, st>>>(p);
+  else trace_multi_kernel<I, 16><<<(unsigned)need, kBlock, 0, st>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_multi(int isect, const TraceParams& p, cudaStream_t st) {
+  switch (isect) {
+    case VSR_ISECT_NONE: return launch_multi<no_intersector>(p, st);
+    case VSR_ISECT_DEFAULT: return launch_multi<default_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE: return launch_multi<alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL: return launch_multi<alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_COUNT: return launch_multi<cost_intersector<default_intersector>>(p, st);
+    case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+      return launch_multi<cost_intersector<alpha_texture_intersector>>(p, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int Q>
 cudaError_t dispatch_isect(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
@@ -548,8 +632,9 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p.perm = perm;
   }
-  cudaError_t e = query == kAny ? dispatch_isect<kAny>(isect, p, st)
-                                : dispatch_isect<kClosest>(isect, p, st);
+  cudaError_t e = query == kMulti ? dispatch_multi(isect, p, st)
+                  : query == kAny ? dispatch_isect<kAny>(isect, p, st)
+                                  : dispatch_isect<kClosest>(isect, p, st);
   if (owned) {
     cudaError_t f = cudaFreeAsync(scratch, st);
     if (e == cudaSuccess) e = f;

@@ -26,6 +26,8 @@ struct TraceParams {
   const uint32_t* perm;          // longest-first block permutation (set by launch_trace)
   void* order_scratch;           // optional stream-ordered scratch for the order pass
   size_t order_scratch_bytes;
+  int max_hits;                  // multi-hit query: hits kept per ray (1..16)
+  uint32_t* num_hits;            // multi-hit query: optional per-ray hit count
   int runtime_kind;
   void* filter_fn;
 };

@@ -42,7 +42,8 @@ MISS = 0xFFFFFFFF
 HIT_DTYPE = np.dtype([("t", "<f4"), ("u", "<f4"), ("v", "<f4"), ("prim", "<u4")])
 COUNTS_DTYPE = np.dtype([("boxes", "<u4"), ("tris", "<u4"), ("alpha", "<u4"), ("reserved", "<u4")])
 
-EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_host",
+EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
+                    "vsr_trace_host",
                     "vsr_destroy", "vsr_last_error", "vsr_bvh_export", "vsr_scene_import",
                     "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version"]
 
@@ -109,6 +110,8 @@ def lib():
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                      P, P, P]
+        L.vsr_trace_multi.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int,
+                                      C.POINTER(IsectParams), P, P, P, P]
         L.vsr_destroy.argtypes = [P]
         L.vsr_last_error.restype = C.c_char_p
         L.vsr_bvh_export.argtypes = [P, C.POINTER(BvhView)]
@@ -116,7 +119,8 @@ def lib():
         L.vsr_scene_stats.argtypes = [P, C.POINTER(Stats)]
         L.vsr_launch_count.restype = C.c_uint64
         L.vsr_abi_version.restype = C.c_uint32
-        for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_host",
+        for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
+                     "vsr_trace_host",
                      "vsr_destroy", "vsr_bvh_export", "vsr_scene_import", "vsr_scene_stats"):
             getattr(L, name).restype = C.c_int
         _lib = L
@@ -227,6 +231,25 @@ class Scene:
         _check(lib().vsr_trace(self._h, _ptr(rays), n, query, isect, C.byref(prm), _ptr(hits),
                                _ptr(counts), _stream_handle(stream)))
         return hits, counts
+
+    def trace_multi(self, rays, max_hits, isect=DEFAULT, hits=None, num_hits=None, counts=None,
+                    stream=None, alpha_threshold=0.01, checker_freq=8):
+        """vsr_trace_multi: the max_hits smallest-t accepted hits per ray, ascending.
+
+        Returns (hits [n, max_hits, 4] float32, num_hits [n] int32, counts or None)."""
+        import torch
+        n = rays.shape[0]
+        if hits is None:
+            hits = torch.empty((n, max_hits, 4), dtype=torch.float32, device=rays.device)
+        if num_hits is None:
+            num_hits = torch.empty((n,), dtype=torch.int32, device=rays.device)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_multi(self._h, _ptr(rays), n, max_hits, isect, C.byref(prm),
+                                     _ptr(hits), _ptr(num_hits), _ptr(counts),
+                                     _stream_handle(stream)))
+        return hits, num_hits, counts
 
     def trace_raw(self, rays_ptr, n, query, isect, hits_ptr, counts_ptr=None, stream=0,
                   alpha_threshold=0.01, checker_freq=8):
