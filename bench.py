@@ -225,7 +225,14 @@ def run_own(args):
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
+    multi_k = 4
+    multi_hits = None
+
     def trace(kind, query=q):
+        if query == "multi":   # multi-hit query, k = 4
+            scene.trace_multi(d_rays, multi_k, kind, hits=multi_hits, num_hits=multi_n,
+                              counts=counts, stream=sh)
+            return
         scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
                         counts.data_ptr(), sh)
 
@@ -309,6 +316,13 @@ def run_own(args):
             a_ms += timed(vsr.NONE, 1, 1)[0]
             b_ms += timed(vsr.DEFAULT, 1, 1)[0]
         extra["variants_mrays"] = var
+        # multi-hit query (4 nearest accepted hits per ray), same intersector
+        multi_hits = torch.empty((n, multi_k, 4), dtype=torch.float32, device="cuda")
+        multi_n = torch.empty((n,), dtype=torch.int32, device="cuda")
+        m, _ = timed(isect, max(5, args.steps // 2), 3, query="multi")
+        extra["multi_hit"] = {"k": multi_k, "value": round(n / (np.mean(m) * 1e-3) / 1e6, 1),
+                              "ms": round(float(np.mean(m)), 4)}
+        del multi_hits, multi_n
         extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
                               "default_ms": round(float(np.median(b_ms)), 4),
                               "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}
