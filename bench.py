@@ -236,35 +236,47 @@ def run_own(args):
         scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
                         counts.data_ptr(), sh)
 
-    def timed(kind, steps, warmup, query=q, sampler=None):
+    def timed(kind, steps, warmup, query=q, sampler=None, kernel_ms=None):
         for _ in range(warmup):
             flush_l2()
             trace(kind, query)
         torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
+        kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)] if kernel_ms is not None else None
+        for pair in kev or []:   # create the CUDA events (torch creates them on first record)
+            for e in pair:
+                e.record(stream)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         l0 = vsr.launch_count()
         ctx = sampler if sampler is not None else _Null()
         with ctx:
-            for a, b in evs:
+            for i, (a, b) in enumerate(evs):
                 flush_l2()
+                if kev:   # events around the trace kernel alone (after the order pass)
+                    vsr.set_kernel_events(*kev[i])
                 a.record(stream)
                 trace(kind, query)
                 b.record(stream)
             torch.cuda.synchronize()
+        vsr.set_kernel_events(None, None)
         launches = vsr.launch_count() - l0
         if world > 1:
             dist.barrier()
         ms = [a.elapsed_time(b) for a, b in evs]
+        if kev:
+            kernel_ms.extend(a.elapsed_time(b) for a, b in kev)
         return ms, launches
 
     # ---- headline ----
     sampler = ClockSampler(local)
-    ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler)
+    kms = []
+    ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler, kernel_ms=kms)
     ms_step = float(np.mean(ms))
+    ms_kernel = float(np.mean(kms))   # the trace kernel alone (roofline denominator)
     if world > 1:
         t = torch.tensor([ms_step], dtype=torch.float64, device=cdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -282,12 +294,16 @@ def run_own(args):
     cnp = vsr.counts_to_numpy(counts)
     bytes_launch, work = algorithmic_bytes(cnp, has_alpha)
     peak, peak_src = load_peaks()
-    achieved = bytes_launch / (ms_step * 1e-3) / 1e9
+    achieved = bytes_launch / (ms_kernel * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "bytes_per_ray": round(bytes_launch / n, 1), "work_per_ray": work,
-                "kernel": f"trace_kernel<{args.query}, {args.isect}>"}
+                "kernel": f"trace_kernel<{args.query}, {args.isect}>",
+                "kernel_ms": round(ms_kernel, 4),
+                "note": "algorithmic bytes (SURVEY.md 8(d)) mostly served by L1/L2: the scene is "
+                        "re-read per ray; DRAM traffic is `traffic` (ncu). The kernel is issue/"
+                        "latency-bound, see `issue`."}
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
@@ -295,6 +311,15 @@ def run_own(args):
             if tr:
                 roofline["traffic"] = tr["dram_bytes_per_launch"]
                 roofline["traffic_source"] = tr.get("source")
+                # issue roofline: ncu's warp-instruction count per launch over the live
+                # kernel time, against 148 SMs x 4 schedulers x 1 inst/clk at the sampled clock
+                mhz = sampler.summary().get("sm_mhz") or 1965.0
+                sms = torch.cuda.get_device_properties(local).multi_processor_count
+                ipeak = sms * 4 * mhz * 1e6
+                iach = tr["warp_instructions_per_launch"] / (ms_kernel * 1e-3)
+                roofline["issue"] = {"achieved": round(iach / 1e9, 1), "peak": round(ipeak / 1e9, 1),
+                                     "unit": "G warp-inst/s", "frac": round(iach / ipeak, 4),
+                                     "simt_threads_per_inst": tr.get("simt_threads_per_inst")}
         except Exception:
             pass
 

@@ -212,6 +212,11 @@ vsr_status vsr_scene_import(const vsr_bvh_view* view, int device, vsr_scene** ou
 
 vsr_status vsr_scene_stats(const vsr_scene* scene, vsr_stats* out);
 
+/* Profiling hook: on this thread, subsequent traces record `start` right before and
+ * `stop` right after the trace kernel itself (cudaEvent_t handles created by the caller on
+ * the scene's device; NULL, NULL disables).  The block-order pass runs before `start`. */
+vsr_status vsr_set_kernel_events(void* start, void* stop);
+
 /* Number of kernels this library has launched in this process (all scenes). */
 uint64_t vsr_launch_count(void);
 

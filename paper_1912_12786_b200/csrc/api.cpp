@@ -351,6 +351,14 @@ const char* vsr_last_error(void) { return g_err.c_str(); }
 
 uint64_t vsr_launch_count(void) { return launch_count(); }
 
+vsr_status vsr_set_kernel_events(void* start, void* stop) {
+  g_err.clear();
+  if ((start == nullptr) != (stop == nullptr))
+    return fail(VSR_ERR_INVALID_ARG, "set both events or neither");
+  set_kernel_events(start, stop);
+  return VSR_OK;
+}
+
 vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out) {
   g_err.clear();
   if (!desc || !out) return fail(VSR_ERR_INVALID_ARG, "NULL desc or out");

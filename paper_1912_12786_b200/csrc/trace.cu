@@ -585,6 +585,15 @@ cudaError_t filter_fn_pointer(int kind, void** out) {
   return e;
 }
 
+// Profiling hook (thread-local): events recorded right before and after the
+// trace kernel itself, i.e. excluding the block-order pass.
+thread_local void* g_kernel_events[2] = {nullptr, nullptr};
+
+void set_kernel_events(void* start, void* stop) {
+  g_kernel_events[0] = start;
+  g_kernel_events[1] = stop;
+}
+
 size_t order_scratch_bytes(uint64_t n) {
   const uint64_t nblocks = (n + kBlock - 1) / kBlock;
   return sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks);
@@ -632,9 +641,11 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p.perm = perm;
   }
+  if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
   cudaError_t e = query == kMulti ? dispatch_multi(isect, p, st)
                   : query == kAny ? dispatch_isect<kAny>(isect, p, st)
                                   : dispatch_isect<kClosest>(isect, p, st);
+  if (g_kernel_events[1]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[1]), st);
   if (owned) {
     cudaError_t f = cudaFreeAsync(scratch, st);
     if (e == cudaSuccess) e = f;

@@ -34,6 +34,7 @@ struct TraceParams {
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);
 size_t order_scratch_bytes(uint64_t n);
+void set_kernel_events(void* start, void* stop);
 cudaError_t filter_fn_pointer(int kind, void** out);
 uint64_t launch_count();
 

@@ -45,7 +45,8 @@ COUNTS_DTYPE = np.dtype([("boxes", "<u4"), ("tris", "<u4"), ("alpha", "<u4"), ("
 EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
                     "vsr_trace_host",
                     "vsr_destroy", "vsr_last_error", "vsr_bvh_export", "vsr_scene_import",
-                    "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version"]
+                    "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version",
+                    "vsr_set_kernel_events"]
 
 
 class VsrError(RuntimeError):
@@ -119,6 +120,8 @@ def lib():
         L.vsr_scene_stats.argtypes = [P, C.POINTER(Stats)]
         L.vsr_launch_count.restype = C.c_uint64
         L.vsr_abi_version.restype = C.c_uint32
+        L.vsr_set_kernel_events.argtypes = [P, P]
+        L.vsr_set_kernel_events.restype = C.c_int
         for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
                      "vsr_trace_host",
                      "vsr_destroy", "vsr_bvh_export", "vsr_scene_import", "vsr_scene_stats"):
@@ -134,6 +137,13 @@ def _check(status: int):
 
 def launch_count() -> int:
     return int(lib().vsr_launch_count())
+
+
+def set_kernel_events(start=None, stop=None):
+    """Profiling hook: record torch.cuda.Event `start`/`stop` around the trace kernel
+    itself (after the block-order pass) on this thread; None, None disables."""
+    h = lambda e: None if e is None else e.cuda_event  # noqa: E731
+    _check(lib().vsr_set_kernel_events(h(start), h(stop)))
 
 
 def _ptr(a):
