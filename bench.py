@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--max-leaf", type=int, default=2, help="BVH build: max triangles per leaf")
+    ap.add_argument("--sah-bins", type=int, default=16, help="BVH build: SAH bins per axis")
     return ap.parse_args()
 
 
@@ -201,11 +202,11 @@ def run_own(args):
     sc, rays = make_workload(args.config, rank)
     t0 = time.time()
     if world > 1:
-        base = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf) if rank == 0 else None
+        base = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf, sah_bins=args.sah_bins) if rank == 0 else None
         scene, _ = shard.broadcast_scene(base, local, dist,
                                          tensor_device=None if backend == "nccl" else "cpu")
     else:
-        scene = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf)
+        scene = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf, sah_bins=args.sah_bins)
     setup_s = time.time() - t0
     stats = scene.stats()
     n = rays.n
@@ -391,7 +392,7 @@ def run_own(args):
             "config": {**config_desc(args.config), "query": args.query, "intersector": args.isect,
                        "rays_per_gpu": n, "resolution": "1920x1080x1spp",
                        "triangles": int(stats["num_tris"]), "bvh_nodes": int(stats["num_nodes"]),
-                       "bvh": f"binned SAH, 16 bins, max_leaf {args.max_leaf}",
+                       "bvh": f"binned SAH, {args.sah_bins} bins, max_leaf {args.max_leaf}",
                        "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
                        "l2": "flushed before every timed step (read of a 256 MiB buffer, outside the events)",
                        "parallelism": f"rays sharded by frame, {world} rank(s), no data-path collective",
