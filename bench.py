@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--max-leaf", type=int, default=2, help="BVH build: max triangles per leaf")
     ap.add_argument("--sah-bins", type=int, default=16, help="BVH build: SAH bins per axis")
+    ap.add_argument("--mode", default="weak", choices=["weak", "tiles"],
+                    help="weak: a frame per rank; tiles: one frame's tiles over the ranks + gather")
     return ap.parse_args()
 
 
@@ -209,9 +211,18 @@ def run_own(args):
         scene = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf, sah_bins=args.sah_bins)
     setup_s = time.time() - t0
     stats = scene.stats()
-    n = rays.n
-    d_rays = torch.from_numpy(rays.data).cuda()
+    tiles = args.mode == "tiles"
+    tile_rays = 64 * rays.spp
+    if tiles:   # strong scaling: this rank's round-robin 8x8-tile shard of ONE frame
+        local_rays = rays.data[shard.rank_ray_indices(rays.n, tile_rays, rank, world)]
+    else:       # weak scaling: this rank's own frame
+        local_rays = rays.data
+    n = local_rays.shape[0]
+    d_rays = torch.from_numpy(np.ascontiguousarray(local_rays)).cuda()
     hits = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    gathered = None
+    if tiles and world > 1:
+        gathered = torch.empty((world * n, 4), dtype=torch.float32, device="cuda" if backend == "nccl" else "cpu")
     counts = torch.empty((n, 4), dtype=torch.int32, device="cuda")
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
     # L2 flush by READING a buffer > 2x L2: it evicts the scene, rays and hits
@@ -236,6 +247,9 @@ def run_own(args):
             return
         scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
                         counts.data_ptr(), sh)
+        if gathered is not None:   # tile mode: assemble the frame's hits on every rank
+            src = hits if backend == "nccl" else hits.cpu()
+            shard.gather_hits(src, rays.n, tile_rays, dist, out=gathered, reorder=False)
 
     def timed(kind, steps, warmup, query=q, sampler=None, kernel_ms=None):
         for _ in range(warmup):
@@ -354,7 +368,7 @@ def run_own(args):
                               "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}
 
     # ---- end to end through vsr_trace_host (pinned host buffers) ----
-    h_rays = torch.from_numpy(rays.data).pin_memory()
+    h_rays = torch.from_numpy(np.ascontiguousarray(local_rays)).pin_memory()
     h_hits = torch.empty((n, 4), dtype=torch.float32).pin_memory()
     for _ in range(2):
         scene.trace_host(h_rays, q, isect, hits=h_hits, stream=stream)
@@ -380,22 +394,25 @@ def run_own(args):
     # ---- cpu baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(sc, rays, args, target_s=args.cpu_seconds)
+        cpu = cpu_baseline(sc, rays, args, target_s=args.cpu_seconds, scene=scene)
 
     if rank == 0:
         clocks = sampler.summary()
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step_max, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if tiles else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic (seeded generators, workloads/)",
             "config": {**config_desc(args.config), "query": args.query, "intersector": args.isect,
-                       "rays_per_gpu": n, "resolution": "1920x1080x1spp",
+                       "rays_per_gpu": n, "resolution": f"{rays.width}x{rays.height}x{rays.spp}spp",
                        "triangles": int(stats["num_tris"]), "bvh_nodes": int(stats["num_nodes"]),
                        "bvh": f"binned SAH, {args.sah_bins} bins, max_leaf {args.max_leaf}",
                        "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
                        "l2": "flushed before every timed step (read of a 256 MiB buffer, outside the events)",
-                       "parallelism": f"rays sharded by frame, {world} rank(s), no data-path collective",
+                       "parallelism": (f"one frame's 8x8 tiles dealt round-robin over {world} rank(s), "
+                                       "hits all-gathered (NCCL) inside each step" if tiles else
+                                       f"rays sharded by frame, {world} rank(s), no data-path collective"),
                        "setup_s": round(setup_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "ms_per_step_each": [round(x, 4) for x in ms], **extra,
@@ -424,7 +441,7 @@ def _oracle_kind(name):
             "alpha_procedural": oracle.ALPHA_PROC, "count": oracle.DEFAULT}[base]
 
 
-def cpu_baseline(sc, rays, args, target_s=12.0):
+def cpu_baseline(sc, rays, args, target_s=12.0, scene=None):
     """Oracle S as it stands (brute force, all host cores) on a bounded seeded sample."""
     import oracle
     oq = oracle.CLOSEST if args.query == "closest" else oracle.ANY
@@ -445,9 +462,22 @@ def cpu_baseline(sc, rays, args, target_s=12.0):
         if dt >= 0.5 * target_s or m >= rays.n:
             break
         m = int(min(rays.n, m * target_s / max(dt, 1e-3)))
-    return {"value": round(m / dt / 1e6, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{m} seeded rays of the {rays.n}-ray frame, brute force vs all "
-                      f"{sc.num_tris} triangles, {dt:.1f} s", "cpu": cpu_model()}
+    out = {"value": round(m / dt / 1e6, 6), "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{m} seeded rays of the {rays.n}-ray frame, brute force vs all "
+                     f"{sc.num_tris} triangles, {dt:.1f} s", "cpu": cpu_model()}
+    if scene is not None:
+        # second, fairer CPU baseline: walker C, the contract BVH
+        # traversal, over the product's exported BVH, the full frame on all cores
+        from tests import bvh_check
+        b = bvh_check.to_oracle(scene.export())
+        oracle.walk(b, rays.data[: min(rays.n, 65536)], oq, ok, nthreads=cores)   # warm
+        t0 = time.perf_counter()
+        oracle.walk(b, rays.data, oq, ok, nthreads=cores)
+        wdt = time.perf_counter() - t0
+        out["walker"] = {"value": round(rays.n / wdt / 1e6, 3), "unit": UNIT, "cores": cores,
+                         "kind": "oracle walker C (BVH traversal, CPU)",
+                         "sample": f"full {rays.n}-ray frame, {wdt:.2f} s"}
+    return out
 
 
 def run_reference(args):

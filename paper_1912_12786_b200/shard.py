@@ -89,18 +89,26 @@ def broadcast_scene(scene_or_none, device, dist, src: int = 0, tensor_device=Non
     return Scene.import_arrays(host, device=-1), host
 
 
-def gather_hits(local_hits, n_total: int, rays_per_tile: int, dist, dst: int = 0):
-    """all_gather_into_tensor equal-size hit shards and scatter into tile order.
+def gather_hits(local_hits, n_total: int, rays_per_tile: int, dist, out=None, reorder=True):
+    """all_gather_into_tensor equal-size hit shards (and re-order into tile order).
 
     local_hits: [n_local, 4] float32 tensor.  Every rank's shard has the same size
-    (the tile counts divide P).  Returns the full [n_total, 4] tensor on every rank."""
+    (the tile counts divide P).  `out`: optional [world * n_local, 4] gather buffer.
+    Returns the full [n_total, 4] tensor on every rank (rank-major if not reorder)."""
     import torch
 
     world = dist.get_world_size()
     sizes = shard_sizes(n_total, rays_per_tile, world)
     assert len(set(sizes)) == 1, "tile counts must divide the world size"
-    gathered = torch.empty((world * sizes[0], 4), dtype=local_hits.dtype, device=local_hits.device)
-    dist.all_gather_into_tensor(gathered, local_hits.contiguous())
+    gathered = out if out is not None else torch.empty(
+        (world * sizes[0], 4), dtype=local_hits.dtype, device=local_hits.device)
+    if local_hits.is_cuda or dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(gathered, local_hits.contiguous())
+    else:   # gloo (CPU tests): list form
+        parts = list(gathered.view(world, sizes[0], 4).unbind(0))
+        dist.all_gather(parts, local_hits.contiguous())
+    if not reorder:
+        return gathered
     # rank r's j-th tile is global tile r + j*world
     g = gathered.view(world, sizes[0] // rays_per_tile, rays_per_tile, 4)
     return g.transpose(0, 1).reshape(n_total, 4)
