@@ -186,6 +186,25 @@ vsr_status vsr_trace_multi(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, 
                            vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                            uint32_t* d_num_hits, vsr_counts* d_counts, void* stream);
 
+/* A LIST of built scenes queried as one (BVHs act as compound primitives,
+ * the object hierarchy "may optionally have more than one root node", and the intersector is
+ * passed on into every BVH's traversal).  Untransformed (no instance matrices).  All scenes on
+ * one device; they must stay alive and unmodified while the group exists.  1 <= count <= 1024.
+ * Errors: INVALID_ARG (NULL, count, mixed devices), NOT_BUILT, UNSUPPORTED (host-only), CUDA, OOM. */
+typedef struct vsr_group vsr_group;
+vsr_status vsr_group_create(vsr_scene* const* scenes, uint32_t count, vsr_group** out);
+vsr_status vsr_group_destroy(vsr_group* group);   /* NULL is a no-op */
+
+/* Trace the list in order with one running best_t: closest = the min-t accepted hit over all
+ * elements (equal t: the earlier element); any = the first accepted hit (list order).  Each
+ * element's root box is tested and counted (counts are summed over the list).
+ * prim_id in d_hits is the index within the hit's own scene; d_which (optional, n uint32) gets
+ * that scene's list index (0xFFFFFFFF on a miss).  Other arguments as vsr_trace; the
+ * RUNTIME_* controls are not provided (VSR_ERR_UNSUPPORTED). */
+vsr_status vsr_trace_group(vsr_group* group, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                           uint32_t* d_which, vsr_counts* d_counts, void* stream);
+
 /* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
  * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
  * overlap the kernel; returns after the stream work completed. */

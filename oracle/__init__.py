@@ -94,6 +94,9 @@ def lib():
         L.walker_trace_multi.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_uint64, C.c_uint32,
                                          C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_int]
+        L.walker_trace_list.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_int,
+                                        C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -283,6 +286,23 @@ def walk(bvh: BvhArrays, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.0
     if rc != 0:
         raise ValueError(f"walker_trace failed ({rc})")
     return hits, counts
+
+
+def walk_list(bvhs, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,
+              nthreads=None):
+    """Contract walker C over a LIST of BVHs: (hits, which uint32[n], counts)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty(n, dtype=HIT_DTYPE)
+    which = np.empty(n, dtype=np.uint32)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    arr = (_Bvh * len(bvhs))(*[b.c_struct() for b in bvhs])
+    rc = lib().walker_trace_list(arr, len(bvhs), _ptr(r), n, query, isect, alpha_threshold,
+                                 checker_freq, _ptr(hits), _ptr(which), _ptr(counts),
+                                 nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_list failed ({rc})")
+    return hits, which, counts
 
 
 def walk_multi(bvh: BvhArrays, rays, k, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,

@@ -135,6 +135,13 @@ int walker_trace_multi(const or_bvh* b, const float* rays, uint64_t n, uint32_t 
                        float alpha_threshold, uint32_t checker_freq, or_hit* hits,
                        uint32_t* nhits, or_counts* counts, int nthreads);
 
+/* Walker C for a LIST of BVHs: walked in order with one running best_t;
+ * every element's root box is tested and counted; which (optional) gets the list index of
+ * the kept hit (0xFFFFFFFF on a miss); prims are indices within their own BVH. */
+int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uint64_t n,
+                      int query, int isect, float alpha_threshold, uint32_t checker_freq,
+                      or_hit* hits, uint32_t* which, or_counts* counts, int nthreads);
+
 /* Slab test of the walker (exposed for pins). Returns box hit; *tn entry
  * clipped to tmin, *tf exit times (1+2*gamma_3) before the best_t clip. */
 int walker_slab(const float* lo, const float* hi, const float* ray, float best_t, float* tn,

@@ -331,6 +331,9 @@ typedef struct {
   or_counts* counts;
   uint32_t K;       /* multi-hit query: hits kept per ray (0 = closest/any) */
   uint32_t* nhits;  /* multi-hit: hits kept per ray (may be NULL) */
+  const or_bvh* list; /* list query: nlist BVHs walked in order (else b alone) */
+  uint32_t nlist;
+  uint32_t* which;  /* list query: list index of the kept hit (may be NULL) */
   uint64_t next;
   int err;
 } wjob_t;
@@ -338,7 +341,7 @@ typedef struct {
 #define MAX_MULTI 64
 
 static int walk_one(const wjob_t* jb, uint64_t r) {
-  const or_bvh* b = jb->b;
+  const or_bvh* b = jb->nlist ? jb->list : jb->b;
   const float* ray = jb->rays + r * 8;
   const float* o = ray;
   const float* d = ray + 4;
@@ -363,8 +366,14 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
   uint32_t nk = 0;
   const uint32_t K = jb->K;
 
+  /* list query: the BVHs in order, one running best_t */
+  const uint32_t nb = jb->nlist ? jb->nlist : 1u;
+  uint32_t which = 0xFFFFFFFFu;
+  for (uint32_t li = 0; li < nb; ++li) {
+  if (jb->nlist) b = &jb->list[li];
+  sp = 0;
   c.boxes++;
-  if (!slab(b->root_lo, b->root_hi, o, inv, tmin, best_t, &tn)) goto done;
+  if (!slab(b->root_lo, b->root_hi, o, inv, tmin, best_t, &tn)) continue;
   uint32_t cur = b->root_ref;
   for (;;) {
     /* inner-node loop */
@@ -421,25 +430,30 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
         }
         if (jb->query == OR_ANY) {
           best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
+          which = li;
           goto done;
         }
         if (!have || t < best_t) {
           best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
           best_t = t;
           have = 1;
+          which = li;
         }
       }
     }
   pop:
     for (;;) {
-      if (sp == 0) goto done;
+      if (sp == 0) goto next_bvh;
       sp--;
       if (st_tn[sp] > best_t) continue;
       cur = st_ref[sp];
       break;
     }
   }
+  next_bvh:;
+  }
 done:
+  if (jb->which) jb->which[r] = which;
   if (K) {
     const or_hit miss = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
     for (uint32_t j = 0; j < K; ++j) jb->hits[r * K + j] = j < nk ? mb[j] : miss;
@@ -489,6 +503,21 @@ int walker_trace_multi(const or_bvh* b, const float* rays, uint64_t n, uint32_t 
   memset(&jb, 0, sizeof jb);
   jb.b = b; jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect; jb.thr = thr;
   jb.M = M; jb.hits = hits; jb.counts = counts; jb.K = K; jb.nhits = nhits;
+  return walker_run(&jb, nthreads);
+}
+
+int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uint64_t n,
+                      int query, int isect, float thr, uint32_t M, or_hit* hits, uint32_t* which,
+                      or_counts* counts, int nthreads) {
+  if (!list || nlist < 1 || !rays || !hits) return -1;
+  if (query != OR_CLOSEST && query != OR_ANY) return -1;
+  if (isect < OR_NONE || isect > OR_COUNT) return -1;
+  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  wjob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.b = list; jb.list = list; jb.nlist = nlist; jb.which = which;
+  jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr;
+  jb.M = M; jb.hits = hits; jb.counts = counts;
   return walker_run(&jb, nthreads);
 }
 

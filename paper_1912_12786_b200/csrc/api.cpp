@@ -592,6 +592,116 @@ vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   return VSR_OK;
 }
 
+}  // extern "C"
+
+struct vsr_group {
+  int device = 0;
+  std::vector<vsr_scene*> scenes;
+  DevScene* d_list = nullptr;
+  IsectData* d_data = nullptr;
+  float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};   // union of the roots (order-pass proxy)
+};
+
+extern "C" {
+
+vsr_status vsr_group_create(vsr_scene* const* scenes, uint32_t count, vsr_group** out) {
+  g_err.clear();
+  if (!scenes || !out) return fail(VSR_ERR_INVALID_ARG, "NULL scenes or out");
+  *out = nullptr;
+  if (count < 1 || count > 1024) return fail(VSR_ERR_INVALID_ARG, "count must be in [1, 1024]");
+  for (uint32_t k = 0; k < count; ++k) {
+    if (!scenes[k]) return fail(VSR_ERR_INVALID_ARG, "NULL scene in list");
+    if (scenes[k]->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene in list");
+    if (!scenes[k]->built) return fail(VSR_ERR_NOT_BUILT, "scene " + std::to_string(k) + " not built");
+    if (scenes[k]->device != scenes[0]->device)
+      return fail(VSR_ERR_INVALID_ARG, "all scenes of a group must be on one device");
+  }
+  vsr_group* g = new (std::nothrow) vsr_group();
+  if (!g) return fail(VSR_ERR_OOM, "group allocation");
+  g->device = scenes[0]->device;
+  g->scenes.assign(scenes, scenes + count);
+  std::vector<DevScene> list(count);
+  std::vector<IsectData> data(count);
+  for (int a = 0; a < 3; ++a) {
+    g->lo[a] = INFINITY;
+    g->hi[a] = -INFINITY;
+  }
+  for (uint32_t k = 0; k < count; ++k) {
+    list[k] = scenes[k]->dev;
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f};
+    for (int a = 0; a < 3; ++a) {
+      g->lo[a] = std::min(g->lo[a], scenes[k]->dev.root_lo[a]);
+      g->hi[a] = std::max(g->hi[a], scenes[k]->dev.root_hi[a]);
+    }
+  }
+  DeviceGuard dg(g->device);
+  cudaError_t e;
+  if ((e = cudaMalloc(&g->d_list, sizeof(DevScene) * count)) != cudaSuccess ||
+      (e = cudaMalloc(&g->d_data, sizeof(IsectData) * count)) != cudaSuccess ||
+      (e = cudaMemcpy(g->d_list, list.data(), sizeof(DevScene) * count, cudaMemcpyHostToDevice)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(g->d_data, data.data(), sizeof(IsectData) * count, cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+    cudaFree(g->d_list);
+    cudaFree(g->d_data);
+    delete g;
+    return cuda_fail(e, "group upload");
+  }
+  *out = g;
+  return VSR_OK;
+}
+
+vsr_status vsr_group_destroy(vsr_group* g) {
+  g_err.clear();
+  if (!g) return VSR_OK;
+  {
+    DeviceGuard dg(g->device);
+    cudaFree(g->d_list);
+    cudaFree(g->d_data);
+  }
+  delete g;
+  return VSR_OK;
+}
+
+vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                           uint32_t* d_which, vsr_counts* d_counts, void* stream) {
+  g_err.clear();
+  if (!g) return fail(VSR_ERR_INVALID_ARG, "NULL group");
+  if ((int)isect >= 100 && valid_isect(isect))
+    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for list queries");
+  TraceParams p;
+  vsr_status st = make_params(g->scenes[0], query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (n == 0) return VSR_OK;
+  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  if (!aligned16(d_rays) || !aligned16(d_hits))
+    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
+  if (d_which && (reinterpret_cast<uintptr_t>(d_which) & 3u))
+    return fail(VSR_ERR_INVALID_ARG, "which buffer must be 4-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  for (int a = 0; a < 3; ++a) {   // the order pass's cost proxy uses the union of the roots
+    p.scene.root_lo[a] = g->lo[a];
+    p.scene.root_hi[a] = g->hi[a];
+  }
+  p.rays = reinterpret_cast<const float4*>(d_rays);
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  p.list = g->d_list;
+  p.list_data = g->d_data;
+  p.list_count = (uint32_t)g->scenes.size();
+  p.which = d_which;
+  DeviceGuard dg(g->device);
+  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
+  cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "list trace launch");
+  return VSR_OK;
+}
+
 vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_query query,
                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* h_hits,
                           vsr_counts* h_counts, void* stream) {

@@ -422,6 +422,61 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_multi_kernel(const Tra
   }
 }
 
+// Point a mask intersector at list element s's texture data (the alpha
+// listing's "member variables", differ per BVH).
+template <class I>
+__device__ __forceinline__ void bind_scene_data(I& isect, const IsectData& d) {
+  if constexpr (std::is_base_of<alpha_texture_intersector, I>::value) {
+    isect.d.sides = d.sides;   // threshold / checker frequency stay the call's
+    isect.d.descs = d.descs;
+    isect.d.texels = d.texels;
+  } else {
+    (void)d;
+  }
+}
+
+// Query over a LIST of BVHs (BVHs act as compound
+// primitives; the intersector is passed on into each BVH's traversal).  The
+// list is walked linearly in order; every element's root box is tested (and
+// counted) with the current best_t, so a closer hit in an earlier BVH prunes
+// later ones.  `which` records the list index of the kept hit.
+template <int Q, class I>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const TraceParams p) {
+  const DevScene* list = p.list;
+  const IsectData* ldata = p.list_data;
+  const uint32_t count = p.list_count;
+  uint32_t* which = p.which;
+  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t id = blk * kBlock + threadIdx.x;
+  if (id >= p.n) return;
+  I isect = make_isect<I>(p);
+  Trav T;
+  float2 stack[kMaxStack];
+  start_ray(p, T, isect, id);   // loads the ray; p.scene is element 0 (root test redone below)
+  isect.reset();
+  const unsigned live = __activemask();
+  const int oct = ray_octant(T.r);
+  const int woct = __match_any_sync(live, oct) == live ? oct : 8;
+  uint32_t hit_in = 0xFFFFFFFFu;
+  NoMulti none;
+  for (uint32_t s = 0; s < count; ++s) {
+    const DevScene S = list[s];
+    bind_scene_data(isect, ldata[s]);
+    const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
+    float tn;
+    if (!box_hook(isect, T.r, root, T.best_t, tn)) continue;
+    const float t_before = T.t;
+    const uint32_t prim_before = T.prim;
+    T.cur = S.root_ref;
+    T.sp = 0;
+    traverse<Q>(S, T, isect, stack, woct, none);
+    if (T.t != t_before || T.prim != prim_before) hit_in = s;
+    if (Q == kAny && T.prim != kMissPrim) break;   // any-hit: the first accepted hit ends it
+  }
+  finish(p, T, isect);
+  if (which) which[id] = hit_in;
+}
+
 // Persistent schedule (VSR_SCHED=persistent): grid sized to residency; warps
 // claim kChunk rays per atomicAdd and refill idle lanes after each leaf once
 // `refill` lanes are idle.  Measured slower than the direct schedule on the
@@ -553,6 +608,29 @@ cudaError_t dispatch_multi(int isect, const TraceParams& p, cudaStream_t st) {
   }
 }
 
+template <int Q, class I>
+cudaError_t launch_list(const TraceParams& p, cudaStream_t st) {
+  const uint64_t need = (p.n + kBlock - 1) / kBlock;
+  if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  trace_list_kernel<Q, I><<<(unsigned)need, kBlock, 0, st>>>(p);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <int Q>
+cudaError_t dispatch_list(int isect, const TraceParams& p, cudaStream_t st) {
+  switch (isect) {
+    case VSR_ISECT_NONE: return launch_list<Q, no_intersector>(p, st);
+    case VSR_ISECT_DEFAULT: return launch_list<Q, default_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE: return launch_list<Q, alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL: return launch_list<Q, alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_COUNT: return launch_list<Q, cost_intersector<default_intersector>>(p, st);
+    case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+      return launch_list<Q, cost_intersector<alpha_texture_intersector>>(p, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int Q>
 cudaError_t dispatch_isect(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
@@ -642,7 +720,9 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     p.perm = perm;
   }
   if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
-  cudaError_t e = query == kMulti ? dispatch_multi(isect, p, st)
+  cudaError_t e = p.list ? (query == kAny ? dispatch_list<kAny>(isect, p, st)
+                                          : dispatch_list<kClosest>(isect, p, st))
+                  : query == kMulti ? dispatch_multi(isect, p, st)
                   : query == kAny ? dispatch_isect<kAny>(isect, p, st)
                                   : dispatch_isect<kClosest>(isect, p, st);
   if (g_kernel_events[1]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[1]), st);

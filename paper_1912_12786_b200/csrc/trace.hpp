@@ -28,6 +28,10 @@ struct TraceParams {
   size_t order_scratch_bytes;
   int max_hits;                  // multi-hit query: hits kept per ray (1..16)
   uint32_t* num_hits;            // multi-hit query: optional per-ray hit count
+  const DevScene* list;          // list query (device array) or nullptr
+  const IsectData* list_data;    // per-element mask data (device array)
+  uint32_t list_count;
+  uint32_t* which;               // list query: optional per-ray list index of the hit
   int runtime_kind;
   void* filter_fn;
 };

@@ -46,7 +46,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_trace_host",
                     "vsr_destroy", "vsr_last_error", "vsr_bvh_export", "vsr_scene_import",
                     "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version",
-                    "vsr_set_kernel_events"]
+                    "vsr_set_kernel_events", "vsr_group_create", "vsr_group_destroy",
+                    "vsr_trace_group"]
 
 
 class VsrError(RuntimeError):
@@ -122,6 +123,12 @@ def lib():
         L.vsr_abi_version.restype = C.c_uint32
         L.vsr_set_kernel_events.argtypes = [P, P]
         L.vsr_set_kernel_events.restype = C.c_int
+        L.vsr_group_create.argtypes = [P, C.c_uint32, C.POINTER(P)]
+        L.vsr_group_destroy.argtypes = [P]
+        L.vsr_trace_group.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
+                                      P, P, P, P]
+        for name in ("vsr_group_create", "vsr_group_destroy", "vsr_trace_group"):
+            getattr(L, name).restype = C.c_int
         for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
                      "vsr_trace_host",
                      "vsr_destroy", "vsr_bvh_export", "vsr_scene_import", "vsr_scene_stats"):
@@ -321,6 +328,45 @@ class Scene:
         h = C.c_void_p()
         _check(lib().vsr_scene_import(C.byref(v), device, C.byref(h)))
         return cls(device=device, _handle=h)
+
+
+class Group:
+    """A list of built scenes queried as one (vsr_group_create / vsr_trace_group)."""
+
+    def __init__(self, scenes):
+        self.scenes = list(scenes)   # keep the scenes alive while the group exists
+        arr = (C.c_void_p * len(self.scenes))(*[s._h.value for s in self.scenes])
+        self._h = C.c_void_p()
+        _check(lib().vsr_group_create(C.cast(arr, C.c_void_p), len(self.scenes),
+                                      C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().vsr_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def trace(self, rays, query=CLOSEST, isect=DEFAULT, hits=None, which=None, counts=None,
+              stream=None, alpha_threshold=0.01, checker_freq=8):
+        """Returns (hits [n, 4], which [n] int32 list index, counts or None)."""
+        import torch
+        n = rays.shape[0]
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
+        if which is None:
+            which = torch.empty((n,), dtype=torch.int32, device=rays.device)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_group(self._h, _ptr(rays), n, query, isect, C.byref(prm),
+                                     _ptr(hits), _ptr(which), _ptr(counts),
+                                     _stream_handle(stream)))
+        return hits, which, counts
 
 
 def hits_to_numpy(hits) -> np.ndarray:

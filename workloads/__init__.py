@@ -31,4 +31,6 @@ from .gen import (  # noqa: F401
     random_soup,
     random_rays,
     stacked_quads,
+    split_scene,
+    concat_scenes,
 )

@@ -34,6 +34,7 @@ class Scene:
     texcoords: np.ndarray
     geom_texture: np.ndarray
     textures: list = field(default_factory=list)
+    source_index: np.ndarray | None = None   # split_scene: original triangle indices
 
     @property
     def num_tris(self) -> int:
@@ -422,6 +423,41 @@ CONFIGS = {
     "C4": "1M-triangle terrain + 20k billboards, 1920×1080, counting intersector",
     "C5": "10M-triangle terrain + 100k billboards, 3840×2160×4 spp",
 }
+
+
+def split_scene(scene: Scene, k: int, axis: int = 0) -> list:
+    """Partition a scene's triangles into k sub-scenes by centroid slab along `axis`
+    (objects for list / compound-BVH queries).  Sub-scenes share the texture list and
+    geom -> texture table; each keeps its triangles in caller order."""
+    c = scene.vertices.reshape(-1, 3, 3)[:, :, axis].mean(axis=1)
+    edges = np.quantile(c, np.linspace(0, 1, k + 1))
+    out = []
+    for j in range(k):
+        m = (c >= edges[j]) & ((c < edges[j + 1]) if j < k - 1 else (c <= edges[j + 1]))
+        out.append(Scene(f"{scene.name}-part{j}", scene.vertices[m], scene.geom_ids[m],
+                         scene.texcoords[m], scene.geom_texture, scene.textures,
+                         np.nonzero(m)[0]))
+    return out
+
+
+def concat_scenes(scenes: list) -> tuple:
+    """One scene holding every sub-scene's triangles in list order (for brute force),
+    plus the start offset of each sub-scene's triangles."""
+    verts, gids, tcs, gtex, texs, offs = [], [], [], [], [], []
+    g_off = t_off = n_off = 0
+    for s in scenes:
+        offs.append(n_off)
+        verts.append(s.vertices)
+        tcs.append(s.texcoords)
+        gids.append(s.geom_ids.astype(np.uint64) + g_off)
+        gtex.append(s.geom_texture.astype(np.uint64) + t_off)
+        texs += list(s.textures)
+        g_off += len(s.geom_texture)
+        t_off += len(s.textures)
+        n_off += s.num_tris
+    sc = Scene("concat", np.concatenate(verts), np.concatenate(gids).astype(np.uint32),
+               np.concatenate(tcs), np.concatenate(gtex).astype(np.uint32), texs)
+    return sc, np.array(offs, dtype=np.int64)
 
 
 CAMERAS = {
