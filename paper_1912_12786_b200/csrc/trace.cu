@@ -18,6 +18,7 @@
 //
 // Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (IEEE fp32
 // contract).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -29,6 +30,7 @@
 
 namespace vsr {
 
+namespace cg = cooperative_groups;
 constexpr int kBlock = 128;
 constexpr uint32_t kMissPrim = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
@@ -355,6 +357,75 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
   if (b >= nblocks) return;
   const uint32_t s = slot[b];
   perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
+}
+
+// Both order phases in ONE cooperative launch (grid-wide barrier between the
+// histogram and the scatter); the grid is sized to be co-resident.
+__global__ void __launch_bounds__(256) order_coop_kernel(const TraceParams p, uint32_t nblocks,
+                                                         uint32_t* hist, uint32_t* slot,
+                                                         uint32_t* perm) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ uint32_t lh[kOrderBuckets], lbase[kOrderBuckets], start[kOrderBuckets];
+  const float dx = p.scene.root_hi[0] - p.scene.root_lo[0];
+  const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
+  const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
+  const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
+  const uint32_t total = 4 * nblocks;
+  const uint32_t stride = gridDim.x * 256;
+  for (uint32_t base = blockIdx.x * 256; base < total + 0; base += stride) {
+    const uint32_t t = base + threadIdx.x;
+    const uint32_t b = t >> 2;
+    float len = 0.0f;
+    if (b < nblocks) {
+      const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * 42u + ((t & 3u) == 3u ? 1u : 0u);
+      if (id < p.n) {
+        const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
+        RayCtx r;
+        make_ray(r, a, d);
+        const float t0x = (p.scene.root_lo[0] - r.ox) * r.ix, t1x = (p.scene.root_hi[0] - r.ox) * r.ix;
+        const float t0y = (p.scene.root_lo[1] - r.oy) * r.iy, t1y = (p.scene.root_hi[1] - r.oy) * r.iy;
+        const float t0z = (p.scene.root_lo[2] - r.oz) * r.iz, t1z = (p.scene.root_hi[2] - r.oz) * r.iz;
+        const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
+        const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
+        if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+      }
+    }
+    len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 1));
+    len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 2));
+    if (threadIdx.x < kOrderBuckets) lh[threadIdx.x] = 0;
+    __syncthreads();
+    const bool leader = (t & 3u) == 0u && b < nblocks;
+    int q = 0;
+    uint32_t lpos = 0;
+    if (leader) {
+      q = diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
+      q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
+      lpos = atomicAdd(lh + q, 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < kOrderBuckets && lh[threadIdx.x])
+      lbase[threadIdx.x] = atomicAdd(hist + threadIdx.x, lh[threadIdx.x]);
+    __syncthreads();
+    if (leader) slot[b] = ((uint32_t)q << 24) | (lbase[q] + lpos);
+    __syncthreads();
+  }
+  grid.sync();
+  if (threadIdx.x < 32) {   // exclusive scan over buckets, most expensive first
+    const unsigned lane = threadIdx.x;
+    const int q = kOrderBuckets - 1 - (int)lane;
+    const uint32_t cnt = __ldcg(hist + q);
+    uint32_t incl = cnt;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if ((int)lane >= o) incl += v;
+    }
+    start[q] = incl - cnt;
+  }
+  __syncthreads();
+  for (uint32_t b = blockIdx.x * 256 + threadIdx.x; b < nblocks; b += stride) {
+    const uint32_t s = __ldcg(slot + b);
+    perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
+  }
 }
 
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
@@ -711,11 +782,29 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     uint32_t* slot = hist + kOrderBuckets;
     uint32_t* perm = slot + nblocks;
     if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess) return e;
+#ifdef VSR_ORDER_COOP
+    {
+      static int coop_blocks = 0;
+      if (coop_blocks == 0) {
+        int nb = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, order_coop_kernel, 256, 0);
+        coop_blocks = (nb > 0 ? nb : 1) * sm_count();
+        if (coop_blocks > sm_count()) coop_blocks = sm_count();   // one CTA per SM is plenty
+      }
+      uint32_t nb32 = (uint32_t)nblocks;
+      void* args[] = {&p, &nb32, &hist, &slot, &perm};
+      if ((e = cudaLaunchCooperativeKernel((const void*)order_coop_kernel, coop_blocks, 256, args, 0,
+                                           st)) != cudaSuccess)
+        return e;
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+#else
     order_cost_kernel<<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(p, (uint32_t)nblocks,
                                                                              hist, slot);
     order_scatter_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, st>>>((uint32_t)nblocks, hist,
                                                                             slot, perm);
     g_launches.fetch_add(2, std::memory_order_relaxed);
+#endif
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p.perm = perm;
   }
