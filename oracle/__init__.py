@@ -71,8 +71,12 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(LIB_PATH)
+        mutant = os.environ.get("ORACLE_MUTANT_LIB")   # tools/mutate_oracle.py only
+        if mutant:
+            L = C.CDLL(mutant)
+        else:
+            build()
+            L = C.CDLL(LIB_PATH)
         L.oracle_trace.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_uint64, C.c_int, C.c_int,
                                    C.c_float, C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_int]

@@ -68,6 +68,12 @@ def test_mt_interval_inclusive_and_parallel(oracle_lib):
     assert not o.mt(np.array([.25, .25, 0, 1e-4, 1, 0, 0, INF], np.float32), *tri)[0]
     # behind the origin -> miss
     assert not o.mt(np.array([.25, .25, 1, 1e-4, 0, 0, 1, INF], np.float32), *tri)[0]
+    # the barycentric range is closed ("u >= 0, v >= 0, u+v <= 1"): rays exactly
+    # on the three edges (values exact in fp32 here) hit
+    for x, y in ((0.5, 0.5), (0.0, 0.5), (0.5, 0.0), (0.0, 0.0)):
+        hit, t, u, v = o.mt(np.array([x, y, -1, 1e-4, 0, 0, 1, INF], np.float32), *tri)
+        assert hit and u == x and v == y, (x, y)
+    assert not o.mt(np.array([0.5, 0.5000001, -1, 1e-4, 0, 0, 1, INF], np.float32), *tri)[0]
 
 
 def _plane_halfplane(ray, vt):
@@ -191,6 +197,13 @@ def test_alpha_threshold_inclusive(oracle_lib):
         h = oracle_lib.trace(sc, ray[None], isect=oracle_lib.ALPHA_TEX)
         assert (h["prim"][0] != 0xFFFFFFFF) == keep, a8
         assert (np.float32(a8) / np.float32(255) >= np.float32(GOLD["alpha_threshold"]["value"])) == keep
+    # inclusive at equality: threshold exactly a8/255 keeps a8 and rejects a8 - 1
+    for a8 in (3, 128, 255):
+        thr = float(np.float32(a8) / np.float32(255))
+        for val, keep in ((a8, True), (a8 - 1, False)):
+            h = oracle_lib.trace(_alpha_scene(val), ray[None], isect=oracle_lib.ALPHA_TEX,
+                                 alpha_threshold=thr)
+            assert (h["prim"][0] != 0xFFFFFFFF) == keep, (a8, val)
 
 
 def _hit_at_bary(u, v):

@@ -1,0 +1,111 @@
+"""Mutation check of the oracle pins (CPU only).
+
+Each mutant is a plausible mistake in oracle/*.c (a dropped term, a wrong sign
+or index, a swapped operand, a non-inclusive comparison, a missing wrap...).
+The mutant library is built from a patched copy and the CPU pin suites run
+against it (ORACLE_MUTANT_LIB); every mutant must make at least one pin fail.
+
+    python tools/mutate_oracle.py > profiles/r01_oracle_mutation.md
+"""
+import os
+import shutil
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ORACLE = os.path.join(ROOT, "oracle")
+PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py"]
+
+MUTANTS = [
+    # (file, original, mutated, description)
+    ("oracle.c", "o[0] = a[1] * b[2] - a[2] * b[1];", "o[0] = a[1] * b[2] + a[2] * b[1];",
+     "cross product: wrong sign in x"),
+    ("oracle.c", "o[1] = a[2] * b[0] - a[0] * b[2];", "o[1] = a[2] * b[1] - a[0] * b[2];",
+     "cross product: wrong index in y"),
+    ("oracle.c", "return (a[0] * b[0] + a[1] * b[1]) + a[2] * b[2];",
+     "return (a[0] * b[0] + a[1] * b[1]);", "dot product: dropped z term"),
+    ("oracle.c", "cross3(d, e2, p);", "cross3(e2, d, p);", "MT: transposed cross operands (p)"),
+    ("oracle.c", "*u = dot3(s, p) * inv;\n  cross3(s, e1, q);\n  *v = dot3(d, q) * inv;",
+     "*v = dot3(s, p) * inv;\n  cross3(s, e1, q);\n  *u = dot3(d, q) * inv;", "MT: u and v swapped"),
+    ("oracle.c", "(*u + *v <= 1.0f)", "(*u + *v < 1.0f)", "MT: edge test not inclusive"),
+    ("oracle.c", "(*t >= tmin) && (*t <= tmax_cur)", "(*t > tmin) && (*t <= tmax_cur)",
+     "MT: tmin not inclusive"),
+    ("oracle.c", "if (!(fabsf(det) >= 1e-12f)) return 0;", "if (!(det >= 1e-12f)) return 0;",
+     "MT: back faces culled"),
+    ("oracle.c", "float w = (1.0f - u) - v;\n  out[0]", "float w = (1.0f - u);\n  out[0]",
+     "lerp: dropped -v in the first weight"),
+    ("oracle.c", "out[1] = (w * a[1] + u * b[1]) + v * c[1];", "out[1] = (w * a[1] + v * b[1]) + u * c[1];",
+     "lerp: barycentrics swapped in t"),
+    ("oracle.c", "return ((i % m) + m) % m;\n}\nfloat oracle_tex_alpha",
+     "return i < 0 ? 0 : (i >= m ? m - 1 : i);\n}\nfloat oracle_tex_alpha", "tex2D: clamp instead of wrap"),
+    ("oracle.c", "uint8_t a8 = rgba[((size_t)j * w + (size_t)i) * 4 + 3];",
+     "uint8_t a8 = rgba[((size_t)i * h + (size_t)j) * 4 + 3];", "tex2D: transposed texel address"),
+    ("oracle.c", "uint8_t a8 = rgba[((size_t)j * w + (size_t)i) * 4 + 3];",
+     "uint8_t a8 = rgba[((size_t)j * w + (size_t)i) * 4 + 0];", "tex2D: red channel instead of alpha"),
+    ("oracle.c", "return a >= thr;\n  }\n  if (isect == OR_ALPHA_PROC)", "return a > thr;\n  }\n  if (isect == OR_ALPHA_PROC)",
+     "alpha threshold not inclusive"),
+    ("oracle.c", "return ((cu + cv) % 2) == 0;", "return ((cu + cv) % 2) == 1;", "checker parity inverted"),
+    ("oracle.c", "int cv = (int)floorf(v * fm);", "int cv = (int)floorf(u * fm);", "checker uses u twice"),
+    ("oracle.c", "if (!have || t < best.t) {", "if (!have || t > best.t) {", "closest: keeps the farthest"),
+    ("oracle.c", "    if (!filter(s, i, jb->isect, u, v, jb->thr, jb->M)) continue;\n    /* accepted */",
+     "    /* accepted */", "filter ignored in the brute force"),
+    ("oracle.c", "if (x->t < y->t) return -1;", "if (x->t > y->t) return -1;", "multi-hit sorted descending"),
+    ("walker.c", "float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));",
+     "float tn = fmaxf(fminf(t0x, t1x), fminf(t0y, t1y));", "slab: z slab and tmin dropped from tnear"),
+    ("walker.c", "if (tn1 < tn0) { nearr = nd->ref[1]; farr = nd->ref[0]; ftn = tn0; }",
+     "if (tn1 > tn0) { nearr = nd->ref[1]; farr = nd->ref[0]; ftn = tn0; }", "walker: far child first"),
+    ("walker.c", "      c.boxes += 2;", "      c.boxes += 1;", "walker: one box count per inner node"),
+    ("walker.c", "      if (st_tn[sp] > best_t) continue;", "", "walker: popped entries never culled"),
+    ("walker.c", "  c.boxes++;\n  if (!slab(b->root_lo", "  if (!slab(b->root_lo", "walker: root test not counted"),
+    ("walker.c", "        if (jb->isect == OR_ALPHA_TEX) c.alpha++;", "", "walker: alpha lookups not counted"),
+    ("walker.c", "ax[a][c] = lo[a];\n    ax[a][2 + c] = hi[a];", "ax[a][2 + c] = lo[a];\n    ax[a][c] = hi[a];",
+     "oracle BVH: lo/hi planes swapped in the node"),
+]
+
+
+def run():
+    rows = []
+    for fname, orig, mut, desc in MUTANTS:
+        tmp = tempfile.mkdtemp(prefix="mut_")
+        try:
+            for f in ("oracle.c", "walker.c", "oracle.h"):
+                shutil.copy(os.path.join(ORACLE, f), tmp)
+            path = os.path.join(tmp, fname)
+            src = open(path).read()
+            if orig not in src:
+                rows.append((desc, "NOT APPLIED (snippet not found)", ""))
+                continue
+            open(path, "w").write(src.replace(orig, mut, 1))
+            lib = os.path.join(tmp, "libmut.so")
+            b = subprocess.run(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-ffp-contract=off",
+                                "-fno-fast-math", "-pthread", "-D_GNU_SOURCE", "-w", "-o", lib,
+                                os.path.join(tmp, "oracle.c"), os.path.join(tmp, "walker.c"), "-lm"],
+                               capture_output=True, text=True)
+            if b.returncode != 0:
+                rows.append((desc, "does not compile", ""))
+                continue
+            env = dict(os.environ, ORACLE_MUTANT_LIB=lib)
+            r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                                *PINS], cwd=ROOT, env=env, capture_output=True, text=True,
+                               timeout=900)
+            failed = [ln.split("::")[-1].split(" ")[0] for ln in r.stdout.splitlines()
+                      if ln.startswith("FAILED")]
+            status = "killed" if r.returncode != 0 else "SURVIVED"
+            rows.append((desc, status, ", ".join(failed[:2])))
+        finally:
+            shutil.rmtree(tmp, ignore_errors=True)
+    return rows
+
+
+if __name__ == "__main__":
+    rows = run()
+    print("# r01 — oracle mutation check (CPU pins only)\n")
+    print("Each row patches one plausible mistake into a copy of `oracle/*.c`, builds it, and runs")
+    print("`" + " ".join(PINS) + "` against it. A pin suite is adequate if every mutant is killed.\n")
+    print("| mutant | result | first failing pin |")
+    print("|---|---|---|")
+    for d, s, f in rows:
+        print(f"| {d} | {s} | {f} |")
+    killed = sum(1 for _, s, _ in rows if s == "killed")
+    print(f"\n{killed} / {len(rows)} mutants killed.")
