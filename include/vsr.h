@@ -132,9 +132,11 @@ typedef struct vsr_scene vsr_scene;
  *            k holds (lo0.k, lo1.k, hi0.k, hi1.k) — child 0 / child 1 slab planes side by
  *            side; every child box must be finite with lo <= hi
  *   tris     48 B each: float v0[3]; uint32 prim_id; float e1[3]; 0; float e2[3]; 0
- *   sides    32 B each: float uv0[2],uv1[2],uv2[2]; uint32 texture; 0
+ *   sides    32 B each: float uv0[2],uv1[2],uv2[2]; uint32 texel_offset (first texel of the
+ *            triangle's texture in `texels`); uint32 dims = (W-1) | (H-1) << 16
  *   texdescs 16 B each: uint64 texel_offset; uint32 width, height
- *   texels    4 B each: RGBA8 packed little-endian (alpha = texel >> 24)
+ *   texels    1 B each: the textures' alpha channel (A8), row-major, textures back to back;
+ *            the mask intersector reads color.w only.  <= 2^32 texels
  * ref encoding: bit31 = leaf; leaf: bits 26..30 = count-1, bits 0..25 = first tri;
  * inner: node index.  root_ref may be a leaf (no nodes). */
 typedef struct {

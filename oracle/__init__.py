@@ -238,7 +238,7 @@ class BvhArrays:
     tris: np.ndarray         # uint32[num_tris, 12]   (48 B)
     sides: np.ndarray        # uint32[num_tris, 8]    (32 B)
     texdescs: np.ndarray     # uint32[num_textures, 4] (16 B: offset lo/hi, w, h)
-    texels: np.ndarray       # uint32[total texels]
+    texels: np.ndarray       # uint8[total texels]  (alpha plane)
 
     def c_struct(self):
         keep = [np.ascontiguousarray(x) for x in (self.nodes, self.tris, self.sides,
@@ -269,10 +269,11 @@ def build_bvh(scene, max_leaf: int = 4) -> BvhArrays:
     td = grab(b.texdescs, b.num_textures, 4)
     for row in td:
         total = max(total, int(row[0]) + (int(row[1]) << 32) + int(row[2]) * int(row[3]))
+    texels = (np.ctypeslib.as_array(C.cast(b.texels, C.POINTER(C.c_uint8)), shape=(total,)).copy()
+              if total else np.zeros(0, np.uint8))
     out = BvhArrays(b.root_ref, np.array(b.root_lo, dtype=np.float32),
                     np.array(b.root_hi, dtype=np.float32), grab(b.nodes, b.num_nodes, 16),
-                    grab(b.tris, b.num_tris, 12), grab(b.sides, b.num_tris, 8), td,
-                    grab(b.texels, total, 1).reshape(-1))
+                    grab(b.tris, b.num_tris, 12), grab(b.sides, b.num_tris, 8), td, texels)
     lib().oracle_bvh_free(C.byref(b))
     return out
 

@@ -97,8 +97,8 @@ typedef struct {          /* 48 B triangle: v0, prim_id, e1, 0, e2, 0 */
   float e1[3]; uint32_t pad1;
   float e2[3]; uint32_t pad2;
 } or_tri;
-typedef struct {          /* 32 B sidecar */
-  float uv[6]; uint32_t tex; uint32_t pad;
+typedef struct {          /* 32 B sidecar: texcoords, texture's first texel, (W-1)|(H-1)<<16 */
+  float uv[6]; uint32_t offset; uint32_t dims;
 } or_side;
 typedef struct {          /* 16 B texture descriptor */
   uint64_t offset; uint32_t w, h;
@@ -112,7 +112,7 @@ typedef struct {
   const or_tri* tris;
   const or_side* sides;
   const or_texdesc* texdescs;
-  const uint32_t* texels;   /* RGBA8 packed little-endian: a = texel >> 24 */
+  const uint8_t* texels;    /* alpha plane (A8), textures back to back */
 } or_bvh;
 
 /* Oracle-side BVH builder: object-median split on the widest centroid axis,

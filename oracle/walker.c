@@ -185,6 +185,20 @@ int oracle_build_bvh(const or_scene* s, uint32_t max_leaf, or_bvh* out) {
   range_bounds(&b, 0, m, lo, hi);
   pad_box(lo, hi);
 
+  /* textures: descriptors and the alpha plane (A8, textures back to back) */
+  uint32_t nt = s->num_textures;
+  or_texdesc* td = (or_texdesc*)calloc(nt ? nt : 1, sizeof(or_texdesc));
+  uint64_t total = 0;
+  for (uint32_t k = 0; k < nt; ++k) {
+    td[k].offset = total; td[k].w = s->tex_w[k]; td[k].h = s->tex_h[k];
+    total += (uint64_t)s->tex_w[k] * s->tex_h[k];
+  }
+  uint8_t* texels = (uint8_t*)malloc(total ? total : 1);
+  for (uint32_t k = 0; k < nt; ++k) {
+    const uint8_t* p = s->tex_rgba[k];
+    uint64_t cnt = (uint64_t)s->tex_w[k] * s->tex_h[k];
+    for (uint64_t q = 0; q < cnt; ++q) texels[td[k].offset + q] = p[4 * q + 3];
+  }
   or_tri* tris = (or_tri*)calloc(m, sizeof(or_tri));
   or_side* sides = (or_side*)calloc(m, sizeof(or_side));
   for (uint32_t k = 0; k < m; ++k) {
@@ -198,22 +212,9 @@ int oracle_build_bvh(const or_scene* s, uint32_t max_leaf, or_bvh* out) {
     tris[k].prim = i;
     memcpy(sides[k].uv, s->texcoords ? s->texcoords + (size_t)i * 6 : (const float[6]){0}, 24);
     uint32_t g = s->geom_ids ? s->geom_ids[i] : 0u;
-    sides[k].tex = s->geom_texture ? s->geom_texture[g] : g;
-  }
-  uint32_t nt = s->num_textures;
-  or_texdesc* td = (or_texdesc*)calloc(nt ? nt : 1, sizeof(or_texdesc));
-  uint64_t total = 0;
-  for (uint32_t k = 0; k < nt; ++k) {
-    td[k].offset = total; td[k].w = s->tex_w[k]; td[k].h = s->tex_h[k];
-    total += (uint64_t)s->tex_w[k] * s->tex_h[k];
-  }
-  uint32_t* texels = (uint32_t*)malloc(sizeof(uint32_t) * (total ? total : 1));
-  for (uint32_t k = 0; k < nt; ++k) {
-    const uint8_t* p = s->tex_rgba[k];
-    uint64_t cnt = (uint64_t)s->tex_w[k] * s->tex_h[k];
-    for (uint64_t q = 0; q < cnt; ++q)
-      texels[td[k].offset + q] = (uint32_t)p[4 * q] | ((uint32_t)p[4 * q + 1] << 8) |
-                                 ((uint32_t)p[4 * q + 2] << 16) | ((uint32_t)p[4 * q + 3] << 24);
+    uint32_t tex = s->geom_texture ? s->geom_texture[g] : g;
+    sides[k].offset = (uint32_t)td[tex].offset;
+    sides[k].dims = (td[tex].w - 1u) | ((td[tex].h - 1u) << 16);
   }
   out->root_ref = root;
   memcpy(out->root_lo, lo, sizeof lo);
@@ -306,10 +307,10 @@ static int walk_filter(const or_bvh* b, uint32_t k, int isect, float u, float v,
     float w = (1.0f - u) - v;
     float s = (w * sd->uv[0] + u * sd->uv[2]) + v * sd->uv[4];
     float t = (w * sd->uv[1] + u * sd->uv[3]) + v * sd->uv[5];
-    const or_texdesc* td = &b->texdescs[sd->tex];
-    long i = wrapi(s, td->w), j = wrapi(t, td->h);
-    uint32_t texel = b->texels[td->offset + (uint64_t)j * td->w + (uint64_t)i];
-    float a = (float)(texel >> 24) / 255.0f;
+    uint32_t w_tex = (sd->dims & 0xFFFFu) + 1u, h_tex = (sd->dims >> 16) + 1u;
+    long i = wrapi(s, w_tex), j = wrapi(t, h_tex);
+    uint8_t a8 = b->texels[(uint64_t)sd->offset + (uint64_t)j * w_tex + (uint64_t)i];
+    float a = (float)a8 / 255.0f;
     return a >= thr;
   }
   if (isect == OR_ALPHA_PROC) {

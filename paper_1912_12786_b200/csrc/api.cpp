@@ -52,7 +52,7 @@ struct DeviceGuard {
 
 struct HostTexture {
   uint32_t w, h;
-  std::vector<uint32_t> texels;   // packed RGBA8, alpha in the top byte
+  std::vector<uint8_t> texels;    // alpha channel (A8)
 };
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -86,13 +86,13 @@ struct vsr_scene {
   bool host_built = false;
   HostBvh host_bvh;
   std::vector<TexDesc> host_descs;
-  std::vector<uint32_t> host_pool;
+  std::vector<uint8_t> host_pool;
   DevScene dev{};
   PairNode* d_nodes = nullptr;
   Tri* d_tris = nullptr;
   Side* d_sides = nullptr;
   TexDesc* d_texdescs = nullptr;
-  uint32_t* d_texels = nullptr;
+  uint8_t* d_texels = nullptr;
   unsigned long long* d_counters = nullptr;   // persistent-kernel work counters
   std::atomic<uint32_t> launch_seq{0};
   uint64_t num_texels = 0;
@@ -222,7 +222,7 @@ vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const f
   s->stats.num_textures = num_textures;
   s->stats.num_texels = num_texels;
   s->stats.device_bytes = (uint64_t)num_nodes * 64 + (uint64_t)num_tris * 80 +
-                          (uint64_t)num_textures * 16 + num_texels * 4;
+                          (uint64_t)num_textures * 16 + num_texels;
   s->built = true;
   s->stats.built = 1;
   return VSR_OK;
@@ -425,8 +425,10 @@ vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out) {
       s->tri_tex[i] = t;
     }
     if (ntex == 0) {
-      s->textures.push_back(HostTexture{1, 1, {0xFFFFFFFFu}});   // implicit opaque white
+      s->textures.push_back(HostTexture{1, 1, {255u}});   // implicit opaque white
     } else {
+      // Only the alpha channel is kept: the mask listing reads color.w alone
+      // (PAPER.md:311-313), so the device pool is an A8 plane.
       s->textures.resize(ntex);
       for (uint32_t k = 0; k < ntex; ++k) {
         const vsr_texture_desc& t = desc->textures[k];
@@ -436,9 +438,7 @@ vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out) {
         size_t cnt = (size_t)t.width * t.height;
         h.texels.resize(cnt);
         const uint8_t* p = t.rgba8;
-        for (size_t q = 0; q < cnt; ++q)
-          h.texels[q] = (uint32_t)p[4 * q] | ((uint32_t)p[4 * q + 1] << 8) |
-                        ((uint32_t)p[4 * q + 2] << 16) | ((uint32_t)p[4 * q + 3] << 24);
+        for (size_t q = 0; q < cnt; ++q) h.texels[q] = p[4 * q + 3];
       }
     }
   } catch (const std::bad_alloc&) {
@@ -465,18 +465,7 @@ vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
     return fail(VSR_ERR_INVALID_ARG, "costs must be finite, intersection_cost > 0");
   if (s->num_tris_input == 0) return fail(VSR_ERR_EMPTY_SCENE, "empty scene: zero triangles");
   auto t0 = std::chrono::steady_clock::now();
-  HostBvh hb;
-  std::string err;
-  BuildInput in{s->vertices.data(), s->num_tris_input,
-                s->has_texcoords ? s->texcoords.data() : nullptr, s->tri_tex.data()};
-  vsr_status st;
-  try {
-    st = build_bvh(in, prm, hb, err);
-  } catch (const std::bad_alloc&) {
-    return fail(VSR_ERR_OOM, "host BVH build");
-  }
-  if (st != VSR_OK) return fail(st, err);
-  // texture pool
+  // texture pool (A8 plane) and per-texture descriptors
   std::vector<TexDesc> descs(s->textures.size());
   uint64_t total = 0;
   for (size_t k = 0; k < s->textures.size(); ++k) {
@@ -485,10 +474,24 @@ vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
     descs[k].h = s->textures[k].h;
     total += (uint64_t)descs[k].w * descs[k].h;
   }
-  std::vector<uint32_t> pool(total);
+  if (total > 0xFFFFFFFFull)
+    return fail(VSR_ERR_UNSUPPORTED, "more than 2^32 texels in total (32-bit sidecar offsets)");
+  std::vector<uint8_t> pool(total);
   for (size_t k = 0; k < s->textures.size(); ++k)
     std::memcpy(pool.data() + descs[k].offset, s->textures[k].texels.data(),
-                s->textures[k].texels.size() * 4);
+                s->textures[k].texels.size());
+  HostBvh hb;
+  std::string err;
+  BuildInput in{s->vertices.data(), s->num_tris_input,
+                s->has_texcoords ? s->texcoords.data() : nullptr, s->tri_tex.data(),
+                descs.data()};
+  vsr_status st;
+  try {
+    st = build_bvh(in, prm, hb, err);
+  } catch (const std::bad_alloc&) {
+    return fail(VSR_ERR_OOM, "host BVH build");
+  }
+  if (st != VSR_OK) return fail(st, err);
   if (s->device < 0) {
     // host-only scene: keep the flattened arrays for export (no device copy)
     s->free_device();
@@ -815,7 +818,7 @@ vsr_status vsr_bvh_export(const vsr_scene* s, vsr_bvh_view* view) {
                           {view->tris, h.tris.data(), (size_t)d.num_tris * 48},
                           {view->sides, h.sides.data(), (size_t)d.num_tris * 32},
                           {view->texdescs, s->host_descs.data(), (size_t)d.num_textures * 16},
-                          {view->texels, s->host_pool.data(), (size_t)s->num_texels * 4}};
+                          {view->texels, s->host_pool.data(), (size_t)s->num_texels}};
     for (const Item& it : items)
       if (it.dst && it.bytes) std::memcpy(it.dst, it.src, it.bytes);
     return VSR_OK;
@@ -825,7 +828,7 @@ vsr_status vsr_bvh_export(const vsr_scene* s, vsr_bvh_view* view) {
                         {view->tris, s->d_tris, (size_t)d.num_tris * 48},
                         {view->sides, s->d_sides, (size_t)d.num_tris * 32},
                         {view->texdescs, s->d_texdescs, (size_t)d.num_textures * 16},
-                        {view->texels, s->d_texels, (size_t)s->num_texels * 4}};
+                        {view->texels, s->d_texels, (size_t)s->num_texels}};
   for (const Item& it : items) {
     if (!it.dst || it.bytes == 0) continue;
     cudaError_t e = cudaMemcpy(it.dst, it.src, it.bytes, cudaMemcpyDefault);
@@ -840,6 +843,7 @@ vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) 
   *out = nullptr;
   if (v->num_tris == 0) return fail(VSR_ERR_EMPTY_SCENE, "imported BVH has no triangles");
   if (v->num_tris > kMaxTris) return fail(VSR_ERR_UNSUPPORTED, "more than 2^26 triangles");
+  if (v->num_texels > 0xFFFFFFFFull) return fail(VSR_ERR_UNSUPPORTED, "more than 2^32 texels");
   if (!v->tris || !v->sides || (v->num_nodes && !v->nodes) || !v->texdescs || !v->texels ||
       v->num_textures == 0)
     return fail(VSR_ERR_INVALID_ARG, "NULL array in view (or zero textures)");
@@ -867,7 +871,8 @@ vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) 
       return fail(VSR_ERR_INVALID_ARG, "texture descriptor " + std::to_string(k) + " out of range");
   }
   for (uint32_t k = 0; k < v->num_tris; ++k)
-    if (sides[k].tex >= v->num_textures)
+    if ((uint64_t)sides[k].texel_offset + (uint64_t)((sides[k].dims & 0xFFFFu) + 1u) *
+                                              ((sides[k].dims >> 16) + 1u) > v->num_texels)
       return fail(VSR_ERR_INVALID_ARG, "sidecar " + std::to_string(k) + " texture out of range");
   // Structure: reachable refs in range, every triangle in exactly one leaf, depth <= 64.
   std::vector<uint8_t> seen_tri(v->num_tris, 0), seen_node(v->num_nodes, 0);
@@ -923,7 +928,7 @@ vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) 
       s->host_pool.resize(v->num_texels);
       cudaError_t e;
       if ((e = to_host(h.tris.data(), v->tris, (size_t)v->num_tris * 48)) != cudaSuccess ||
-          (e = to_host(s->host_pool.data(), v->texels, (size_t)v->num_texels * 4)) != cudaSuccess) {
+          (e = to_host(s->host_pool.data(), v->texels, (size_t)v->num_texels)) != cudaSuccess) {
         delete s;
         return cuda_fail(e, "import copy");
       }

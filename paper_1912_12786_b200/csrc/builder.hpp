@@ -14,6 +14,7 @@ struct BuildInput {
   uint32_t num_tris;
   const float* texcoords;   // 6 per triangle or nullptr
   const uint32_t* tri_tex;  // resolved texture index per triangle
+  const TexDesc* tex_table; // per texture: offset in the A8 pool, width, height
 };
 
 struct HostBvh {

@@ -340,8 +340,9 @@ vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh&
       Side& s = out.sides[k];
       if (in.texcoords) std::memcpy(s.uv, in.texcoords + 6 * (size_t)p, sizeof s.uv);
       else std::memset(s.uv, 0, sizeof s.uv);
-      s.tex = in.tri_tex[p];
-      s.pad = 0;
+      const TexDesc& td = in.tex_table[in.tri_tex[p]];
+      s.texel_offset = (uint32_t)td.offset;
+      s.dims = pack_dims(td.w, td.h);
     }
   });
   return VSR_OK;

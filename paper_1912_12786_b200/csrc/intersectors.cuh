@@ -269,12 +269,12 @@ __device__ __forceinline__ bool alpha_keep(const IsectData& d, uint32_t k, float
   const float w = (1.0f - u) - v;
   const float s = (w * s0.x + u * s0.z) + v * s1.x;
   const float t = (w * s0.y + u * s0.w) + v * s1.y;
-  const uint4 td = __ldg(reinterpret_cast<const uint4*>(d.descs + __float_as_uint(s1.z)));
-  const uint64_t off = (uint64_t)td.x | ((uint64_t)td.y << 32);
-  const uint32_t i = wrap_texel(s, td.z);
-  const uint32_t j = wrap_texel(t, td.w);
-  const uint32_t texel = __ldg(d.texels + off + (uint64_t)j * td.z + i);
-  return (texel >> 24) >= d.a_min;
+  const uint32_t dims = __float_as_uint(s1.w);
+  const uint32_t tw = (dims & 0xFFFFu) + 1u, th = (dims >> 16) + 1u;
+  const uint32_t i = wrap_texel(s, tw);
+  const uint32_t j = wrap_texel(t, th);
+  const uint32_t a8 = __ldg(d.texels + (uint64_t)__float_as_uint(s1.z) + (uint64_t)j * tw + i);
+  return a8 >= d.a_min;
 }
 
 // §4 procedural mask, read as a barycentric checkerboard (readings A4/A5).

@@ -41,12 +41,17 @@ struct alignas(16) Tri {
 };
 static_assert(sizeof(Tri) == 48, "Tri must be 48 B");
 
+// Alpha sidecar: the three texcoords and the triangle's texture resolved to
+// its place in the alpha plane (byte offset) and its size, so a lookup is one
+// 32-B sidecar read and one byte read, with no descriptor indirection.
 struct alignas(16) Side {
   float uv[6];
-  uint32_t tex;
-  uint32_t pad;
+  uint32_t texel_offset;   // first texel of the texture in the A8 pool
+  uint32_t dims;           // (W - 1) | (H - 1) << 16
 };
 static_assert(sizeof(Side) == 32, "Side must be 32 B");
+
+inline uint32_t pack_dims(uint32_t w, uint32_t h) { return (w - 1u) | ((h - 1u) << 16); }
 
 struct alignas(16) TexDesc {
   uint64_t offset;
@@ -64,7 +69,7 @@ struct DevScene {
   const Tri* tris;
   const Side* sides;
   const TexDesc* texdescs;
-  const uint32_t* texels;
+  const uint8_t* texels;   // A8 alpha plane (the listing reads color.w only)
   uint32_t root_ref;
   float root_lo[3], root_hi[3];
   uint32_t num_nodes, num_tris, num_textures;
@@ -81,7 +86,7 @@ constexpr uint32_t kCounterSlots = 256;
 struct IsectData {
   const Side* sides;
   const TexDesc* descs;
-  const uint32_t* texels;
+  const uint8_t* texels;
   uint32_t a_min;   // smallest a8 with (float)a8/255.0f >= threshold (exact, host-derived)
   float fm;         // checker frequency M as float
 };

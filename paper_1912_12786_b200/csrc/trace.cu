@@ -31,7 +31,10 @@
 namespace vsr {
 
 namespace cg = cooperative_groups;
-constexpr int kBlock = 128;
+#ifndef VSR_BLOCK
+#define VSR_BLOCK 128
+#endif
+constexpr int kBlock = VSR_BLOCK;   // rays per thread block (= per order-pass unit)
 constexpr uint32_t kMissPrim = 0xFFFFFFFFu;
 constexpr unsigned kFull = 0xFFFFFFFFu;
 enum : int { kClosest = 0, kAny = 1, kMulti = 2 };
@@ -299,7 +302,7 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
   const uint32_t b = t >> 2;
   float len = 0.0f;
   if (b < nblocks) {
-    const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * 42u + ((t & 3u) == 3u ? 1u : 0u);
+    const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * (uint32_t)((kBlock - 1) / 3);
     if (id < p.n) {
       const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
       RayCtx r;
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(256) order_coop_kernel(const TraceParams p, ui
     const uint32_t b = t >> 2;
     float len = 0.0f;
     if (b < nblocks) {
-      const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * 42u + ((t & 3u) == 3u ? 1u : 0u);
+      const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * (uint32_t)((kBlock - 1) / 3);
       if (id < p.n) {
         const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
         RayCtx r;

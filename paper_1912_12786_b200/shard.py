@@ -67,21 +67,25 @@ def broadcast_scene(scene_or_none, device, dist, src: int = 0, tensor_device=Non
     dist.broadcast(meta, src)
     meta = meta.cpu().numpy()
     widths = {"nodes": 16, "tris": 12, "sides": 8, "texdescs": 4, "texels": 1}
+    # 32-bit words everywhere except the A8 alpha plane
+    dtypes = {"texels": (np.uint8, torch.uint8)}
     out = {"root_ref": int(meta[0]), "root_lo": meta[1:4].astype(np.float32),
            "root_hi": meta[4:7].astype(np.float32)}
     for k, key in enumerate(ARRAY_KEYS):
         rows = int(meta[7 + k])
         shape = (rows, widths[key]) if widths[key] > 1 else (rows,)
+        np_dt, t_dt = dtypes.get(key, (np.int32, torch.int32))
         if rank == src:
-            t = torch.from_numpy(arrs[key].view(np.int32).reshape(shape)).to(tdev)
+            t = torch.from_numpy(np.ascontiguousarray(arrs[key]).view(np_dt).reshape(shape)).to(tdev)
         else:
-            t = torch.empty(shape, dtype=torch.int32, device=tdev)
+            t = torch.empty(shape, dtype=t_dt, device=tdev)
         if t.numel():
             dist.broadcast(t, src)
         out[key] = t
     if rank == src and scene_or_none is not None and device >= 0:
         return scene_or_none, out
-    host = {k: (v.cpu().numpy().view(np.uint32) if hasattr(v, "cpu") else v) for k, v in out.items()}
+    host = {k: (v.cpu().numpy().view(np.uint8 if k == "texels" else np.uint32)
+                if hasattr(v, "cpu") else v) for k, v in out.items()}
     if device >= 0:
         # import straight from the device buffers the broadcast filled
         dev = {k: v for k, v in out.items()}

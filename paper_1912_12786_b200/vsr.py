@@ -298,7 +298,7 @@ class Scene:
             "tris": np.zeros((v.num_tris, 12), np.uint32),
             "sides": np.zeros((v.num_tris, 8), np.uint32),
             "texdescs": np.zeros((v.num_textures, 4), np.uint32),
-            "texels": np.zeros(v.num_texels, np.uint32),
+            "texels": np.zeros(v.num_texels, np.uint8),   # alpha plane (A8)
         }
         v.nodes, v.tris, v.sides, v.texdescs, v.texels = (
             _ptr(arrs["nodes"]) if v.num_nodes else None, _ptr(arrs["tris"]), _ptr(arrs["sides"]),

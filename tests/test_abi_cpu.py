@@ -183,7 +183,7 @@ def test_import_validation(vsr):
     assert _err(vsr, lambda: vsr.Scene.import_arrays(bad)) == vsr.ERR_INVALID_ARG
     bad = dict(e)
     bad["sides"] = e["sides"].copy()
-    bad["sides"][3, 6] = 99                          # texture index out of range
+    bad["sides"][3, 6] = 10 ** 6                     # texel offset past the alpha plane
     assert _err(vsr, lambda: vsr.Scene.import_arrays(bad)) == vsr.ERR_INVALID_ARG
     bad = dict(e)
     bad["root_ref"] = 0x80000000 | (3 << 26) | 198   # leaf range past the end

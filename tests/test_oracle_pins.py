@@ -458,9 +458,11 @@ def _hand_bvh(z_left=1.0, z_right=3.0, transparent_left=False):
             tf_[i, 4:7] = e1
             tf_[i, 8:11] = e2
             sf[i, 0:6] = [0, 0, 1, 0, 1, 1] if k == 0 else [0, 0, 1, 1, 0, 1]
+            # sidecar word 6 = first texel of the texture, word 7 = (W-1)|(H-1)<<16 (1x1)
             sides[i, 6] = 0 if (q == 0 and transparent_left) else 1
+            sides[i, 7] = 0
     texdescs = np.array([[0, 0, 1, 1], [1, 0, 1, 1]], np.uint32)
-    texels = np.array([0x00FFFFFF, 0xFFFFFFFF], np.uint32)
+    texels = np.array([0, 255], np.uint8)          # A8 plane: transparent, opaque
     return oracle_lib_bvh(0, np.array([0, 0, min(z_left, z_right)], f),
                           np.array([1, 1, max(z_left, z_right)], f), nodes, tris, sides, texdescs,
                           texels)

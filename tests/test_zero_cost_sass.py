@@ -54,11 +54,11 @@ def test_intersector_code_only_where_used(sass, q):
     alpha = _find(sass, q, "25alpha_texture_intersector")
     fnptr = _find(sass, q, "25runtime_fnptr_intersector")
     # the alpha listing adds sidecar, descriptor and texel loads
-    # 32-bit global loads: the block-order entry in every kernel, plus the
-    # RGBA8 texel fetch (tex2D) only where the alpha intersector is compiled in
-    texel = re.compile(r"^(@!?P\d\s+)?LDG\.E\.CONSTANT\b")
-    n32 = lambda fn: sum(1 for i in fn if texel.match(i))  # noqa: E731
-    assert n32(alpha) > n32(default)
+    # the byte load of the A8 alpha plane (tex2D) exists only where the alpha
+    # intersector is compiled in
+    texel = re.compile(r"^(@!?P\d\s+)?LDG\.E\.U8\b")
+    assert any(texel.match(i) for i in alpha)
+    assert not any(texel.match(i) for i in default)
     indirect = re.compile(r"^(@!?P\d\s+)?CALL\S*\s+R\d+")   # call through a register = fn pointer
     assert not any(indirect.match(i) for i in default)
     assert not any(indirect.match(i) for i in alpha)
