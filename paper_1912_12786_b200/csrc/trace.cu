@@ -9,12 +9,13 @@
 // intersector's numbers do not depend on which lanes share a warp — they are
 // deterministic and match the CPU walker bit for bit.
 //
-// Scheduling (B200): persistent warps.  The grid is sized to the occupancy
-// limit (148 SMs x resident blocks); every warp repeatedly claims rays from a
-// global counter (one atomicAdd per refill, ballot/popc compaction) and keeps
-// tracing.  A warp refills its idle lanes after each processed leaf as soon
-// as `refill` lanes are idle ("dynamic fetch"), so short rays (sky) do not
-// leave lanes idle behind long ones (forest) and there is no last-wave tail.
+// Scheduling (B200), measured in profiles/r01_tuning.md: one thread per ray,
+// 128-ray blocks launched longest-first (a small order pass estimates each
+// block's cost from its rays' segment inside the root box), so the blocks
+// whose single-ray latency would set the tail start first.  A persistent
+// dynamic-fetch kernel (warps claim rays from a global counter and refill
+// idle lanes) is kept as VSR_SCHED=persistent; it loses on coherent primary
+// rays.
 //
 // Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (IEEE fp32
 // contract).
