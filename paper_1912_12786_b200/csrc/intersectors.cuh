@@ -195,6 +195,7 @@ __device__ __forceinline__ hit_record intersect(const RayCtx& r, const TriData& 
   hr.k = k;
   const float e1x = tri.b.x, e1y = tri.b.y, e1z = tri.b.z;
   const float e2x = tri.c.x, e2y = tri.c.y, e2z = tri.c.z;
+#ifdef VSR_SCALAR_MT
   // p = cross(d, e2)
   const float px = r.dy * e2z - r.dz * e2y;
   const float py = r.dz * e2x - r.dx * e2z;
@@ -209,6 +210,39 @@ __device__ __forceinline__ hit_record intersect(const RayCtx& r, const TriData& 
   const float qz = sx * e1y - sy * e1x;
   const float v = ((r.dx * qx + r.dy * qy) + r.dz * qz) * inv;
   const float t = ((e2x * qx + e2y * qy) + e2z * qz) * inv;
+#else
+  // The same operations, the independent (x, y) pairs issued as FMUL2/FADD2
+  // (each lane one IEEE RN op, so every value is bit-identical to the scalar
+  // textbook order of DESIGN.md A.1; VSR_SCALAR_MT builds the scalar form).
+  // p = cross(d, e2)
+  const float px = r.dy * e2z - r.dz * e2y;
+  const float py = r.dz * e2x - r.dx * e2z;
+  const float pz = r.dx * e2y - r.dy * e2x;
+  const f2_t pxy = pk(px, py);
+  float ax, ay;
+  upk(mul2(pk(e1x, e1y), pxy), ax, ay);                 // (e1x*px, e1y*py)
+  const float det = (ax + ay) + e1z * pz;
+  const float inv = 1.0f / det;
+  float sx, sy;
+  upk(sub2(pk(r.ox, r.oy), pk(tri.a.x, tri.a.y)), sx, sy);
+  const float sz = r.oz - tri.a.z;
+  float bx, by;
+  upk(mul2(pk(sx, sy), pxy), bx, by);                   // (sx*px, sy*py)
+  const float U = (bx + by) + sz * pz;
+  // q = cross(s, e1)
+  const float qx = sy * e1z - sz * e1y;
+  const float qy = sz * e1x - sx * e1z;
+  const float qz = sx * e1y - sy * e1x;
+  const f2_t qxy = pk(qx, qy);
+  float cx, cy, gx, gy;
+  upk(mul2(pk(r.dx, r.dy), qxy), cx, cy);               // (dx*qx, dy*qy)
+  upk(mul2(pk(e2x, e2y), qxy), gx, gy);                 // (e2x*qx, e2y*qy)
+  const float V = (cx + cy) + r.dz * qz;
+  const float T = (gx + gy) + e2z * qz;
+  float u, v;
+  upk(mul2(pk(U, V), pk(inv, inv)), u, v);
+  const float t = T * inv;
+#endif
   hr.t = t;
   hr.u = u;
   hr.v = v;
