@@ -295,6 +295,8 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
+  const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
+  p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
   return VSR_OK;
 }
 
@@ -324,6 +326,9 @@ cudaError_t launch_with_scratch(vsr_scene* s, int query, int isect, TraceParams&
       o->ptr = nullptr;
       o->cap = 0;
       if ((e = cudaMalloc(&o->ptr, bytes)) != cudaSuccess) return e;
+      // the order histogram must be zero at each launch's entry (launch_trace
+      // keeps it so: the trace kernel re-zeroes it)
+      if ((e = cudaMemset(o->ptr, 0, bytes)) != cudaSuccess) return e;
       o->cap = bytes;
     }
     if ((e = cudaStreamWaitEvent(st, o->ev, 0)) != cudaSuccess) return e;

@@ -25,6 +25,7 @@
 #include <atomic>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "intersectors.cuh"
 #include "trace.hpp"
@@ -299,6 +300,7 @@ constexpr int kOrderBuckets = 32;
 
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
+  asm volatile("griddepcontrol.launch_dependents;");   // let the scatter kernel's CTAs launch
   const uint32_t t = blockIdx.x * 256 + threadIdx.x;   // 4 sample rays per 128-ray block
   const uint32_t b = t >> 2;
   float len = 0.0f;
@@ -345,10 +347,12 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
 __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, const uint32_t* hist,
                                                             const uint32_t* slot, uint32_t* perm) {
   __shared__ uint32_t start[kOrderBuckets];
+  asm volatile("griddepcontrol.launch_dependents;");   // the trace kernel may launch now ...
+  asm volatile("griddepcontrol.wait;" ::: "memory");    // ... and this one waits for the cost pass
   if (threadIdx.x < 32) {   // exclusive scan over buckets, most expensive first
     const unsigned lane = threadIdx.x;
     const int q = kOrderBuckets - 1 - (int)lane;
-    const uint32_t cnt = hist[q];
+    const uint32_t cnt = __ldcg(hist + q);
     uint32_t incl = cnt;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
   __syncthreads();
   const uint32_t b = blockIdx.x * 256 + threadIdx.x;
   if (b >= nblocks) return;
-  const uint32_t s = slot[b];
+  const uint32_t s = __ldcg(slot + b);
   perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
 }
 
@@ -432,6 +436,18 @@ __global__ void __launch_bounds__(256) order_coop_kernel(const TraceParams p, ui
   }
 }
 
+// First statement of every trace kernel.  After an order pass the kernel is a
+// programmatic dependent launch (PDL): its CTAs may be resident before the
+// scatter kernel ends, so it waits for it here (a no-op for a plain launch),
+// then reads the permutation through L2 (.cg: no L1 line from an earlier
+// launch of the same scratch can be hit) and re-zeroes the histogram for the
+// scratch's next use (the stream orders that after this launch).
+__device__ __forceinline__ uint64_t launch_block(const TraceParams& p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.hist_reset && blockIdx.x == 0 && threadIdx.x < kOrderBuckets) p.hist_reset[threadIdx.x] = 0u;
+  return p.perm ? (uint64_t)__ldcg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+}
+
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
@@ -440,7 +456,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
 #endif
-  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
   if (id < p.n) {
     I isect = make_isect<I>(p);
@@ -471,7 +487,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
 // buffer (runtime max_hits <= K).  Output ray-major: hits[id*max_hits + j].
 template <class I, int K>
 __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_multi_kernel(const TraceParams p) {
-  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
   if (id >= p.n) return;
   I isect = make_isect<I>(p);
@@ -521,7 +537,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const Trac
   const IsectData* ldata = p.list_data;
   const uint32_t count = p.list_count;
   uint32_t* which = p.which;
-  const uint64_t blk = p.perm ? (uint64_t)__ldg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+  const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
   if (id >= p.n) return;
   I isect = make_isect<I>(p);
@@ -637,6 +653,23 @@ int sm_count() {
   return cache[dev];
 }
 
+// <<<grid, block, 0, st>>>, as a programmatic dependent launch when `pdl`
+// (the kernel starts with griddepcontrol.wait, see launch_block).
+template <typename... Args, typename... Act>
+cudaError_t launch_k(void (*k)(Args...), uint64_t grid, unsigned block, bool pdl, cudaStream_t st,
+                     Act&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Act>(args)...);
+}
+
 template <int Q, class I>
 cudaError_t launch(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
@@ -654,7 +687,8 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
     trace_kernel_persistent<Q, I><<<blocks, kBlock, 0, st>>>(p);
   } else {
     if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-    trace_kernel<Q, I><<<(unsigned)need, kBlock, 0, st>>>(p);
+    cudaError_t e = launch_k(trace_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
+    if (e != cudaSuccess) return e;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
@@ -664,8 +698,10 @@ template <class I>
 cudaError_t launch_multi(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
   if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  if (p.max_hits <= 4) trace_multi_kernel<I, 4><<<(unsigned)need, kBlock, 0, st>>>(p);
-  else trace_multi_kernel<I, 16><<<(unsigned)need, kBlock, 0, st>>>(p);
+  const bool pdl = p.perm && p.pdl;
+  cudaError_t e = p.max_hits <= 4 ? launch_k(trace_multi_kernel<I, 4>, need, kBlock, pdl, st, p)
+                                  : launch_k(trace_multi_kernel<I, 16>, need, kBlock, pdl, st, p);
+  if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -687,7 +723,8 @@ template <int Q, class I>
 cudaError_t launch_list(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
   if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-  trace_list_kernel<Q, I><<<(unsigned)need, kBlock, 0, st>>>(p);
+  cudaError_t e = launch_k(trace_list_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
+  if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -756,6 +793,7 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
   if (p_in.n == 0) return cudaSuccess;
   TraceParams p = p_in;
   p.perm = nullptr;
+  p.hist_reset = nullptr;
   const uint64_t nblocks = (p.n + kBlock - 1) / kBlock;
   void* scratch = nullptr;
   bool owned = false;
@@ -785,7 +823,14 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     uint32_t* hist = static_cast<uint32_t*>(scratch);
     uint32_t* slot = hist + kOrderBuckets;
     uint32_t* perm = slot + nblocks;
-    if ((e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess) return e;
+#ifdef VSR_ORDER_COOP
+    const bool zeroed = false;
+#else
+    const bool zeroed = !owned;   // caller scratch: zero at entry, kept so by the trace kernel
+#endif
+    if (!zeroed &&
+        (e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess)
+      return e;
 #ifdef VSR_ORDER_COOP
     {
       static int coop_blocks = 0;
@@ -805,9 +850,15 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
 #else
     order_cost_kernel<<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(p, (uint32_t)nblocks,
                                                                              hist, slot);
-    order_scatter_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, st>>>((uint32_t)nblocks, hist,
-                                                                            slot, perm);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = launch_k(order_scatter_kernel, (nblocks + 255) / 256, 256, p.pdl != 0, st,
+                      (uint32_t)nblocks, (const uint32_t*)hist, (const uint32_t*)slot, perm)) !=
+        cudaSuccess) {
+      if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
+      return e;
+    }
     g_launches.fetch_add(2, std::memory_order_relaxed);
+    if (!owned) p.hist_reset = hist;   // the trace kernel re-zeroes it for the next launch
 #endif
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p.perm = perm;
@@ -819,6 +870,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
                   : query == kAny ? dispatch_isect<kAny>(isect, p, st)
                                   : dispatch_isect<kClosest>(isect, p, st);
   if (g_kernel_events[1]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[1]), st);
+  if (e != cudaSuccess && p.hist_reset)   // the trace kernel did not run: restore the invariant
+    cudaMemsetAsync(p.hist_reset, 0, sizeof(uint32_t) * kOrderBuckets, st);
   if (owned) {
     cudaError_t f = cudaFreeAsync(scratch, st);
     if (e == cudaSuccess) e = f;

@@ -24,6 +24,8 @@ struct TraceParams {
   int sched;                     // kSchedDirect (default) or kSchedPersistent
   int order;                     // 1: launch blocks longest-first (direct schedule)
   const uint32_t* perm;          // longest-first block permutation (set by launch_trace)
+  uint32_t* hist_reset;          // order histogram the trace kernel re-zeroes (set by launch_trace)
+  int pdl;                       // launch the order pass + trace kernel as PDL dependents
   void* order_scratch;           // optional stream-ordered scratch for the order pass
   size_t order_scratch_bytes;
   int max_hits;                  // multi-hit query: hits kept per ray (1..16)
