@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="own", choices=["own", "reference"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--query", default="closest", choices=["closest", "any"])
+    ap.add_argument("--query", default="any", choices=["closest", "any"])
     ap.add_argument("--isect", default="alpha_texture")
     ap.add_argument("--no-variants", action="store_true", help="skip the C3 intersector sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")

@@ -66,6 +66,19 @@ __device__ __forceinline__ void make_ray(RayCtx& r, float4 a, float4 b) {
   r.iz = 1.0f / (fabsf(b.z) > 0x1p-80f ? b.z : copysignf(0x1p-80f, b.z));
 }
 
+// Three-input min/max (sm_100 FMNMX3).  min/max are exact and, NaN operands
+// being ignored, associative: max3(a, b, c) == fmaxf(fmaxf(a, b), c) bit for bit.
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fmin3(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 struct Aabb {
   float lx, ly, lz, hx, hy, hz;
 };
@@ -110,8 +123,8 @@ __device__ __forceinline__ bool intersect(const RayCtx& r, const Aabb& b, float 
   const float t0x = (b.lx - r.ox) * r.ix, t1x = (b.hx - r.ox) * r.ix;
   const float t0y = (b.ly - r.oy) * r.iy, t1y = (b.hy - r.oy) * r.iy;
   const float t0z = (b.lz - r.oz) * r.iz, t1z = (b.hz - r.oz) * r.iz;
-  const float n = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), r.tmin));
-  float f = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
+  const float n = fmax3(fminf(t0x, t1x), fminf(t0y, t1y), fmaxf(fminf(t0z, t1z), r.tmin));
+  float f = fmin3(fmaxf(t0x, t1x), fmaxf(t0y, t1y), fmaxf(t0z, t1z)) * 1.0000003576f;
   f = fminf(f, best_t);
   tn = n;
   return n <= f;
@@ -132,10 +145,10 @@ __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair&
   upk(mul2(sub2(pk(b.z.x, b.z.y), oz2), iz2), t0z0, t0z1);
   upk(mul2(sub2(pk(b.z.z, b.z.w), oz2), iz2), t1z0, t1z1);
   BoxPairHit h;
-  h.tn0 = fmaxf(fmaxf(fminf(t0x0, t1x0), fminf(t0y0, t1y0)), fmaxf(fminf(t0z0, t1z0), r.tmin));
-  h.tn1 = fmaxf(fmaxf(fminf(t0x1, t1x1), fminf(t0y1, t1y1)), fmaxf(fminf(t0z1, t1z1), r.tmin));
-  const float f0 = fminf(fminf(fmaxf(t0x0, t1x0), fmaxf(t0y0, t1y0)), fmaxf(t0z0, t1z0));
-  const float f1 = fminf(fminf(fmaxf(t0x1, t1x1), fmaxf(t0y1, t1y1)), fmaxf(t0z1, t1z1));
+  h.tn0 = fmax3(fminf(t0x0, t1x0), fminf(t0y0, t1y0), fmaxf(fminf(t0z0, t1z0), r.tmin));
+  h.tn1 = fmax3(fminf(t0x1, t1x1), fminf(t0y1, t1y1), fmaxf(fminf(t0z1, t1z1), r.tmin));
+  const float f0 = fmin3(fmaxf(t0x0, t1x0), fmaxf(t0y0, t1y0), fmaxf(t0z0, t1z0));
+  const float f1 = fmin3(fmaxf(t0x1, t1x1), fmaxf(t0y1, t1y1), fmaxf(t0z1, t1z1));
   float g0, g1;
   upk(mul2(pk(f0, f1), pk(1.0000003576f, 1.0000003576f)), g0, g1);
   h.h0 = h.tn0 <= fminf(g0, best_t);
@@ -171,10 +184,10 @@ __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair&
   upk(mul2(sub2(sz ? hiz : loz, oz2), iz2), nz0, nz1);
   upk(mul2(sub2(sz ? loz : hiz, oz2), iz2), fz0, fz1);
   BoxPairHit h;
-  h.tn0 = fmaxf(fmaxf(nx0, ny0), fmaxf(nz0, r.tmin));
-  h.tn1 = fmaxf(fmaxf(nx1, ny1), fmaxf(nz1, r.tmin));
+  h.tn0 = fmax3(nx0, ny0, fmaxf(nz0, r.tmin));
+  h.tn1 = fmax3(nx1, ny1, fmaxf(nz1, r.tmin));
   float g0, g1;
-  upk(mul2(pk(fminf(fminf(fx0, fy0), fz0), fminf(fminf(fx1, fy1), fz1)),
+  upk(mul2(pk(fmin3(fx0, fy0, fz0), fmin3(fx1, fy1, fz1)),
            pk(1.0000003576f, 1.0000003576f)),
       g0, g1);
   h.h0 = h.tn0 <= fminf(g0, best_t);
