@@ -366,6 +366,35 @@ def run_own(args):
         extra["multi_hit"] = {"k": multi_k, "value": round(n / (np.mean(m) * 1e-3) / 1e6, 1),
                               "ms": round(float(np.mean(m)), 4)}
         del multi_hits, multi_n
+        # NEXT-2: two-level instancing — instanced tree models over the
+        # same ground square, this rank's frame, same query and intersector
+        import workloads as W
+        models, ibvh, imat = W.instanced_forest()
+        iscenes = [vsr.Scene.from_workload(s, device=local).build() for s in models]
+        inst = vsr.Instances(iscenes, ibvh, imat)
+        inst_ids = torch.empty((n,), dtype=torch.int32, device="cuda")
+
+        def trace_inst():
+            inst.trace(d_rays, q, isect, hits=hits, inst=inst_ids, stream=stream)
+
+        for _ in range(3):
+            flush_l2()
+            trace_inst()
+        torch.cuda.synchronize()
+        ievs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(max(5, args.steps // 2))]
+        for a, b in ievs:
+            flush_l2()
+            a.record(stream)
+            trace_inst()
+            b.record(stream)
+        torch.cuda.synchronize()
+        im = float(np.mean([a.elapsed_time(b) for a, b in ievs]))
+        extra["instanced"] = {"workload": f"{len(ibvh)} instances of {len(models)} tree models "
+                                          f"({models[0].num_tris} tris each), C2 camera",
+                              "value": round(n / (im * 1e-3) / 1e6, 1), "ms": round(im, 4),
+                              "hit_fraction": round(float((inst_ids != -1).float().mean()), 3)}
+        del inst, iscenes, inst_ids
         extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
                               "default_ms": round(float(np.median(b_ms)), 4),
                               "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}

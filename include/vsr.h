@@ -207,6 +207,59 @@ vsr_status vsr_trace_group(vsr_group* group, const vsr_ray* d_rays, uint64_t n, 
                            vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                            uint32_t* d_which, vsr_counts* d_counts, void* stream);
 
+/* Two-level INSTANCING ("object instancing, where the BVH will store BVHs as
+ * primitives"): a top-level BVH (binned SAH, built here, untimed) over instances, each showing
+ * one built scene through an affine map.  A ray reaching an instance in the top-level traversal
+ * is mapped into the instance's object space and traverses that scene's BVH with the same
+ * intersector and the same running best_t (closest: min t over all instances; any: the first
+ * accepted hit in traversal order).
+ *
+ * vsr_instance.object_from_world: row-major 3x4 [A | b] taking WORLD points to OBJECT points,
+ * p_obj = A p + b.  The ray maps, in fp32 in exactly this order (reading A27):
+ *   o'_i = ((A_i0*o_x + A_i1*o_y) + A_i2*o_z) + b_i,   d'_i = (A_i0*d_x + A_i1*d_y) + A_i2*d_z,
+ * tmin and tmax unchanged, so t is the same parameter in both spaces.  A must be finite and
+ * invertible (|det A| > 1e-30 in fp64).  Instance world boxes: the scene's padded root box mapped
+ * by the fp64 inverse, then padded outward by 2^-10 of (box diagonal + max |coordinate|)
+ * (conservative for rays whose origin lies within ~1000 scene diagonals; reading A27).
+ * Scenes: built, one device, alive and unmodified while the object exists; 1..1024 scenes,
+ * 1..2^26 instances.  Host-only scenes (device -1) give host-only instances: built and
+ * exportable, not traceable.  params: top-level build (NULL = {1, 16, 1, 1}; max_leaf_size
+ * 1..32).  Errors: INVALID_ARG (NULL, counts, bvh index, non-finite or singular matrix, mixed
+ * devices, bad params), NOT_BUILT, BVH_TOO_DEEP, CUDA, OOM. */
+typedef struct {
+  uint32_t bvh;                  /* index into the scenes array */
+  float object_from_world[12];   /* [A | b], row-major */
+} vsr_instance;
+typedef struct vsr_instances vsr_instances;
+vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
+                                const vsr_instance* instances, uint32_t num_instances,
+                                const vsr_build_params* params, vsr_instances** out);
+vsr_status vsr_instances_destroy(vsr_instances* inst);   /* NULL is a no-op */
+
+/* Trace rays against the instanced hierarchy.  Counting (COUNT*): the top-level root box once,
+ * 2 per top-level inner node, then per instance reached its scene's root box (1), 2 per inner
+ * node and 1 per triangle, as in vsr_trace.  prim_id in d_hits is the index within the hit's
+ * scene; d_inst (optional, n uint32, 4-B aligned) gets the caller's instance index (0xFFFFFFFF
+ * on a miss).  Other arguments as vsr_trace; RUNTIME_* controls and host-only instances:
+ * VSR_ERR_UNSUPPORTED. */
+vsr_status vsr_trace_instances(vsr_instances* inst, const vsr_ray* d_rays, uint64_t n,
+                               vsr_query query, vsr_isect isect, const vsr_isect_params* params,
+                               vsr_hit* d_hits, uint32_t* d_inst, vsr_counts* d_counts,
+                               void* stream);
+
+/* The built top level, for checking (host copies; NULL pointers: sizes only).
+ * nodes: num_nodes x 64 B pair nodes (export layout, leaf refs index `records`);
+ * records: num_instances x 64 B in leaf order: float object_from_world[12], uint32 bvh,
+ * uint32 instance index (the caller's), uint32 pad[2]. */
+typedef struct {
+  uint32_t root_ref;
+  float root_lo[3], root_hi[3];
+  uint32_t num_nodes, num_instances, max_depth;
+  void* nodes;
+  void* records;
+} vsr_instances_view;
+vsr_status vsr_instances_export(const vsr_instances* inst, vsr_instances_view* view);
+
 /* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
  * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
  * overlap the kernel; returns after the stream work completed. */

@@ -101,6 +101,11 @@ def lib():
         L.walker_trace_list.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64, C.c_int,
                                         C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p,
                                         C.c_void_p, C.c_int]
+        L.walker_trace_instances.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_void_p, C.c_uint32,
+                                             C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_float,
+                                             C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_int]
+        L.oracle_ray_to_object.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -324,3 +329,101 @@ def walk_multi(bvh: BvhArrays, rays, k, isect=DEFAULT, alpha_threshold=0.01, che
     if rc != 0:
         raise ValueError(f"walker_trace_multi failed ({rc})")
     return hits, nh, counts
+
+
+# ----------------------------------------------------------------------------
+# Two-level instancing (reading A27)
+# ----------------------------------------------------------------------------
+
+def ray_to_object(m, ray):
+    """walker.c's ray map of reading A27 for one ray (8 floats)."""
+    mm = np.ascontiguousarray(m, dtype=np.float32).reshape(12)
+    r = np.ascontiguousarray(ray, dtype=np.float32).reshape(8)
+    out = np.zeros(8, dtype=np.float32)
+    lib().oracle_ray_to_object(_ptr(mm), _ptr(r), _ptr(out))
+    return out
+
+
+def rays_to_object(rays, m):
+    """Reading A27 written out in numpy fp32 (one IEEE op per step, no FMA):
+    o'_i = ((A_i0*o_x + A_i1*o_y) + A_i2*o_z) + b_i,  d'_i = (A_i0*d_x + A_i1*d_y) + A_i2*d_z."""
+    r = _rays(rays)
+    A = np.ascontiguousarray(m, dtype=np.float32).reshape(3, 4)
+    out = r.copy()
+    o, d = r[:, 0:3], r[:, 4:7]
+    for i in range(3):
+        a0, a1, a2, b = (np.float32(A[i, j]) for j in range(4))
+        out[:, i] = ((a0 * o[:, 0] + a1 * o[:, 1]) + a2 * o[:, 2]) + b
+        out[:, 4 + i] = (a0 * d[:, 0] + a1 * d[:, 1]) + a2 * d[:, 2]
+    return out
+
+
+def trace_instances(scenes, bvh, mats, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01,
+                    checker_freq=8, nthreads=None):
+    """Brute force over every instance: instance j shows scenes[bvh[j]]
+    through the [A | b] map mats[j]; its candidates are oracle S on the mapped rays.
+    CLOSEST: min t over all instances (equal t: the lower instance index); ANY: the lowest
+    instance index with an accepted hit.  Returns (hits, inst uint32, flags uint32, ntie
+    uint32): flags = the winner's X-flags, plus X1 when another instance's best t is within
+    1e-5 relative of the winner's; ntie = instances whose best t equals the winner's."""
+    r = _rays(rays)
+    n = r.shape[0]
+    bvh = np.asarray(bvh, dtype=np.int64).reshape(-1)
+    mats = np.asarray(mats, dtype=np.float32).reshape(-1, 12)
+    sc = [_as_scene(s) for s in scenes]
+    best = np.empty(n, dtype=HIT_DTYPE)
+    best["t"] = np.inf
+    best["u"] = 0
+    best["v"] = 0
+    best["prim"] = 0xFFFFFFFF
+    inst = np.full(n, 0xFFFFFFFF, dtype=np.uint32)
+    flags = np.zeros(n, dtype=np.uint32)
+    all_t = np.full((len(bvh), n), np.inf, dtype=np.float64)
+    for j in range(len(bvh)):
+        h, fl = trace(sc[bvh[j]], rays_to_object(r, mats[j]), query, isect, alpha_threshold,
+                      checker_freq, flags=True, nthreads=nthreads)
+        hit = h["prim"] != 0xFFFFFFFF
+        all_t[j, hit] = h["t"][hit]
+        if query == ANY:
+            take = hit & (inst == 0xFFFFFFFF)
+        else:
+            take = hit & (h["t"] < best["t"])
+        best[take] = h[take]
+        inst[take] = j
+        flags[take] = fl[take]
+    won = inst != 0xFFFFFFFF
+    ntie = np.zeros(n, dtype=np.uint32)
+    if won.any():
+        tw = best["t"].astype(np.float64)
+        eq = all_t == tw[None, :]
+        ntie = np.where(won, eq.sum(axis=0), 0).astype(np.uint32)
+        with np.errstate(invalid="ignore"):   # inf - inf on rays no instance hits
+            near = np.abs(all_t - tw[None, :]) <= 1e-5 * np.maximum(np.abs(tw[None, :]), 1e-30)
+        others = near.sum(axis=0) > 1
+        flags |= np.where(won & others, X1, 0).astype(np.uint32)
+    return best, inst, flags, ntie
+
+
+def walk_instances(top, records, bottoms, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01,
+                   checker_freq=8, nthreads=None):
+    """Contract walker C over a two-level hierarchy.  top: dict with root_ref, root_lo,
+    root_hi, nodes [m, 16] uint32; records [k, 16] uint32 (64 B or_instance, leaf order);
+    bottoms: list of BvhArrays.  Returns (hits, inst uint32, counts)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    recs = np.ascontiguousarray(records, dtype=np.uint32).reshape(-1, 16)
+    nodes = np.ascontiguousarray(top["nodes"], dtype=np.uint32).reshape(-1, 16)
+    tb = _Bvh(int(top["root_ref"]), (C.c_float * 3)(*[float(x) for x in top["root_lo"]]),
+              (C.c_float * 3)(*[float(x) for x in top["root_hi"]]), nodes.shape[0], recs.shape[0],
+              0, _ptr(nodes) if nodes.shape[0] else None, None, None, None, None)
+    arr = (_Bvh * len(bottoms))(*[b.c_struct() for b in bottoms])
+    hits = np.empty(n, dtype=HIT_DTYPE)
+    inst = np.empty(n, dtype=np.uint32)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    rc = lib().walker_trace_instances(C.byref(tb), _ptr(recs), arr, len(bottoms), _ptr(r), n,
+                                      query, isect, alpha_threshold, checker_freq, _ptr(hits),
+                                      _ptr(inst), _ptr(counts), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_instances failed ({rc})")
+    return hits, inst, counts
+

@@ -142,6 +142,26 @@ int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uin
                       int query, int isect, float alpha_threshold, uint32_t checker_freq,
                       or_hit* hits, uint32_t* which, or_counts* counts, int nthreads);
 
+/* Two-level instancing ("the BVH will store BVHs as primitives"):
+ * a top-level BVH whose leaves index `recs` (64 B records: float m[12] = [A | b]
+ * object_from_world row-major, uint32 bvh, uint32 caller index, 2 x pad).  Walker C
+ * for it: the top level is walked like any BVH (root box counted once, 2 box tests per
+ * inner node); at a top-level leaf each instance, in stored order, maps the ray to
+ * object space (reading A27: o'_i = ((A_i0 o_x + A_i1 o_y) + A_i2 o_z) + b_i, d'_i =
+ * (A_i0 d_x + A_i1 d_y) + A_i2 d_z, fp32, no FMA) and walks bottoms[bvh] from its root
+ * box (counted) with the one running best_t.  inst (optional) gets the caller index of
+ * the kept hit (0xFFFFFFFF on a miss).  top->num_tris = number of records. */
+typedef struct {
+  float m[12]; uint32_t bvh, index, pad[2];
+} or_instance;
+int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_bvh* bottoms,
+                           uint32_t nbottoms, const float* rays, uint64_t n, int query,
+                           int isect, float alpha_threshold, uint32_t checker_freq,
+                           or_hit* hits, uint32_t* inst, or_counts* counts, int nthreads);
+
+/* The ray map of reading A27 on its own (pins): out = 8 floats (o', tmin, d', tmax). */
+void oracle_ray_to_object(const float* m, const float* ray, float* out);
+
 /* Slab test of the walker (exposed for pins). Returns box hit; *tn entry
  * clipped to tmin, *tf exit times (1+2*gamma_3) before the best_t clip. */
 int walker_slab(const float* lo, const float* hi, const float* ray, float best_t, float* tn,

@@ -534,3 +534,235 @@ static int walker_run(wjob_t* jb, int nthreads) {
   }
   return jb->err ? -1 : 0;
 }
+
+/* ====================== two-level instancing (walker C) ===================== */
+
+void oracle_ray_to_object(const float* m, const float* ray, float* out) {
+  const float* o = ray;
+  const float* d = ray + 4;
+  for (int i = 0; i < 3; ++i) {
+    const float* r = m + 4 * i;
+    out[i] = ((r[0] * o[0] + r[1] * o[1]) + r[2] * o[2]) + r[3];
+    out[4 + i] = (r[0] * d[0] + r[1] * d[1]) + r[2] * d[2];
+  }
+  out[3] = ray[3];
+  out[7] = ray[7];
+}
+
+typedef struct {
+  or_hit best;
+  float best_t;
+  int have;
+  or_counts c;
+  int bad;
+} istate_t;
+
+typedef struct {
+  const or_bvh* top;
+  const or_instance* recs;
+  const or_bvh* bottoms;
+  uint32_t nbottoms;
+  const float* rays;
+  uint64_t n;
+  int query, isect;
+  float thr;
+  uint32_t M;
+  or_hit* hits;
+  uint32_t* inst;
+  or_counts* counts;
+  uint64_t next;
+  int err;
+} ijob_t;
+
+/* One bottom BVH with the running state (the while-while loop of walk_one,
+ * closest / any only).  Returns 1 when an any-hit query accepted a hit. */
+static int walk_bottom(const ijob_t* jb, const or_bvh* b, const float* ray, istate_t* S) {
+  const float* o = ray;
+  const float* d = ray + 4;
+  const float tmin = ray[3];
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    float dk = d[a];
+    inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
+  }
+  uint32_t st_ref[MAX_STACK];
+  float st_tn[MAX_STACK];
+  int sp = 0;
+  float tn;
+  S->c.boxes++;
+  if (!slab(b->root_lo, b->root_hi, o, inv, tmin, S->best_t, &tn)) return 0;
+  uint32_t cur = b->root_ref;
+  for (;;) {
+    while (!(cur & LEAF_BIT)) {
+      if (cur >= b->num_nodes) { S->bad = 1; return 0; }
+      const or_node* nd = &b->nodes[cur];
+      float tn0, tn1, lo0[3], hi0[3], lo1[3], hi1[3];
+      S->c.boxes += 2;
+      get_child_box(nd, 0, lo0, hi0);
+      get_child_box(nd, 1, lo1, hi1);
+      int h0 = slab(lo0, hi0, o, inv, tmin, S->best_t, &tn0);
+      int h1 = slab(lo1, hi1, o, inv, tmin, S->best_t, &tn1);
+      if (h0 && h1) {
+        if (sp >= MAX_STACK) { S->bad = 1; return 0; }
+        if (tn1 < tn0) { st_ref[sp] = nd->ref[0]; st_tn[sp] = tn0; cur = nd->ref[1]; }
+        else { st_ref[sp] = nd->ref[1]; st_tn[sp] = tn1; cur = nd->ref[0]; }
+        sp++;
+      } else if (h0) {
+        cur = nd->ref[0];
+      } else if (h1) {
+        cur = nd->ref[1];
+      } else {
+        goto pop;
+      }
+    }
+    {
+      uint32_t first = cur & 0x03FFFFFFu;
+      uint32_t cnt = ((cur >> 26) & 31u) + 1u;
+      if ((uint64_t)first + cnt > b->num_tris) { S->bad = 1; return 0; }
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        const or_tri* tr = &b->tris[k];
+        float t, u, v;
+        S->c.tris++;
+        if (!mt_tri(tr, o, d, tmin, S->best_t, &t, &u, &v)) continue;
+        if (jb->isect == OR_ALPHA_TEX) S->c.alpha++;
+        if (!walk_filter(b, k, jb->isect, u, v, jb->thr, jb->M)) continue;
+        if (jb->query == OR_ANY) {
+          S->best.t = t; S->best.u = u; S->best.v = v; S->best.prim = tr->prim;
+          S->have = 1;
+          return 1;
+        }
+        if (!S->have || t < S->best_t) {
+          S->best.t = t; S->best.u = u; S->best.v = v; S->best.prim = tr->prim;
+          S->best_t = t;
+          S->have = 1;
+        }
+      }
+    }
+  pop:
+    for (;;) {
+      if (sp == 0) return 0;
+      sp--;
+      if (st_tn[sp] > S->best_t) continue;
+      cur = st_ref[sp];
+      break;
+    }
+  }
+}
+
+static void walk_instances_one(ijob_t* jb, uint64_t r) {
+  const float* ray = jb->rays + r * 8;
+  const float* o = ray;
+  const float* d = ray + 4;
+  const float tmin = ray[3];
+  const or_bvh* top = jb->top;
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    float dk = d[a];
+    inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
+  }
+  istate_t S;
+  memset(&S, 0, sizeof S);
+  S.best.t = INFINITY;
+  S.best.prim = 0xFFFFFFFFu;
+  S.best_t = ray[7];
+  uint32_t which = 0xFFFFFFFFu;
+  uint32_t st_ref[MAX_STACK];
+  float st_tn[MAX_STACK];
+  int sp = 0;
+  float tn;
+  S.c.boxes++;
+  if (!slab(top->root_lo, top->root_hi, o, inv, tmin, S.best_t, &tn)) goto done;
+  uint32_t cur = top->root_ref;
+  for (;;) {
+    while (!(cur & LEAF_BIT)) {
+      if (cur >= top->num_nodes) { S.bad = 1; goto done; }
+      const or_node* nd = &top->nodes[cur];
+      float tn0, tn1, lo0[3], hi0[3], lo1[3], hi1[3];
+      S.c.boxes += 2;
+      get_child_box(nd, 0, lo0, hi0);
+      get_child_box(nd, 1, lo1, hi1);
+      int h0 = slab(lo0, hi0, o, inv, tmin, S.best_t, &tn0);
+      int h1 = slab(lo1, hi1, o, inv, tmin, S.best_t, &tn1);
+      if (h0 && h1) {
+        if (sp >= MAX_STACK) { S.bad = 1; goto done; }
+        if (tn1 < tn0) { st_ref[sp] = nd->ref[0]; st_tn[sp] = tn0; cur = nd->ref[1]; }
+        else { st_ref[sp] = nd->ref[1]; st_tn[sp] = tn1; cur = nd->ref[0]; }
+        sp++;
+      } else if (h0) {
+        cur = nd->ref[0];
+      } else if (h1) {
+        cur = nd->ref[1];
+      } else {
+        goto pop;
+      }
+    }
+    {
+      /* top-level leaf: its instances in stored order (the BVH's "primitives") */
+      uint32_t first = cur & 0x03FFFFFFu;
+      uint32_t cnt = ((cur >> 26) & 31u) + 1u;
+      if ((uint64_t)first + cnt > top->num_tris) { S.bad = 1; goto done; }
+      for (uint32_t k = first; k < first + cnt; ++k) {
+        const or_instance* in = &jb->recs[k];
+        if (in->bvh >= jb->nbottoms) { S.bad = 1; goto done; }
+        float oray[8];
+        oracle_ray_to_object(in->m, ray, oray);
+        const int had = S.have;
+        const float bt = S.best_t;
+        const int stop = walk_bottom(jb, &jb->bottoms[in->bvh], oray, &S);
+        if (S.bad) goto done;
+        if ((S.have && !had) || S.best_t < bt) which = in->index;
+        if (stop) goto done;
+      }
+    }
+  pop:
+    for (;;) {
+      if (sp == 0) goto done;
+      sp--;
+      if (st_tn[sp] > S.best_t) continue;
+      cur = st_ref[sp];
+      break;
+    }
+  }
+done:
+  jb->hits[r] = S.best;
+  if (jb->inst) jb->inst[r] = which;
+  if (jb->counts) jb->counts[r] = S.c;
+  if (S.bad) __atomic_store_n(&jb->err, 1, __ATOMIC_RELAXED);
+}
+
+static void* iworker(void* arg) {
+  ijob_t* jb = (ijob_t*)arg;
+  const uint64_t chunk = 256;
+  for (;;) {
+    uint64_t s = __atomic_fetch_add(&jb->next, chunk, __ATOMIC_RELAXED);
+    if (s >= jb->n) break;
+    uint64_t e = s + chunk < jb->n ? s + chunk : jb->n;
+    for (uint64_t r = s; r < e; ++r) walk_instances_one(jb, r);
+  }
+  return NULL;
+}
+
+int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_bvh* bottoms,
+                           uint32_t nbottoms, const float* rays, uint64_t n, int query,
+                           int isect, float thr, uint32_t M, or_hit* hits, uint32_t* inst,
+                           or_counts* counts, int nthreads) {
+  if (!top || !recs || !bottoms || nbottoms < 1 || !rays || !hits) return -1;
+  if (query != OR_CLOSEST && query != OR_ANY) return -1;
+  if (isect < OR_NONE || isect > OR_COUNT) return -1;
+  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  ijob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.top = top; jb.recs = recs; jb.bottoms = bottoms; jb.nbottoms = nbottoms;
+  jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr; jb.M = M;
+  jb.hits = hits; jb.inst = inst; jb.counts = counts;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads == 1) {
+    iworker(&jb);
+  } else {
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, iworker, &jb);
+    for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+    free(th);
+  }
+  return jb.err ? -1 : 0;
+}

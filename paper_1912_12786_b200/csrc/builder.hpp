@@ -29,4 +29,10 @@ struct HostBvh {
 vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
                      std::string& err);
 
+// Top level of a two-level (instanced) hierarchy: the same binned SAH over
+// instance world boxes (6 floats per instance: lo xyz, hi xyz); `order`
+// receives the instance indices in leaf order (a leaf's `first` indexes it).
+vsr_status build_top(const float* boxes, uint32_t n, const vsr_build_params& prm, HostBvh& out,
+                     std::vector<uint32_t>& order, std::string& err);
+
 }  // namespace vsr

@@ -224,43 +224,14 @@ void parallel_for(size_t n, F f) {
   for (auto& x : th) x.join();
 }
 
-}  // namespace
-
-vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
-                     std::string& err) {
-  const uint32_t N = in.num_tris;
-  std::vector<uint8_t> degen(N);
-  parallel_for(N, [&](size_t b, size_t e) {
-    for (size_t i = b; i < e; ++i) degen[i] = degenerate(in.vertices + 9 * i);
-  });
-  std::vector<uint32_t> idx;
-  idx.reserve(N);
-  for (uint32_t i = 0; i < N; ++i)
-    if (!degen[i]) idx.push_back(i);
-  out.num_degenerate = N - (uint32_t)idx.size();
+// The tree over prims idx[0, m) with boxes pbox / centroids cen: binned SAH,
+// flattened depth-first pre-order with padded child boxes.  Fills out.nodes,
+// root_ref, root box, max_depth, num_leaves; idx ends in leaf order (a leaf's
+// `first` indexes idx).
+vsr_status build_tree(const std::vector<Box>& pbox, const std::vector<float>& cen,
+                      std::vector<uint32_t>& idx, const vsr_build_params& prm, HostBvh& out,
+                      std::string& err) {
   const uint32_t m = (uint32_t)idx.size();
-  if (m == 0) {
-    err = "empty scene: no non-degenerate triangles";
-    return VSR_ERR_EMPTY_SCENE;
-  }
-  if (m > kMaxTris) {
-    err = "more than 2^26 triangles are not supported by the 26-bit leaf encoding";
-    return VSR_ERR_UNSUPPORTED;
-  }
-  std::vector<Box> pbox(N);
-  std::vector<float> cen(3 * (size_t)N);
-  parallel_for(N, [&](size_t b, size_t e) {
-    for (size_t i = b; i < e; ++i) {
-      const float* vt = in.vertices + 9 * i;
-      Box bx;
-      for (int a = 0; a < 3; ++a) {
-        bx.lo[a] = std::min(std::min(vt[a], vt[3 + a]), vt[6 + a]);
-        bx.hi[a] = std::max(std::max(vt[a], vt[3 + a]), vt[6 + a]);
-        cen[3 * i + a] = 0.5f * bx.lo[a] + 0.5f * bx.hi[a];
-      }
-      pbox[i] = bx;
-    }
-  });
   Ctx c;
   c.pbox = &pbox;
   c.cen = &cen;
@@ -322,6 +293,48 @@ vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh&
     out.root_ref = 0;
   }
   pad_out(root, out.root_lo, out.root_hi);
+  return VSR_OK;
+}
+
+}  // namespace
+
+vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
+                     std::string& err) {
+  const uint32_t N = in.num_tris;
+  std::vector<uint8_t> degen(N);
+  parallel_for(N, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) degen[i] = degenerate(in.vertices + 9 * i);
+  });
+  std::vector<uint32_t> idx;
+  idx.reserve(N);
+  for (uint32_t i = 0; i < N; ++i)
+    if (!degen[i]) idx.push_back(i);
+  out.num_degenerate = N - (uint32_t)idx.size();
+  const uint32_t m = (uint32_t)idx.size();
+  if (m == 0) {
+    err = "empty scene: no non-degenerate triangles";
+    return VSR_ERR_EMPTY_SCENE;
+  }
+  if (m > kMaxTris) {
+    err = "more than 2^26 triangles are not supported by the 26-bit leaf encoding";
+    return VSR_ERR_UNSUPPORTED;
+  }
+  std::vector<Box> pbox(N);
+  std::vector<float> cen(3 * (size_t)N);
+  parallel_for(N, [&](size_t b, size_t e) {
+    for (size_t i = b; i < e; ++i) {
+      const float* vt = in.vertices + 9 * i;
+      Box bx;
+      for (int a = 0; a < 3; ++a) {
+        bx.lo[a] = std::min(std::min(vt[a], vt[3 + a]), vt[6 + a]);
+        bx.hi[a] = std::max(std::max(vt[a], vt[3 + a]), vt[6 + a]);
+        cen[3 * i + a] = 0.5f * bx.lo[a] + 0.5f * bx.hi[a];
+      }
+      pbox[i] = bx;
+    }
+  });
+  vsr_status st = build_tree(pbox, cen, idx, prm, out, err);
+  if (st != VSR_OK) return st;
 
   out.tris.resize(m);
   out.sides.resize(m);
@@ -346,6 +359,31 @@ vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh&
     }
   });
   return VSR_OK;
+}
+
+vsr_status build_top(const float* boxes, uint32_t n, const vsr_build_params& prm, HostBvh& out,
+                     std::vector<uint32_t>& order, std::string& err) {
+  if (n == 0) {
+    err = "no instances";
+    return VSR_ERR_EMPTY_SCENE;
+  }
+  if (n > kMaxTris) {
+    err = "more than 2^26 instances are not supported by the 26-bit leaf encoding";
+    return VSR_ERR_UNSUPPORTED;
+  }
+  std::vector<Box> pbox(n);
+  std::vector<float> cen(3 * (size_t)n);
+  for (uint32_t i = 0; i < n; ++i) {
+    for (int a = 0; a < 3; ++a) {
+      pbox[i].lo[a] = boxes[6 * (size_t)i + a];
+      pbox[i].hi[a] = boxes[6 * (size_t)i + 3 + a];
+      cen[3 * (size_t)i + a] = 0.5f * pbox[i].lo[a] + 0.5f * pbox[i].hi[a];
+    }
+  }
+  order.resize(n);
+  for (uint32_t i = 0; i < n; ++i) order[i] = i;
+  out.num_degenerate = 0;
+  return build_tree(pbox, cen, order, prm, out, err);
 }
 
 }  // namespace vsr

@@ -91,4 +91,15 @@ struct IsectData {
   float fm;         // checker frequency M as float
 };
 
+// One instance of a two-level hierarchy (vsr.h vsr_instance), in top-level
+// leaf order: the [A | b] map rays take into object space, rows padded to
+// float4 so the record is 4 x LDG.128.
+struct alignas(16) Instance {
+  float m[12];       // row-major 3x4 object_from_world
+  uint32_t bvh;      // element of the scene list
+  uint32_t index;    // the caller's instance index
+  uint32_t pad[2];
+};
+static_assert(sizeof(Instance) == 64, "Instance must be 64 B");
+
 }  // namespace vsr

@@ -229,24 +229,36 @@ __device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, fl
 // Whole traversal of one ray.  `oct` is warp-uniform: 0..7 if every lane of
 // the warp has that octant (primary rays: all but the centre row/column
 // tiles), 8 otherwise; the switch is taken once per leaf, uniformly.
+template <class I>
+__device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect, float2* stack,
+                                            int oct) {
+  switch (oct) {
+    case 0: return descend<0>(S, T, isect, stack);
+    case 1: return descend<1>(S, T, isect, stack);
+    case 2: return descend<2>(S, T, isect, stack);
+    case 3: return descend<3>(S, T, isect, stack);
+    case 4: return descend<4>(S, T, isect, stack);
+    case 5: return descend<5>(S, T, isect, stack);
+    case 6: return descend<6>(S, T, isect, stack);
+    case 7: return descend<7>(S, T, isect, stack);
+    default: return descend<-1>(S, T, isect, stack);
+  }
+}
+
 template <int Q, class I, class M = NoMulti>
 __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, float2* stack,
                                          int oct, M& mb) {
   for (;;) {
-    bool at_leaf;
-    switch (oct) {
-      case 0: at_leaf = descend<0>(S, T, isect, stack); break;
-      case 1: at_leaf = descend<1>(S, T, isect, stack); break;
-      case 2: at_leaf = descend<2>(S, T, isect, stack); break;
-      case 3: at_leaf = descend<3>(S, T, isect, stack); break;
-      case 4: at_leaf = descend<4>(S, T, isect, stack); break;
-      case 5: at_leaf = descend<5>(S, T, isect, stack); break;
-      case 6: at_leaf = descend<6>(S, T, isect, stack); break;
-      case 7: at_leaf = descend<7>(S, T, isect, stack); break;
-      default: at_leaf = descend<-1>(S, T, isect, stack); break;
-    }
+    const bool at_leaf = descend_oct(S, T, isect, stack, oct);
     if (!at_leaf || leaf<Q>(S, T, isect, mb) || !pop(T, stack)) return;
   }
+}
+
+// Warp-uniform octant of the converged lanes' rays, 8 when they disagree.
+__device__ __forceinline__ int warp_octant(const RayCtx& r) {
+  const unsigned live = __activemask();
+  const int oct = ray_octant(r);
+  return __match_any_sync(live, oct) == live ? oct : 8;
 }
 
 template <class I>
@@ -568,6 +580,86 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const Trac
   if (which) which[id] = hit_in;
 }
 
+// ---------------------------------------------------------------------------
+// Two-level instancing ("the BVH will store BVHs as
+// primitives").  p.scene is the top level (pair nodes over instance world
+// boxes; a leaf's range indexes p.instances); p.list / p.list_data are the
+// instanced scenes.  A top-level leaf runs, per instance, the whole bottom
+// traversal with the ray mapped to object space (reading A27) and the shared
+// best_t; the bottom's stack entries sit above the top level's.
+// ---------------------------------------------------------------------------
+constexpr int kInstStack = 2 * kMaxStack;
+
+__device__ __forceinline__ void to_object(const float4 r0, const float4 r1, const float4 r2,
+                                          const RayCtx& w, float4& a, float4& b) {
+  a.x = ((r0.x * w.ox + r0.y * w.oy) + r0.z * w.oz) + r0.w;
+  a.y = ((r1.x * w.ox + r1.y * w.oy) + r1.z * w.oz) + r1.w;
+  a.z = ((r2.x * w.ox + r2.y * w.oy) + r2.z * w.oz) + r2.w;
+  a.w = w.tmin;
+  b.x = (r0.x * w.dx + r0.y * w.dy) + r0.z * w.dz;
+  b.y = (r1.x * w.dx + r1.y * w.dy) + r1.z * w.dz;
+  b.z = (r2.x * w.dx + r2.y * w.dy) + r2.z * w.dz;
+}
+
+// Instance k of the current top-level leaf.  Returns true when the query is
+// finished (any-hit accepted a primitive).
+template <int Q, class I>
+__device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& isect,
+                                              float2* stack, uint32_t k, uint32_t& hit_in) {
+  const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
+  const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
+  const uint32_t b = __float_as_uint(ex.x);
+  const DevScene& S = p.list[b];
+  bind_scene_data(isect, p.list_data[b]);
+  Trav B = T;   // running best (t, u, v, prim, have, best_t) carried in and out
+  float4 oa, ob;
+  to_object(r0, r1, r2, T.r, oa, ob);
+  make_ray(B.r, oa, ob);
+  B.sp = 0;
+  B.cur = S.root_ref;
+  const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
+  float tn;
+  if (!box_hook(isect, B.r, root, B.best_t, tn)) return false;
+  NoMulti none;
+  traverse<Q>(S, B, isect, stack, warp_octant(B.r), none);
+  const bool better = Q == kAny ? B.prim != kMissPrim : ((B.have && !T.have) || B.best_t < T.best_t);
+  if (better) {
+    T.best_t = B.best_t;
+    T.have = B.have;
+    T.t = B.t;
+    T.u = B.u;
+    T.v = B.v;
+    T.prim = B.prim;
+    hit_in = __float_as_uint(ex.y);
+  }
+  return Q == kAny && better;
+}
+
+template <int Q, class I>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_kernel(const TraceParams p) {
+  const uint64_t blk = launch_block(p);
+  const uint64_t id = blk * kBlock + threadIdx.x;
+  if (id >= p.n) return;
+  I isect = make_isect<I>(p);
+  Trav T;
+  float2 stack[kInstStack];   // top level below, the current instance's entries above
+  uint32_t hit_in = 0xFFFFFFFFu;
+  if (start_ray(p, T, isect, id)) {   // world ray; counted test of the top-level root box
+    const int woct = warp_octant(T.r);
+    for (;;) {
+      if (!descend_oct(p.scene, T, isect, stack, woct)) break;
+      const uint32_t first = T.cur & kLeafFirstMask;
+      const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
+      bool done = false;
+      for (uint32_t k = first; k < end && !done; ++k)
+        done = instance_leaf<Q>(p, T, isect, stack + T.sp, k, hit_in);
+      if (done || !pop(T, stack)) break;
+    }
+  }
+  finish(p, T, isect);
+  if (p.which) p.which[id] = hit_in;
+}
+
 // Persistent schedule (VSR_SCHED=persistent): grid sized to residency; warps
 // claim kChunk rays per atomicAdd and refill idle lanes after each leaf once
 // `refill` lanes are idle.  Measured slower than the direct schedule on the
@@ -729,6 +821,30 @@ cudaError_t launch_list(const TraceParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int Q, class I>
+cudaError_t launch_inst(const TraceParams& p, cudaStream_t st) {
+  const uint64_t need = (p.n + kBlock - 1) / kBlock;
+  if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  cudaError_t e = launch_k(trace_instances_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
+  if (e != cudaSuccess) return e;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+template <int Q>
+cudaError_t dispatch_inst(int isect, const TraceParams& p, cudaStream_t st) {
+  switch (isect) {
+    case VSR_ISECT_NONE: return launch_inst<Q, no_intersector>(p, st);
+    case VSR_ISECT_DEFAULT: return launch_inst<Q, default_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE: return launch_inst<Q, alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL: return launch_inst<Q, alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_COUNT: return launch_inst<Q, cost_intersector<default_intersector>>(p, st);
+    case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+      return launch_inst<Q, cost_intersector<alpha_texture_intersector>>(p, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int Q>
 cudaError_t dispatch_list(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
@@ -864,7 +980,9 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     p.perm = perm;
   }
   if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
-  cudaError_t e = p.list ? (query == kAny ? dispatch_list<kAny>(isect, p, st)
+  cudaError_t e = p.instances ? (query == kAny ? dispatch_inst<kAny>(isect, p, st)
+                                                : dispatch_inst<kClosest>(isect, p, st))
+                  : p.list ? (query == kAny ? dispatch_list<kAny>(isect, p, st)
                                           : dispatch_list<kClosest>(isect, p, st))
                   : query == kMulti ? dispatch_multi(isect, p, st)
                   : query == kAny ? dispatch_isect<kAny>(isect, p, st)

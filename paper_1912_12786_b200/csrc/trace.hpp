@@ -33,7 +33,8 @@ struct TraceParams {
   const DevScene* list;          // list query (device array) or nullptr
   const IsectData* list_data;    // per-element mask data (device array)
   uint32_t list_count;
-  uint32_t* which;               // list query: optional per-ray list index of the hit
+  uint32_t* which;               // list / instance query: optional per-ray element of the hit
+  const Instance* instances;     // instance query: records in top-level leaf order (p.scene = top)
   int runtime_kind;
   void* filter_fn;
 };

@@ -47,7 +47,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_destroy", "vsr_last_error", "vsr_bvh_export", "vsr_scene_import",
                     "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version",
                     "vsr_set_kernel_events", "vsr_group_create", "vsr_group_destroy",
-                    "vsr_trace_group"]
+                    "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
+                    "vsr_trace_instances", "vsr_instances_export"]
 
 
 class VsrError(RuntimeError):
@@ -82,6 +83,16 @@ class BvhView(C.Structure):
                 ("num_nodes", C.c_uint32), ("num_tris", C.c_uint32), ("num_textures", C.c_uint32),
                 ("num_texels", C.c_uint64), ("nodes", C.c_void_p), ("tris", C.c_void_p),
                 ("sides", C.c_void_p), ("texdescs", C.c_void_p), ("texels", C.c_void_p)]
+
+
+class Instance(C.Structure):
+    _fields_ = [("bvh", C.c_uint32), ("object_from_world", C.c_float * 12)]
+
+
+class InstancesView(C.Structure):
+    _fields_ = [("root_ref", C.c_uint32), ("root_lo", C.c_float * 3), ("root_hi", C.c_float * 3),
+                ("num_nodes", C.c_uint32), ("num_instances", C.c_uint32),
+                ("max_depth", C.c_uint32), ("nodes", C.c_void_p), ("records", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -127,7 +138,15 @@ def lib():
         L.vsr_group_destroy.argtypes = [P]
         L.vsr_trace_group.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                       P, P, P, P]
-        for name in ("vsr_group_create", "vsr_group_destroy", "vsr_trace_group"):
+        L.vsr_instances_create.argtypes = [P, C.c_uint32, P, C.c_uint32, C.POINTER(BuildParams),
+                                           C.POINTER(P)]
+        L.vsr_instances_destroy.argtypes = [P]
+        L.vsr_instances_export.argtypes = [P, C.POINTER(InstancesView)]
+        L.vsr_trace_instances.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int,
+                                          C.POINTER(IsectParams), P, P, P, P]
+        for name in ("vsr_group_create", "vsr_group_destroy", "vsr_trace_group",
+                     "vsr_instances_create", "vsr_instances_destroy", "vsr_instances_export",
+                     "vsr_trace_instances"):
             getattr(L, name).restype = C.c_int
         for name in ("vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace_multi",
                      "vsr_trace_host",
@@ -367,6 +386,69 @@ class Group:
                                      _ptr(hits), _ptr(which), _ptr(counts),
                                      _stream_handle(stream)))
         return hits, which, counts
+
+
+class Instances:
+    """Two-level instancing (vsr_instances_create / vsr_trace_instances): a top-level BVH
+    over instances of built scenes, each seen through an object_from_world [A | b] map."""
+
+    def __init__(self, scenes, bvh, object_from_world, max_leaf_size=1, sah_bins=16):
+        self.scenes = list(scenes)   # keep the scenes alive while the instances exist
+        bvh = np.ascontiguousarray(bvh, dtype=np.uint32).reshape(-1)
+        m = np.ascontiguousarray(object_from_world, dtype=np.float32).reshape(-1, 12)
+        assert m.shape[0] == bvh.shape[0], "one 3x4 matrix per instance"
+        arr = (Instance * max(1, bvh.shape[0]))()
+        for k in range(bvh.shape[0]):
+            arr[k].bvh = int(bvh[k])
+            arr[k].object_from_world = (C.c_float * 12)(*m[k].tolist())
+        sc = (C.c_void_p * len(self.scenes))(*[s._h.value for s in self.scenes])
+        prm = BuildParams(max_leaf_size, sah_bins, 1.0, 1.0)
+        self._h = C.c_void_p()
+        _check(lib().vsr_instances_create(C.cast(sc, C.c_void_p), len(self.scenes),
+                                          C.cast(arr, C.c_void_p), bvh.shape[0], C.byref(prm),
+                                          C.byref(self._h)))
+
+    def close(self):
+        if self._h:
+            lib().vsr_instances_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def trace(self, rays, query=CLOSEST, isect=DEFAULT, hits=None, inst=None, counts=None,
+              stream=None, alpha_threshold=0.01, checker_freq=8):
+        """Returns (hits [n, 4], inst [n] int32 caller instance index, counts or None)."""
+        import torch
+        n = rays.shape[0]
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
+        if inst is None:
+            inst = torch.empty((n,), dtype=torch.int32, device=rays.device)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_instances(self._h, _ptr(rays), n, query, isect, C.byref(prm),
+                                         _ptr(hits), _ptr(inst), _ptr(counts),
+                                         _stream_handle(stream)))
+        return hits, inst, counts
+
+    def export(self) -> dict:
+        """Host copies of the top level: nodes [num_nodes, 16] uint32 (pair nodes) and
+        records [num_instances, 16] uint32 (12 matrix floats, bvh, index, pad, pad)."""
+        v = InstancesView()
+        _check(lib().vsr_instances_export(self._h, C.byref(v)))
+        nodes = np.zeros((v.num_nodes, 16), np.uint32)
+        recs = np.zeros((v.num_instances, 16), np.uint32)
+        v.nodes = _ptr(nodes) if v.num_nodes else None
+        v.records = _ptr(recs)
+        _check(lib().vsr_instances_export(self._h, C.byref(v)))
+        return {"root_ref": int(v.root_ref), "root_lo": np.array(v.root_lo, np.float32),
+                "root_hi": np.array(v.root_hi, np.float32), "nodes": nodes, "records": recs,
+                "max_depth": int(v.max_depth)}
 
 
 def hits_to_numpy(hits) -> np.ndarray:

@@ -15,7 +15,8 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE = os.path.join(ROOT, "oracle")
-PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py"]
+PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py",
+        "tests/test_instances_cpu.py"]
 
 MUTANTS = [
     # (file, original, mutated, description)
@@ -61,6 +62,17 @@ MUTANTS = [
     ("walker.c", "        if (jb->isect == OR_ALPHA_TEX) c.alpha++;", "", "walker: alpha lookups not counted"),
     ("walker.c", "ax[a][c] = lo[a];\n    ax[a][2 + c] = hi[a];", "ax[a][2 + c] = lo[a];\n    ax[a][c] = hi[a];",
      "oracle BVH: lo/hi planes swapped in the node"),
+    ("walker.c", "out[i] = ((r[0] * o[0] + r[1] * o[1]) + r[2] * o[2]) + r[3];",
+     "out[i] = ((r[0] * o[0] + r[1] * o[1]) + r[2] * o[2]);", "instance map: translation dropped"),
+    ("walker.c", "out[4 + i] = (r[0] * d[0] + r[1] * d[1]) + r[2] * d[2];",
+     "out[4 + i] = (m[i] * d[0] + m[4 + i] * d[1]) + m[8 + i] * d[2];",
+     "instance map: direction by the transposed matrix"),
+    ("walker.c", "  S->c.boxes++;\n  if (!slab(b->root_lo", "  if (!slab(b->root_lo",
+     "instances: bottom root test not counted"),
+    ("walker.c", "if ((S.have && !had) || S.best_t < bt) which = in->index;",
+     "if ((S.have && !had) || S.best_t < bt) which = k;",
+     "instances: leaf position reported instead of the caller's index"),
+    ("walker.c", "        if (stop) goto done;", "", "instances: any-hit keeps walking after a hit"),
 ]
 
 

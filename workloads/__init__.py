@@ -33,4 +33,7 @@ from .gen import (  # noqa: F401
     stacked_quads,
     split_scene,
     concat_scenes,
+    tree_model,
+    object_from_world,
+    instanced_forest,
 )

@@ -425,6 +425,57 @@ CONFIGS = {
 }
 
 
+# --------------------------------------------------------------------------
+# two-level instancing (NEXT-2; "the BVH will store BVHs as primitives")
+# --------------------------------------------------------------------------
+
+def tree_model(seed: int, n_cards: int = 16, textures=None) -> Scene:
+    """One tree object in its own space: n_cards vertical alpha cards (the C2 billboard
+    recipe) scattered within 4 m of the y axis, base at y = 0."""
+    verts, tcs, gids = _billboards(n_cards, 4.0, seed)
+    if textures is None:
+        textures = tree_textures(4, 256, seed + 100, discs=24)
+    gtex = (pcg_hash(np.arange(n_cards, dtype=np.uint32) + np.uint32(seed * 7919))
+            % np.uint32(len(textures))).astype(np.uint32)
+    return Scene(f"tree{seed}", verts, gids, tcs, gtex, textures)
+
+
+def object_from_world(yaw, scale, tx, ty, tz, shear=0.0) -> np.ndarray:
+    """[A | b] (float32, 12 per instance) of world_from_object = T(t) R_y(yaw) S(scale) K(shear),
+    K(shear) = identity + shear in the x-from-y entry; inverted in float64."""
+    yaw, scale, tx, ty, tz = (np.atleast_1d(np.asarray(x, np.float64)) for x in (yaw, scale, tx, ty, tz))
+    shear = np.broadcast_to(np.asarray(shear, np.float64), yaw.shape)
+    n = yaw.shape[0]
+    out = np.empty((n, 12), np.float32)
+    for k in range(n):
+        c, s_ = math.cos(yaw[k]), math.sin(yaw[k])
+        R = np.array([[c, 0.0, s_], [0.0, 1.0, 0.0], [-s_, 0.0, c]])
+        K = np.eye(3)
+        K[0, 1] = shear[k]
+        W = R @ (scale[k] * K)
+        A = np.linalg.inv(W)
+        b = -A @ np.array([tx[k], ty[k], tz[k]])
+        out[k] = np.concatenate([A, b[:, None]], axis=1).reshape(12)
+    return out
+
+
+def instanced_forest(n_instances: int = 10000, n_models: int = 4, cards: int = 64,
+                     extent: float = 250.0, seed: int = 5, textures=None):
+    """NEXT-2 workload: n_models tree models of `cards` alpha cards each, instanced
+    n_instances times over the C2 ground square with a random yaw, uniform scale 0.7-1.4
+    and a small shear.  Returns (models, bvh uint32[n], object_from_world float32[n, 12])."""
+    if textures is None:
+        textures = tree_textures(8, 512, seed + 1, discs=32)
+    models = [tree_model(seed * 31 + k, cards, textures) for k in range(n_models)]
+    rng = np.random.default_rng(seed)
+    bvh = rng.integers(0, n_models, n_instances).astype(np.uint32)
+    m = object_from_world(rng.uniform(0, 2 * math.pi, n_instances), rng.uniform(0.7, 1.4, n_instances),
+                          rng.uniform(-extent, extent, n_instances), np.zeros(n_instances),
+                          rng.uniform(-extent, extent, n_instances),
+                          rng.uniform(-0.1, 0.1, n_instances))
+    return models, bvh, m
+
+
 def split_scene(scene: Scene, k: int, axis: int = 0) -> list:
     """Partition a scene's triangles into k sub-scenes by centroid slab along `axis`
     (objects for list / compound-BVH queries).  Sub-scenes share the texture list and
