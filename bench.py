@@ -366,6 +366,7 @@ def run_own(args):
         extra["multi_hit"] = {"k": multi_k, "value": round(n / (np.mean(m) * 1e-3) / 1e6, 1),
                               "ms": round(float(np.mean(m)), 4)}
         del multi_hits, multi_n
+    if not args.no_variants and args.config in ("C2", "C3"):
         # NEXT-2: two-level instancing — instanced tree models over the
         # same ground square, this rank's frame, same query and intersector
         import workloads as W
@@ -395,6 +396,23 @@ def run_own(args):
                               "value": round(n / (im * 1e-3) / 1e6, 1), "ms": round(im, 4),
                               "hit_fraction": round(float((inst_ids != -1).float().mean()), 3)}
         del inst, iscenes, inst_ids
+    if not args.no_variants:
+        # NEXT-3: the same scene built by the GPU linear-BVH builder (build time, trace speed)
+        gscene = vsr.Scene.from_workload(sc, device=local)
+        gscene.build_gpu(args.max_leaf)   # first call: CUDA module / CUB setup
+        gscene.build_gpu(args.max_leaf)
+        gst = gscene.stats()
+        saved = scene
+        scene = gscene
+        mg, _ = timed(isect, max(5, args.steps // 2), 3)
+        scene = saved
+        extra["gpu_build"] = {"builder": "vsr_bvh_build_gpu (LBVH, Karras 2012)",
+                              "build_ms": round(gst["build_ms"], 2),
+                              "host_sah_build_ms": round(stats["build_ms"], 2),
+                              "nodes": gst["num_nodes"], "max_depth": gst["max_depth"],
+                              "value": round(n / (np.mean(mg) * 1e-3) / 1e6, 1),
+                              "ms": round(float(np.mean(mg)), 4)}
+        del gscene
         extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
                               "default_ms": round(float(np.median(b_ms)), 4),
                               "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}

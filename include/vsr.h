@@ -169,6 +169,14 @@ vsr_status vsr_scene_create(const vsr_scene_desc* desc, vsr_scene** out);
  * Errors: INVALID_ARG, EMPTY_SCENE, BVH_TOO_DEEP, UNSUPPORTED, CUDA, OOM. */
 vsr_status vsr_bvh_build(vsr_scene* scene, const vsr_build_params* params);
 
+/* Build the BVH on the scene's GPU instead: a linear BVH (Karras,
+ * HPG 2012 — 63-bit centroid Morton codes, device radix sort, one thread per internal node,
+ * bottom-up boxes), subtrees of <= max_leaf_size (1..32) triangles collapsed into leaves.  Same
+ * export layout, padding, degenerate rule and depth bound as vsr_bvh_build; lower tree quality
+ * than binned SAH (slower traces), a much faster build.  Synchronous; untimed setup.
+ * Errors: INVALID_ARG, EMPTY_SCENE, BVH_TOO_DEEP, UNSUPPORTED (host-only scene), CUDA, OOM. */
+vsr_status vsr_bvh_build_gpu(vsr_scene* scene, uint32_t max_leaf_size);
+
 /* Enqueue one trace of n rays on `stream` (a cudaStream_t; NULL = legacy default).
  * d_rays / d_hits / d_counts are caller-owned DEVICE buffers on the scene's device,
  * 16-B aligned.  d_counts is required iff isect is COUNT or COUNT_ALPHA_TEXTURE.

@@ -17,7 +17,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvsr.so")
-SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu"]
+SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu", "lbvh.cu"]
 HEADERS = ["layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

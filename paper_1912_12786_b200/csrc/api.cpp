@@ -533,6 +533,71 @@ vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
   return VSR_OK;
 }
 
+vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  if (s->vertices.empty() && s->num_tris_input == 0 && s->built)
+    return fail(VSR_ERR_INVALID_ARG, "imported scenes cannot be rebuilt");
+  if (max_leaf_size < 1 || max_leaf_size > kMaxLeafSize)
+    return fail(VSR_ERR_INVALID_ARG, "max_leaf_size must be in [1, 32]");
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene: use vsr_bvh_build");
+  if (s->num_tris_input == 0) return fail(VSR_ERR_EMPTY_SCENE, "empty scene: zero triangles");
+  auto t0 = std::chrono::steady_clock::now();
+  std::vector<TexDesc> descs(s->textures.size());
+  uint64_t total = 0;
+  for (size_t k = 0; k < s->textures.size(); ++k) {
+    descs[k].offset = total;
+    descs[k].w = s->textures[k].w;
+    descs[k].h = s->textures[k].h;
+    total += (uint64_t)descs[k].w * descs[k].h;
+  }
+  if (total > 0xFFFFFFFFull)
+    return fail(VSR_ERR_UNSUPPORTED, "more than 2^32 texels in total (32-bit sidecar offsets)");
+  std::vector<uint8_t> pool(total);
+  for (size_t k = 0; k < s->textures.size(); ++k)
+    std::memcpy(pool.data() + descs[k].offset, s->textures[k].texels.data(),
+                s->textures[k].texels.size());
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  const uint32_t n = s->num_tris_input;
+  float* d_v = nullptr;
+  float* d_tc = nullptr;
+  uint32_t* d_tt = nullptr;
+  TexDesc* d_desc = nullptr;
+  auto cleanup = [&] {
+    cudaFree(d_v);
+    cudaFree(d_tc);
+    cudaFree(d_tt);
+    cudaFree(d_desc);
+  };
+  vsr_status st;
+  if ((st = dev_upload(&d_v, s->vertices.data(), 9 * (size_t)n, "vertices")) != VSR_OK ||
+      (s->has_texcoords &&
+       (st = dev_upload(&d_tc, s->texcoords.data(), 6 * (size_t)n, "texcoords")) != VSR_OK) ||
+      (st = dev_upload(&d_tt, s->tri_tex.data(), n, "texture indices")) != VSR_OK ||
+      (st = dev_upload(&d_desc, descs.data(), descs.size(), "texdescs")) != VSR_OK) {
+    cleanup();
+    return st;
+  }
+  GpuBvh gb;
+  std::string err;
+  st = build_bvh_gpu(d_v, d_tc, d_tt, d_desc, n, max_leaf_size, gb, err);
+  cleanup();
+  if (st != VSR_OK) return fail(st, err);
+  st = upload(s, gb.root_ref, gb.root_lo, gb.root_hi, gb.nodes, gb.num_nodes, gb.tris, gb.sides,
+              gb.num_tris, descs.data(), (uint32_t)descs.size(), pool.data(), total);
+  cudaFree(gb.nodes);
+  cudaFree(gb.tris);
+  cudaFree(gb.sides);
+  if (st != VSR_OK) return st;
+  s->stats.num_degenerate = gb.num_degenerate;
+  s->stats.num_leaves = gb.num_leaves;
+  s->stats.max_depth = gb.max_depth;
+  s->stats.build_ms =
+      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return VSR_OK;
+}
+
 vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream) {

@@ -29,6 +29,21 @@ struct HostBvh {
 vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
                      std::string& err);
 
+// GPU linear BVH (lbvh.cu) on the current device from device inputs (9 floats
+// per triangle, optional 6 texcoords, resolved texture index, texture table).
+// Outputs are device arrays in the export layout, owned by the caller (cudaFree).
+struct GpuBvh {
+  PairNode* nodes = nullptr;
+  Tri* tris = nullptr;
+  Side* sides = nullptr;
+  uint32_t num_nodes = 0, num_tris = 0, root_ref = 0;
+  uint32_t max_depth = 0, num_leaves = 0, num_degenerate = 0;
+  float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
+};
+vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
+                         const uint32_t* d_tri_tex, const TexDesc* d_tex, uint32_t n,
+                         uint32_t max_leaf, GpuBvh& out, std::string& err);
+
 // Top level of a two-level (instanced) hierarchy: the same binned SAH over
 // instance world boxes (6 floats per instance: lo xyz, hi xyz); `order`
 // receives the instance indices in leaf order (a leaf's `first` indexes it).

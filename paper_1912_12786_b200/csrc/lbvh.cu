@@ -1,0 +1,430 @@
+// lbvh.cu — GPU BVH builder ("GPU builder (LBVH / PLOC)").
+//
+// The paper assumes a BVH exists and does not describe its
+// construction; the host binned-SAH builder (bvh_build.cpp) stays the default.
+// This is the linear BVH of Karras (HPG 2012): 63-bit Morton codes of the
+// triangle centroids, a device radix sort, one thread per internal node finds
+// its key range and split from the longest common prefixes, boxes are unioned
+// bottom-up (the second child to arrive at a parent computes it), subtrees of
+// <= max_leaf triangles collapse into leaves, and the surviving nodes are
+// compacted and written in the same export layout as the host builder:
+// 64-B pair nodes with the same 2^-20 outward padding, triangles and sidecars
+// gathered into leaf order.  Setup only (untimed); any valid BVH prunes exactly,
+// so traversal results do not depend on which builder made the tree.
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "builder.hpp"
+
+namespace vsr {
+namespace {
+
+constexpr int kT = 256;
+constexpr uint64_t kInvalidKey = ~0ull;
+
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7FFFFFFF;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7FFFFFFF); }
+
+struct Box6 {
+  float lo[3], hi[3];
+};
+
+// Per triangle: degenerate test (as the host builder: e1 x e2 == 0 in fp64 on the
+// fp32 edges), bounds, centroid (0.5 lo + 0.5 hi), centroid bounds, valid count.
+__global__ void prep_kernel(const float* __restrict__ v, uint32_t n, Box6* __restrict__ box,
+                            float* __restrict__ cen, uint8_t* __restrict__ valid,
+                            int* __restrict__ cbounds, uint32_t* __restrict__ nvalid) {
+  const uint32_t i = blockIdx.x * kT + threadIdx.x;
+  float c[3] = {0, 0, 0};
+  bool ok = false;
+  if (i < n) {
+    const float* t = v + 9 * (size_t)i;
+    const float e1[3] = {t[3] - t[0], t[4] - t[1], t[5] - t[2]};
+    const float e2[3] = {t[6] - t[0], t[7] - t[1], t[8] - t[2]};
+    const double x = (double)e1[1] * e2[2] - (double)e1[2] * e2[1];
+    const double y = (double)e1[2] * e2[0] - (double)e1[0] * e2[2];
+    const double z = (double)e1[0] * e2[1] - (double)e1[1] * e2[0];
+    ok = !(x == 0.0 && y == 0.0 && z == 0.0);
+    Box6 b;
+    for (int a = 0; a < 3; ++a) {
+      b.lo[a] = fminf(fminf(t[a], t[3 + a]), t[6 + a]);
+      b.hi[a] = fmaxf(fmaxf(t[a], t[3 + a]), t[6 + a]);
+      c[a] = 0.5f * b.lo[a] + 0.5f * b.hi[a];
+      cen[3 * (size_t)i + a] = c[a];
+    }
+    box[i] = b;
+    valid[i] = ok;
+  }
+  // centroid bounds of the valid triangles: warp reduce, one atomic per warp
+  for (int a = 0; a < 3; ++a) {
+    int lo = ok ? f2ord(c[a]) : 0x7FFFFFFF, hi = ok ? f2ord(c[a]) : (int)0x80000000;
+    for (int o = 16; o; o >>= 1) {
+      lo = min(lo, __shfl_xor_sync(0xFFFFFFFFu, lo, o));
+      hi = max(hi, __shfl_xor_sync(0xFFFFFFFFu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMin(cbounds + a, lo);
+      atomicMax(cbounds + 3 + a, hi);
+    }
+  }
+  const unsigned bal = __ballot_sync(0xFFFFFFFFu, ok);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(nvalid, (uint32_t)__popc(bal));
+}
+
+__device__ __forceinline__ uint64_t spread21(uint64_t x) {
+  x &= 0x1FFFFFull;
+  x = (x | x << 32) & 0x1F00000000FFFFull;
+  x = (x | x << 16) & 0x1F0000FF0000FFull;
+  x = (x | x << 8) & 0x100F00F00F00F00Full;
+  x = (x | x << 4) & 0x10C30C30C30C30C3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+__global__ void morton_kernel(const float* __restrict__ cen, const uint8_t* __restrict__ valid,
+                              const int* __restrict__ cbounds, uint32_t n,
+                              uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const uint32_t i = blockIdx.x * kT + threadIdx.x;
+  if (i >= n) return;
+  vals[i] = i;
+  if (!valid[i]) {
+    keys[i] = kInvalidKey;   // sorts after every valid code (63-bit codes)
+    return;
+  }
+  uint64_t q[3];
+  for (int a = 0; a < 3; ++a) {
+    const float lo = ord2f(cbounds[a]), hi = ord2f(cbounds[3 + a]);
+    const float ext = hi - lo;
+    float u = ext > 0.0f ? (cen[3 * (size_t)i + a] - lo) / ext : 0.0f;
+    u = fminf(fmaxf(u, 0.0f), 1.0f);
+    q[a] = (uint64_t)fminf(u * 2097152.0f, 2097151.0f);
+  }
+  keys[i] = spread21(q[0]) << 2 | spread21(q[1]) << 1 | spread21(q[2]);
+}
+
+// Longest common prefix of sorted keys i and j (index tie-break for equal keys).
+__device__ __forceinline__ int delta(const uint64_t* k, int m, int i, int j) {
+  if (j < 0 || j >= m) return -1;
+  const uint64_t a = k[i], b = k[j];
+  return a == b ? 64 + __clz((unsigned)(i ^ j)) : __clzll((long long)(a ^ b));
+}
+
+// Karras 2012, Fig. 4: internal node i's range [first, last] and split gamma.
+// Children: internal node index in [0, m-1) or leaf j encoded as ~j.
+__global__ void karras_kernel(const uint64_t* __restrict__ k, int m, int2* __restrict__ range,
+                              int2* __restrict__ child, int* __restrict__ parent_node,
+                              int* __restrict__ parent_leaf) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= m - 1) return;
+  const int d = delta(k, m, i, i + 1) - delta(k, m, i, i - 1) >= 0 ? 1 : -1;
+  const int dmin = delta(k, m, i, i - d);
+  int lmax = 2;
+  while (delta(k, m, i, i + lmax * d) > dmin) lmax *= 2;
+  int l = 0;
+  for (int t = lmax / 2; t >= 1; t /= 2)
+    if (delta(k, m, i, i + (l + t) * d) > dmin) l += t;
+  const int j = i + l * d;
+  const int dnode = delta(k, m, i, j);
+  int s = 0;
+  for (int div = 2;; div *= 2) {
+    const int t = (l + div - 1) / div;
+    if (delta(k, m, i, i + (s + t) * d) > dnode) s += t;
+    if (t <= 1) break;
+  }
+  const int gamma = i + s * d + min(d, 0);
+  const int first = min(i, j), last = max(i, j);
+  range[i] = make_int2(first, last);
+  const int left = first == gamma ? ~gamma : gamma;
+  const int right = last == gamma + 1 ? ~(gamma + 1) : gamma + 1;
+  child[i] = make_int2(left, right);
+  if (left < 0) parent_leaf[~left] = i; else parent_node[left] = i;
+  if (right < 0) parent_leaf[~right] = i; else parent_node[right] = i;
+}
+
+__device__ __forceinline__ Box6 unite(const Box6& a, const Box6& b) {
+  Box6 r;
+  for (int q = 0; q < 3; ++q) {
+    r.lo[q] = fminf(a.lo[q], b.lo[q]);
+    r.hi[q] = fmaxf(a.hi[q], b.hi[q]);
+  }
+  return r;
+}
+
+__device__ __forceinline__ Box6 load_box(const Box6* p) {
+  Box6 b;
+  const volatile float* f = reinterpret_cast<const volatile float*>(p);
+  for (int q = 0; q < 3; ++q) {
+    b.lo[q] = f[q];
+    b.hi[q] = f[3 + q];
+  }
+  return b;
+}
+
+// Bottom-up boxes: each leaf climbs; the second arrival at a node unites its children.
+__global__ void boxes_kernel(const Box6* __restrict__ prim_box, const uint32_t* __restrict__ order,
+                             int m, const int2* __restrict__ child, const int* __restrict__ parent_node,
+                             const int* __restrict__ parent_leaf, Box6* node_box,
+                             int* __restrict__ arrivals) {
+  const int j = blockIdx.x * kT + threadIdx.x;
+  if (j >= m) return;
+  int p = parent_leaf[j];
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(arrivals + p, 1) == 0) return;   // the sibling subtree is not done yet
+    __threadfence();
+    const int2 c = child[p];
+    const Box6 a = c.x < 0 ? prim_box[order[~c.x]] : load_box(node_box + c.x);
+    const Box6 b = c.y < 0 ? prim_box[order[~c.y]] : load_box(node_box + c.y);
+    node_box[p] = unite(a, b);
+    p = p == 0 ? -1 : parent_node[p];
+  }
+}
+
+__global__ void live_kernel(const int2* __restrict__ range, int m, uint32_t max_leaf,
+                            uint32_t* __restrict__ live) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= m - 1) return;
+  live[i] = (uint32_t)(range[i].y - range[i].x + 1) > max_leaf ? 1u : 0u;
+}
+
+// Outward padding 2^-20 * max(1, |x|) in fp64, rounded outward to fp32 (the host builder's pad_out).
+__device__ __forceinline__ void pad_box(const Box6& b, float* lo, float* hi) {
+  for (int q = 0; q < 3; ++q) {
+    const double l = b.lo[q], h = b.hi[q];
+    const double ld = l - ldexp(fmax(1.0, fabs(l)), -20), hd = h + ldexp(fmax(1.0, fabs(h)), -20);
+    float lf = __double2float_rd(ld), hf = __double2float_ru(hd);
+    lo[q] = lf;
+    hi[q] = hf;
+  }
+}
+
+__device__ __forceinline__ uint32_t leaf_ref(int first, int count) {
+  return kLeafBit | ((uint32_t)(count - 1) << kLeafCountShift) | (uint32_t)first;
+}
+
+// Write the surviving nodes (compacted index = exclusive scan of `live`) as pair
+// nodes; children at or below max_leaf become leaves over their key range.
+__global__ void write_kernel(const int2* __restrict__ range, const int2* __restrict__ child,
+                             const uint32_t* __restrict__ live, const uint32_t* __restrict__ newidx,
+                             const Box6* __restrict__ node_box, const Box6* __restrict__ prim_box,
+                             const uint32_t* __restrict__ order, int m, PairNode* __restrict__ out,
+                             const int* __restrict__ parent_node, uint32_t* __restrict__ max_depth,
+                             uint32_t* __restrict__ num_leaves) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= m - 1 || !live[i]) return;
+  PairNode nd;
+  const int2 c = child[i];
+  const int cs[2] = {c.x, c.y};
+  uint32_t leaves = 0;
+  for (int s = 0; s < 2; ++s) {
+    const int ch = cs[s];
+    Box6 b;
+    if (ch < 0) {
+      b = prim_box[order[~ch]];
+      nd.ref[s] = leaf_ref(~ch, 1);
+      ++leaves;
+    } else {
+      b = node_box[ch];
+      if (live[ch]) {
+        nd.ref[s] = newidx[ch];
+      } else {
+        nd.ref[s] = leaf_ref(range[ch].x, range[ch].y - range[ch].x + 1);
+        ++leaves;
+      }
+    }
+    float lo[3], hi[3];
+    pad_box(b, lo, hi);
+    nd.x[s] = lo[0];
+    nd.x[2 + s] = hi[0];
+    nd.y[s] = lo[1];
+    nd.y[2 + s] = hi[1];
+    nd.z[s] = lo[2];
+    nd.z[2 + s] = hi[2];
+  }
+  nd.pad[0] = nd.pad[1] = 0;
+  out[newidx[i]] = nd;
+  // depth of this node's children (root = 0): ancestors are live, so climb
+  uint32_t depth = 1;
+  for (int p = i; p != 0; p = parent_node[p]) ++depth;
+  atomicMax(max_depth, depth);
+  if (leaves) atomicAdd(num_leaves, leaves);
+}
+
+__global__ void gather_kernel(const float* __restrict__ v, const float* __restrict__ tc,
+                              const uint32_t* __restrict__ tri_tex, const TexDesc* __restrict__ tex,
+                              const uint32_t* __restrict__ order, int m, Tri* __restrict__ tris,
+                              Side* __restrict__ sides) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= m) return;
+  const uint32_t p = order[k];
+  const float* t = v + 9 * (size_t)p;
+  Tri tr;
+  for (int a = 0; a < 3; ++a) {
+    tr.v0[a] = t[a];
+    tr.e1[a] = t[3 + a] - t[a];
+    tr.e2[a] = t[6 + a] - t[a];
+  }
+  tr.prim = p;
+  tr.pad1 = tr.pad2 = 0;
+  tris[k] = tr;
+  Side sd;
+  for (int q = 0; q < 6; ++q) sd.uv[q] = tc ? tc[6 * (size_t)p + q] : 0.0f;
+  const TexDesc d = tex[tri_tex[p]];
+  sd.texel_offset = (uint32_t)d.offset;
+  sd.dims = (d.w - 1u) | ((d.h - 1u) << 16);
+  sides[k] = sd;
+}
+
+__global__ void root_box_kernel(const Box6* __restrict__ prim_box, const uint32_t* __restrict__ order,
+                                int m, const Box6* __restrict__ node_box, float* __restrict__ out) {
+  // single thread: the root box is node 0's (m >= 2) or the lone leaf's union
+  Box6 b;
+  if (m >= 2) {
+    b = node_box[0];
+  } else {
+    b = prim_box[order[0]];
+  }
+  pad_box(b, out, out + 3);
+}
+
+template <class T>
+cudaError_t alloc(T** p, size_t count) {
+  return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
+}
+
+}  // namespace
+
+vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
+                         const uint32_t* d_tri_tex, const TexDesc* d_tex, uint32_t n,
+                         uint32_t max_leaf, GpuBvh& out, std::string& err) {
+  cudaStream_t st = nullptr;
+  Box6* box = nullptr;
+  float* cen = nullptr;
+  uint8_t* valid = nullptr;
+  int* cb = nullptr;
+  uint32_t* counters = nullptr;   // [0] valid, [1] max depth, [2] leaves
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  uint32_t *vals = nullptr, *vals2 = nullptr, *live = nullptr, *newidx = nullptr;
+  int2 *range = nullptr, *child = nullptr;
+  int *parent_node = nullptr, *parent_leaf = nullptr, *arrivals = nullptr;
+  Box6* node_box = nullptr;
+  float* root = nullptr;
+  void* tmp = nullptr;
+  out = GpuBvh{};
+  cudaError_t e = cudaSuccess;
+  auto fin = [&](vsr_status s, const std::string& msg) {
+    cudaFree(box); cudaFree(cen); cudaFree(valid); cudaFree(cb); cudaFree(counters);
+    cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(live);
+    cudaFree(newidx); cudaFree(range); cudaFree(child); cudaFree(parent_node);
+    cudaFree(parent_leaf); cudaFree(arrivals); cudaFree(node_box); cudaFree(root); cudaFree(tmp);
+    if (s != VSR_OK) {
+      cudaFree(out.nodes); cudaFree(out.tris); cudaFree(out.sides);
+      out = GpuBvh{};
+      err = msg + (e != cudaSuccess ? std::string(": ") + cudaGetErrorString(e) : std::string());
+    }
+    return s;
+  };
+#define VSR_TRY(x)                                  \
+  if ((e = (x)) != cudaSuccess) return fin(e == cudaErrorMemoryAllocation ? VSR_ERR_OOM : VSR_ERR_CUDA, #x)
+  const unsigned g = (n + kT - 1) / kT;
+  VSR_TRY(alloc(&box, n));
+  VSR_TRY(alloc(&cen, 3 * (size_t)n));
+  VSR_TRY(alloc(&valid, n));
+  VSR_TRY(alloc(&cb, 6));
+  VSR_TRY(alloc(&counters, 3));
+  const int init[6] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, (int)0x80000000, (int)0x80000000,
+                       (int)0x80000000};
+  VSR_TRY(cudaMemcpy(cb, init, sizeof init, cudaMemcpyHostToDevice));
+  VSR_TRY(cudaMemset(counters, 0, 3 * sizeof(uint32_t)));
+  prep_kernel<<<g, kT, 0, st>>>(d_vertices, n, box, cen, valid, cb, counters);
+  VSR_TRY(cudaGetLastError());
+  uint32_t m32 = 0;
+  VSR_TRY(cudaMemcpy(&m32, counters, sizeof m32, cudaMemcpyDeviceToHost));
+  out.num_degenerate = n - m32;
+  const int m = (int)m32;
+  if (m == 0) return fin(VSR_ERR_EMPTY_SCENE, "empty scene: no non-degenerate triangles");
+  if (m32 > kMaxTris)
+    return fin(VSR_ERR_UNSUPPORTED, "more than 2^26 triangles are not supported by the 26-bit leaf encoding");
+  VSR_TRY(alloc(&keys, n));
+  VSR_TRY(alloc(&keys2, n));
+  VSR_TRY(alloc(&vals, n));
+  VSR_TRY(alloc(&vals2, n));
+  morton_kernel<<<g, kT, 0, st>>>(cen, valid, cb, n, keys, vals);
+  VSR_TRY(cudaGetLastError());
+  size_t tmp_bytes = 0, scan_bytes = 0;
+  VSR_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, 64, st));
+  VSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, live, newidx, m > 1 ? m - 1 : 1, st));
+  VSR_TRY(cudaMalloc(&tmp, tmp_bytes > scan_bytes ? tmp_bytes : scan_bytes));
+  // stable LSD radix sort: equal codes keep ascending triangle index
+  VSR_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys2, vals, vals2, (int)n, 0, 64, st));
+  const uint32_t* order = vals2;   // sorted triangle indices; the first m are the valid ones
+  const unsigned gi = m > 1 ? (unsigned)((m - 1 + kT - 1) / kT) : 1u;
+  const unsigned gl = (unsigned)((m + kT - 1) / kT);
+  if (m >= 2) {
+    VSR_TRY(alloc(&range, m - 1));
+    VSR_TRY(alloc(&child, m - 1));
+    VSR_TRY(alloc(&parent_node, m - 1));
+    VSR_TRY(alloc(&parent_leaf, m));
+    VSR_TRY(alloc(&arrivals, m - 1));
+    VSR_TRY(alloc(&node_box, m - 1));
+    VSR_TRY(alloc(&live, m - 1));
+    VSR_TRY(alloc(&newidx, m - 1));
+    VSR_TRY(cudaMemsetAsync(arrivals, 0, sizeof(int) * (m - 1), st));
+    VSR_TRY(cudaMemsetAsync(parent_node, 0xFF, sizeof(int) * (m - 1), st));
+    karras_kernel<<<gi, kT, 0, st>>>(keys2, m, range, child, parent_node, parent_leaf);
+    VSR_TRY(cudaGetLastError());
+    boxes_kernel<<<gl, kT, 0, st>>>(box, order, m, child, parent_node, parent_leaf, node_box,
+                                    arrivals);
+    VSR_TRY(cudaGetLastError());
+    live_kernel<<<gi, kT, 0, st>>>(range, m, max_leaf, live);
+    VSR_TRY(cudaGetLastError());
+    VSR_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, live, newidx, m - 1, st));
+    uint32_t last_idx = 0, last_live = 0;
+    VSR_TRY(cudaMemcpy(&last_idx, newidx + (m - 2), sizeof last_idx, cudaMemcpyDeviceToHost));
+    VSR_TRY(cudaMemcpy(&last_live, live + (m - 2), sizeof last_live, cudaMemcpyDeviceToHost));
+    out.num_nodes = last_idx + last_live;
+  }
+  VSR_TRY(alloc(&out.nodes, out.num_nodes));
+  VSR_TRY(alloc(&out.tris, m));
+  VSR_TRY(alloc(&out.sides, m));
+  VSR_TRY(alloc(&root, 6));
+  if (out.num_nodes) {
+    write_kernel<<<gi, kT, 0, st>>>(range, child, live, newidx, node_box, box, order, m, out.nodes,
+                                    parent_node, counters + 1, counters + 2);
+    VSR_TRY(cudaGetLastError());
+  }
+  gather_kernel<<<gl, kT, 0, st>>>(d_vertices, d_texcoords, d_tri_tex, d_tex, order, m, out.tris,
+                                   out.sides);
+  VSR_TRY(cudaGetLastError());
+  root_box_kernel<<<1, 1, 0, st>>>(box, order, m, node_box, root);
+  VSR_TRY(cudaGetLastError());
+  uint32_t cnt[3];
+  VSR_TRY(cudaMemcpy(cnt, counters, sizeof cnt, cudaMemcpyDeviceToHost));
+  VSR_TRY(cudaMemcpy(out.root_lo, root, 3 * sizeof(float), cudaMemcpyDeviceToHost));
+  VSR_TRY(cudaMemcpy(out.root_hi, root + 3, 3 * sizeof(float), cudaMemcpyDeviceToHost));
+  out.num_tris = m32;
+  if (out.num_nodes) {
+    out.root_ref = 0;
+    out.max_depth = cnt[1];
+    out.num_leaves = cnt[2];
+  } else {   // m <= max_leaf: one leaf
+    out.root_ref = kLeafBit | ((m32 - 1u) << kLeafCountShift);
+    out.max_depth = 0;
+    out.num_leaves = 1;
+  }
+  if (out.max_depth > (uint32_t)kMaxStack) {
+    e = cudaSuccess;
+    return fin(VSR_ERR_BVH_TOO_DEEP, "BVH deeper than 64 levels (traversal stack bound)");
+  }
+  return fin(VSR_OK, "");
+#undef VSR_TRY
+}
+
+}  // namespace vsr

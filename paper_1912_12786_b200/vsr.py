@@ -48,7 +48,7 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version",
                     "vsr_set_kernel_events", "vsr_group_create", "vsr_group_destroy",
                     "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
-                    "vsr_trace_instances", "vsr_instances_export"]
+                    "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu"]
 
 
 class VsrError(RuntimeError):
@@ -120,6 +120,8 @@ def lib():
         P = C.c_void_p
         L.vsr_scene_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(P)]
         L.vsr_bvh_build.argtypes = [P, C.POINTER(BuildParams)]
+        L.vsr_bvh_build_gpu.argtypes = [P, C.c_uint32]
+        L.vsr_bvh_build_gpu.restype = C.c_int
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                      P, P, P]
@@ -243,6 +245,11 @@ class Scene:
     def build(self, max_leaf_size=2, sah_bins=16, traversal_cost=1.0, intersection_cost=1.0):
         prm = BuildParams(max_leaf_size, sah_bins, traversal_cost, intersection_cost)
         _check(lib().vsr_bvh_build(self._h, C.byref(prm)))
+        return self
+
+    def build_gpu(self, max_leaf_size=2):
+        """vsr_bvh_build_gpu: linear BVH built on the scene's GPU (NEXT-3)."""
+        _check(lib().vsr_bvh_build_gpu(self._h, max_leaf_size))
         return self
 
     def stats(self) -> dict:
