@@ -396,6 +396,36 @@ def run_own(args):
                               "value": round(n / (im * 1e-3) / 1e6, 1), "ms": round(im, 4),
                               "hit_fraction": round(float((inst_ids != -1).float().mean()), 3)}
         del inst, iscenes, inst_ids
+    import workloads as W
+    if not args.no_variants and args.config in W.CAMERAS and not tiles:
+        # NEXT-4: the same frame with its primary rays generated inside the trace kernel
+        # (vsr_trace_pinhole: no ray buffer); e2e = that + the hits' copy to pinned host memory
+        eye, look, up, fov, cw, chh, cspp = W.CAMERAS[args.config]
+        sh_x = 2.0 * rank
+        cam = vsr.pinhole_camera((eye[0] + sh_x, eye[1], eye[2]), (look[0] + sh_x, look[1], look[2]),
+                                 up, fov, cw, chh, cspp)
+        h_out = torch.empty((n, 4), dtype=torch.float32).pin_memory()
+        gen_ms, gen_e2e = [], []
+        for it in range(3 + 2 * max(5, args.steps // 2)):
+            flush_l2()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            c = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            scene.trace_pinhole(cam, q, isect, hits=hits, stream=stream)
+            b.record(stream)
+            h_out.copy_(hits, non_blocking=True)
+            c.record(stream)
+            c.synchronize()
+            if it >= 3:
+                gen_ms.append(a.elapsed_time(b))
+                gen_e2e.append(a.elapsed_time(c))
+        gm, ge = float(np.mean(gen_ms)), float(np.mean(gen_e2e))
+        extra["raygen"] = {"api": "vsr_trace_pinhole (rays generated in the trace kernel)",
+                           "value": round(n / (gm * 1e-3) / 1e6, 1), "ms": round(gm, 4),
+                           "e2e": {"value": round(n / (ge * 1e-3) / 1e6, 1), "ms": round(ge, 4),
+                                   "h2d_bytes_per_step": 0, "d2h_bytes_per_step": n * 16}}
+        del h_out
     if not args.no_variants:
         # NEXT-3: the same scene built by the GPU linear-BVH builder (build time, trace speed)
         gscene = vsr.Scene.from_workload(sc, device=local)

@@ -186,6 +186,29 @@ vsr_status vsr_trace(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_qu
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream);
 
+/* Primary rays generated INSIDE the trace kernel (SURVEY.md §8(f) NEXT-4 "fused camera ray
+ * generator": no ray buffer, no 32 B/ray read).  Ray i is the i-th of the input recipe's
+ * (8x8 tile, sample, y, x) order and is bit-identical to the host recipe:
+ *   px, py = pixel, s = sample; spp = 1: (jx, jy) = (0.5, 0.5); spp = k*k: jx = ((s % k) + r1)/k,
+ *   jy = ((s / k) + r2)/k, r1,2 = pcg_hash32((key*2 [+1] + 7919*jitter_seed) mod 2^32) / 2^32,
+ *   key = (py*width + px)*spp + s;  sx = 2(px + jx)/width - 1,  sy = 1 - 2(py + jy)/height;
+ *   d = fp32((w + (sx*tan_half_vfov*aspect) u) + (sy*tan_half_vfov) v)   [fp64, this order],
+ *   o = fp32(eye), [tmin, tmax] as given.
+ * w, u, v: the camera's forward / right / up unit vectors in fp64 (vsr.py pinhole_camera).
+ * n = width*height*spp rays; d_hits / d_counts in ray order as vsr_trace.  Not provided for the
+ * RUNTIME_* controls.  Errors: INVALID_ARG (NULL, width/height not multiples of 8, spp not a
+ * square, non-finite camera, more than 2^31 blocks), NOT_BUILT, UNSUPPORTED, CUDA. */
+typedef struct {
+  double eye[3];
+  double w[3], u[3], v[3];
+  double tan_half_vfov, aspect;
+  uint32_t width, height, spp, jitter_seed;
+  float tmin, tmax;
+} vsr_pinhole;
+vsr_status vsr_trace_pinhole(vsr_scene* scene, const vsr_pinhole* camera, vsr_query query,
+                             vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                             vsr_counts* d_counts, void* stream);
+
 /* Multi-hit query ("the first N hit points"): per ray the
  * max_hits (1..16) smallest-t ACCEPTED hits in ascending t (equal t: the order traversal found
  * them).  Once max_hits hits are held, tmax shrinks to the worst kept t.

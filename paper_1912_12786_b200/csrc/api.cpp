@@ -598,6 +598,66 @@ vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
   return VSR_OK;
 }
 
+vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query query,
+                             vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                             vsr_counts* d_counts, void* stream) {
+  g_err.clear();
+  if (!s || !cam) return fail(VSR_ERR_INVALID_ARG, "NULL scene or camera");
+  if ((int)isect >= 100 && valid_isect(isect))
+    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided with in-kernel ray generation");
+  TraceParams p;
+  vsr_status st = make_params(s, query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
+  if (cam->width == 0 || cam->height == 0 || cam->width % 8 || cam->height % 8)
+    return fail(VSR_ERR_INVALID_ARG, "width and height must be positive multiples of 8");
+  uint32_t side = 1;
+  while (side * side < cam->spp && side < 65536) ++side;
+  if (cam->spp == 0 || side * side != cam->spp)
+    return fail(VSR_ERR_INVALID_ARG, "spp must be a perfect square >= 1");
+  const double* vals[] = {cam->eye, cam->w, cam->u, cam->v};
+  for (const double* vv : vals)
+    for (int k = 0; k < 3; ++k)
+      if (!std::isfinite(vv[k])) return fail(VSR_ERR_INVALID_ARG, "non-finite camera");
+  if (!std::isfinite(cam->tan_half_vfov) || !std::isfinite(cam->aspect) || std::isnan(cam->tmin) ||
+      std::isnan(cam->tmax))
+    return fail(VSR_ERR_INVALID_ARG, "non-finite camera");
+  const uint64_t n = (uint64_t)cam->width * cam->height * cam->spp;
+  if (!d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL hits buffer");
+  if (!aligned16(d_hits)) return fail(VSR_ERR_INVALID_ARG, "hits buffer must be 16-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  p.gen = 1;
+  for (int k = 0; k < 3; ++k) {
+    p.cam.eye[k] = cam->eye[k];
+    p.cam.w[k] = cam->w[k];
+    p.cam.u[k] = cam->u[k];
+    p.cam.v[k] = cam->v[k];
+  }
+  p.cam.tan_half = cam->tan_half_vfov;
+  p.cam.aspect = cam->aspect;
+  p.cam.width = cam->width;
+  p.cam.height = cam->height;
+  p.cam.spp = cam->spp;
+  p.cam.seed = cam->jitter_seed;
+  p.cam.side = side;
+  p.cam.tmin = cam->tmin;
+  p.cam.tmax = cam->tmax;
+  p.sched = kSchedDirect;   // the persistent schedule reads a ray buffer
+  p.rays = nullptr;
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "pinhole trace launch");
+  return VSR_OK;
+}
+
 vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream) {

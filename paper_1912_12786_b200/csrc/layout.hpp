@@ -91,6 +91,15 @@ struct IsectData {
   float fm;         // checker frequency M as float
 };
 
+// Pinhole camera for rays generated inside the trace kernel (vsr.h vsr_pinhole;
+// `side` = sqrt(spp), precomputed on the host).
+struct Pinhole {
+  double eye[3], w[3], u[3], v[3];
+  double tan_half, aspect;
+  uint32_t width, height, spp, seed, side;
+  float tmin, tmax;
+};
+
 // One instance of a two-level hierarchy (vsr.h vsr_instance), in top-level
 // leaf order: the [A | b] map rays take into object space, rows padded to
 // float4 so the record is 4 x LDG.128.

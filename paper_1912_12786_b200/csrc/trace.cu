@@ -87,12 +87,59 @@ __device__ __forceinline__ bool pop(Trav& T, const float2* stack) {
   return false;
 }
 
-// Load ray `id`, test the root box once (counted, reading A11).
+// ---- fused primary-ray generation (vsr.h vsr_pinhole) ----
+// Ray `id` of the (8x8 tile, sample, y, x) order, computed with exactly the
+// fp64 operations of the input recipe (workloads.pinhole_rays)
+// and rounded to fp32, so it is bit-identical to the host-generated ray.
+__device__ __forceinline__ uint32_t pcg_hash32(uint64_t x) {
+  x &= 0xFFFFFFFFull;
+  const uint64_t state = (x * 747796405ull + 2891336453ull) & 0xFFFFFFFFull;
+  const uint64_t shift = (state >> 28) + 4ull;
+  const uint64_t word = (((state >> shift) ^ state) * 277803737ull) & 0xFFFFFFFFull;
+  return (uint32_t)((word >> 22) ^ word);
+}
+
+__device__ __forceinline__ void gen_ray(const Pinhole& c, uint64_t id, float4& a, float4& b) {
+  const uint64_t per_tile = 64ull * c.spp;
+  const uint64_t tile = id / per_tile, rem = id % per_tile;
+  const uint32_t smp = (uint32_t)(rem >> 6), q = (uint32_t)(rem & 63u);
+  const uint64_t tx = c.width >> 3;
+  const uint64_t px = (tile % tx) * 8ull + (q & 7u), py = (tile / tx) * 8ull + (q >> 3);
+  double jx = 0.5, jy = 0.5;
+  if (c.spp > 1) {
+    const uint64_t key = (py * c.width + px) * c.spp + smp;
+    const uint64_t seed = (uint64_t)c.seed * 7919ull;
+    const double r1 = (double)pcg_hash32(key * 2ull + seed) / 4294967296.0;
+    const double r2 = (double)pcg_hash32(key * 2ull + (1ull + seed)) / 4294967296.0;
+    jx = ((double)(smp % c.side) + r1) / (double)c.side;
+    jy = ((double)(smp / c.side) + r2) / (double)c.side;
+  }
+  const double sx = 2.0 * ((double)px + jx) / (double)c.width - 1.0;
+  const double sy = 1.0 - 2.0 * ((double)py + jy) / (double)c.height;
+  const double A = sx * c.tan_half * c.aspect, B = sy * c.tan_half;
+  a = make_float4(__double2float_rn(c.eye[0]), __double2float_rn(c.eye[1]),
+                  __double2float_rn(c.eye[2]), c.tmin);
+  b = make_float4(__double2float_rn((c.w[0] + A * c.u[0]) + B * c.v[0]),
+                  __double2float_rn((c.w[1] + A * c.u[1]) + B * c.v[1]),
+                  __double2float_rn((c.w[2] + A * c.u[2]) + B * c.v[2]), c.tmax);
+}
+
+template <bool GEN>
+__device__ __forceinline__ void fetch_ray(const TraceParams& p, uint64_t id, float4& a, float4& b) {
+  if constexpr (GEN) {
+    gen_ray(p.cam, id, a, b);
+  } else {
+    a = __ldg(p.rays + 2 * id);
+    b = __ldg(p.rays + 2 * id + 1);
+  }
+}
+
+// Load (or generate) ray `id`, test the root box once (counted, reading A11).
 // Returns true if the ray needs traversal.
-template <class I>
+template <bool GEN = false, class I>
 __device__ __forceinline__ bool start_ray(const TraceParams& p, Trav& T, I& isect, uint64_t id) {
-  const float4 a = __ldg(p.rays + 2 * id);
-  const float4 b = __ldg(p.rays + 2 * id + 1);
+  float4 a, b;
+  fetch_ray<GEN>(p, id, a, b);
   make_ray(T.r, a, b);
   T.best_t = b.w;
   T.have = false;
@@ -310,6 +357,7 @@ __device__ __forceinline__ uint64_t global_ns() {
 // ---------------------------------------------------------------------------
 constexpr int kOrderBuckets = 32;
 
+template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
   asm volatile("griddepcontrol.launch_dependents;");   // let the scatter kernel's CTAs launch
@@ -319,7 +367,8 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
   if (b < nblocks) {
     const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * (uint32_t)((kBlock - 1) / 3);
     if (id < p.n) {
-      const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
+      float4 a, d;
+      fetch_ray<GEN>(p, id, a, d);
       RayCtx r;
       make_ray(r, a, d);
       const float t0x = (p.scene.root_lo[0] - r.ox) * r.ix, t1x = (p.scene.root_hi[0] - r.ox) * r.ix;
@@ -463,7 +512,7 @@ __device__ __forceinline__ uint64_t launch_block(const TraceParams& p) {
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
-template <int Q, class I>
+template <int Q, class I, bool GEN = false>
 __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TraceParams p) {
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
@@ -474,7 +523,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
     I isect = make_isect<I>(p);
     Trav T;
     float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
-    const bool go = start_ray(p, T, isect, id);
+    const bool go = start_ray<GEN>(p, T, isect, id);
     // warp-uniform octant: specialised slab test when all live lanes agree
     const unsigned live = __activemask();
     const int oct = ray_octant(T.r);
@@ -779,7 +828,16 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
     trace_kernel_persistent<Q, I><<<blocks, kBlock, 0, st>>>(p);
   } else {
     if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
-    cudaError_t e = launch_k(trace_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
+    cudaError_t e;
+    if (p.gen) {   // fused ray generation: not built for the run-time controls
+      if constexpr (std::is_same<I, runtime_switch_intersector>::value ||
+                    std::is_same<I, runtime_fnptr_intersector>::value)
+        return cudaErrorInvalidValue;
+      else
+        e = launch_k(trace_kernel<Q, I, true>, need, kBlock, p.perm && p.pdl, st, p);
+    } else {
+      e = launch_k(trace_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
+    }
     if (e != cudaSuccess) return e;
   }
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -964,8 +1022,12 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
       g_launches.fetch_add(1, std::memory_order_relaxed);
     }
 #else
-    order_cost_kernel<<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(p, (uint32_t)nblocks,
-                                                                             hist, slot);
+    if (p.gen)
+      order_cost_kernel<true><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
+          p, (uint32_t)nblocks, hist, slot);
+    else
+      order_cost_kernel<false><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
+          p, (uint32_t)nblocks, hist, slot);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if ((e = launch_k(order_scatter_kernel, (nblocks + 255) / 256, 256, p.pdl != 0, st,
                       (uint32_t)nblocks, (const uint32_t*)hist, (const uint32_t*)slot, perm)) !=

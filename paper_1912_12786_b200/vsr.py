@@ -9,6 +9,7 @@ only (``torch.Tensor.data_ptr()``, ``torch.cuda.current_stream().cuda_stream``).
 from __future__ import annotations
 
 import ctypes as C
+import math
 import os
 
 import numpy as np
@@ -48,7 +49,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_scene_stats", "vsr_launch_count", "vsr_abi_version",
                     "vsr_set_kernel_events", "vsr_group_create", "vsr_group_destroy",
                     "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
-                    "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu"]
+                    "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
+                    "vsr_trace_pinhole"]
 
 
 class VsrError(RuntimeError):
@@ -95,6 +97,35 @@ class InstancesView(C.Structure):
                 ("max_depth", C.c_uint32), ("nodes", C.c_void_p), ("records", C.c_void_p)]
 
 
+class Pinhole(C.Structure):
+    _fields_ = [("eye", C.c_double * 3), ("w", C.c_double * 3), ("u", C.c_double * 3),
+                ("v", C.c_double * 3), ("tan_half_vfov", C.c_double), ("aspect", C.c_double),
+                ("width", C.c_uint32), ("height", C.c_uint32), ("spp", C.c_uint32),
+                ("jitter_seed", C.c_uint32), ("tmin", C.c_float), ("tmax", C.c_float)]
+
+
+def pinhole_camera(eye, look_at, up, vfov_deg, width, height, spp=1, jitter_seed=6, tmin=1e-4,
+                   tmax=float("inf")) -> Pinhole:
+    """vsr_pinhole for a look-at camera: w = normalize(look_at - eye), u = normalize(up x w),
+    v = w x u, all in fp64 (the input recipe's basis)."""
+    e = np.asarray(eye, dtype=np.float64)
+    w = np.asarray(look_at, dtype=np.float64) - e
+    w /= np.linalg.norm(w)
+    u = np.cross(np.asarray(up, dtype=np.float64), w)
+    u /= np.linalg.norm(u)
+    v = np.cross(w, u)
+    c = Pinhole()
+    c.eye = (C.c_double * 3)(*e.tolist())
+    c.w = (C.c_double * 3)(*w.tolist())
+    c.u = (C.c_double * 3)(*u.tolist())
+    c.v = (C.c_double * 3)(*v.tolist())
+    c.tan_half_vfov = math.tan(math.radians(vfov_deg) * 0.5)
+    c.aspect = width / height
+    c.width, c.height, c.spp, c.jitter_seed = width, height, spp, jitter_seed
+    c.tmin, c.tmax = tmin, tmax
+    return c
+
+
 class Stats(C.Structure):
     _fields_ = [("num_tris_input", C.c_uint32), ("num_tris", C.c_uint32),
                 ("num_degenerate", C.c_uint32), ("num_nodes", C.c_uint32),
@@ -121,6 +152,9 @@ def lib():
         L.vsr_scene_create.argtypes = [C.POINTER(SceneDesc), C.POINTER(P)]
         L.vsr_bvh_build.argtypes = [P, C.POINTER(BuildParams)]
         L.vsr_bvh_build_gpu.argtypes = [P, C.c_uint32]
+        L.vsr_trace_pinhole.argtypes = [P, C.POINTER(Pinhole), C.c_int, C.c_int,
+                                        C.POINTER(IsectParams), P, P, P]
+        L.vsr_trace_pinhole.restype = C.c_int
         L.vsr_bvh_build_gpu.restype = C.c_int
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
@@ -273,6 +307,21 @@ class Scene:
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace(self._h, _ptr(rays), n, query, isect, C.byref(prm), _ptr(hits),
                                _ptr(counts), _stream_handle(stream)))
+        return hits, counts
+
+    def trace_pinhole(self, camera, query=CLOSEST, isect=DEFAULT, hits=None, counts=None,
+                      stream=None, alpha_threshold=0.01, checker_freq=8):
+        """vsr_trace_pinhole: primary rays generated in the kernel from `camera`
+        (pinhole_camera(...)); returns (hits [n, 4], counts or None) in ray order."""
+        import torch
+        n = camera.width * camera.height * camera.spp
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.float32, device=f"cuda:{self.device}")
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=hits.device)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_pinhole(self._h, C.byref(camera), query, isect, C.byref(prm),
+                                       _ptr(hits), _ptr(counts), _stream_handle(stream)))
         return hits, counts
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, hits=None, num_hits=None, counts=None,

@@ -32,16 +32,21 @@ def sass():
     return funcs
 
 
-def _find(funcs, q, tag):
-    names = [n for n in funcs if f"trace_kernelILi{q}E" in n and tag in n and "cost_" not in n]
+def _find(funcs, q, tag, gen=False):
+    """The trace kernel for query q and intersector `tag`; gen: the fused ray-generation
+    instantiation (template flag GEN, mangled Lb1)."""
+    flag = "ELb1E" if gen else "ELb0E"
+    names = [n for n in funcs if f"trace_kernelILi{q}E" in n and tag in n and "cost_" not in n
+             and flag in n]
     assert len(names) == 1, names
     return funcs[names[0]]
 
 
+@pytest.mark.parametrize("gen", [False, True])
 @pytest.mark.parametrize("q", [0, 1])
-def test_none_and_default_sass_identical(sass, q):
-    a = _find(sass, q, "14no_intersector")
-    b = _find(sass, q, "19default_intersector")
+def test_none_and_default_sass_identical(sass, q, gen):
+    a = _find(sass, q, "14no_intersector", gen)
+    b = _find(sass, q, "19default_intersector", gen)
     assert len(a) > 100
     assert a == b
 
