@@ -39,6 +39,7 @@ if ROOT not in sys.path:
 METRIC = "Mrays/s per B200 (alpha-mask any-hit, 1080p) at 1/2/4/8 GPUs; % HBM roofline"
 UNIT = "Mrays/s"
 ISECTS = ("none", "default", "alpha_texture", "alpha_procedural", "count", "count_alpha_texture",
+          "alpha_texture_bilinear", "alpha_procedural_uv",
           "runtime_switch_default", "runtime_fnptr_default", "runtime_switch_alpha_texture",
           "runtime_fnptr_alpha_texture")
 

@@ -65,6 +65,11 @@ typedef enum { VSR_QUERY_CLOSEST = 0, VSR_QUERY_ANY = 1 } vsr_query;
  *                     ++num_tris per triangle hook, default filter; writes d_counts.
  *   COUNT_ALPHA_TEXTURE  bvh_costs stacked on ALPHA_TEXTURE (the cost of the alpha
  *                     intersector's traversal; also counts alpha lookups).
+ *   ALPHA_TEXTURE_BILINEAR  NEXT-4 variant (reading A28): as ALPHA_TEXTURE with a
+ *                     bilinear filter (texel centres (i+.5)/W, wrap) and the filtered alpha
+ *                     compared with alpha_threshold.
+ *   ALPHA_PROCEDURAL_UV  NEXT-4 variant: the checker of ALPHA_PROCEDURAL evaluated on the
+ *                     interpolated texcoords (s, t) instead of the barycentrics.
  *   RUNTIME_*         measurement controls for the zero-cost claim: the same
  *                     traversal with the filter chosen at RUN time inside the loop,
  *                     the Embree/OptiX style the paper contrasts with.
@@ -77,6 +82,8 @@ typedef enum {
   VSR_ISECT_ALPHA_PROCEDURAL = 3,
   VSR_ISECT_COUNT = 4,
   VSR_ISECT_COUNT_ALPHA_TEXTURE = 5,
+  VSR_ISECT_ALPHA_TEXTURE_BILINEAR = 6,
+  VSR_ISECT_ALPHA_PROCEDURAL_UV = 7,
   VSR_ISECT_RUNTIME_SWITCH_DEFAULT = 101,
   VSR_ISECT_RUNTIME_SWITCH_ALPHA_TEXTURE = 102,
   VSR_ISECT_RUNTIME_SWITCH_ALPHA_PROCEDURAL = 103,

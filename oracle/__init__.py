@@ -25,7 +25,8 @@ LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 CLOSEST, ANY = 0, 1
 NONE, DEFAULT, ALPHA_TEX, ALPHA_PROC, COUNT = 0, 1, 2, 3, 4
-X1, X2, X3, X4 = 1, 2, 4, 8
+ALPHA_TEX_BILINEAR, ALPHA_PROC_UV = 5, 6     # NEXT-4 sampling variants (reading A28)
+X1, X2, X3, X4, X5 = 1, 2, 4, 8, 16
 
 HIT_DTYPE = np.dtype([("t", "<f4"), ("u", "<f4"), ("v", "<f4"), ("prim", "<u4")])
 COUNT_DTYPE = np.dtype([("boxes", "<u4"), ("tris", "<u4"), ("alpha", "<u4")])
@@ -85,6 +86,9 @@ def lib():
         L.oracle_mt.argtypes = [C.c_void_p] * 4 + [C.c_float] + [C.POINTER(C.c_float)] * 3
         L.oracle_tex_alpha.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_float, C.c_float]
         L.oracle_tex_alpha.restype = C.c_float
+        L.oracle_tex_alpha_bilinear.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_float,
+                                                C.c_float]
+        L.oracle_tex_alpha_bilinear.restype = C.c_float
         L.oracle_lerp2.argtypes = [C.c_void_p] * 3 + [C.c_float, C.c_float, C.c_void_p]
         L.oracle_build_bvh.argtypes = [C.POINTER(_Scene), C.c_uint32, C.POINTER(_Bvh)]
         L.oracle_bvh_free.argtypes = [C.POINTER(_Bvh)]
@@ -210,6 +214,11 @@ def mt(ray, v0, v1, v2, tmax=None):
 def tex_alpha(tex, s, t):
     tex = np.ascontiguousarray(tex, dtype=np.uint8)
     return lib().oracle_tex_alpha(tex.shape[1], tex.shape[0], _ptr(tex), s, t)
+
+
+def tex_alpha_bilinear(tex, s, t):
+    tex = np.ascontiguousarray(tex, dtype=np.uint8)
+    return lib().oracle_tex_alpha_bilinear(tex.shape[1], tex.shape[0], _ptr(tex), s, t)
 
 
 def slab(lo, hi, ray, best_t=None):

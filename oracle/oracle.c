@@ -97,6 +97,36 @@ float oracle_tex_alpha(uint32_t w, uint32_t h, const uint8_t* rgba, float s, flo
   return (float)a8 / 255.0f;
 }
 
+static long wrap_long(long i, long m) { return ((i % m) + m) % m; }
+
+float oracle_tex_alpha_bilinear(uint32_t w, uint32_t h, const uint8_t* rgba, float s, float t) {
+  float x = s * (float)w - 0.5f;
+  float y = t * (float)h - 0.5f;
+  float x0 = floorf(x), y0 = floorf(y);
+  float fx = x - x0, fy = y - y0;
+  long i0 = wrap_long((long)x0, w), i1 = wrap_long((long)x0 + 1, w);
+  long j0 = wrap_long((long)y0, h), j1 = wrap_long((long)y0 + 1, h);
+  float a00 = (float)rgba[((size_t)j0 * w + (size_t)i0) * 4 + 3] / 255.0f;
+  float a10 = (float)rgba[((size_t)j0 * w + (size_t)i1) * 4 + 3] / 255.0f;
+  float a01 = (float)rgba[((size_t)j1 * w + (size_t)i0) * 4 + 3] / 255.0f;
+  float a11 = (float)rgba[((size_t)j1 * w + (size_t)i1) * 4 + 3] / 255.0f;
+  return ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;
+}
+
+/* bilinear alpha in double (flags only) */
+static double bilinear_double(uint32_t w, uint32_t h, const uint8_t* rgba, double s, double t) {
+  double x = s * w - 0.5, y = t * h - 0.5;
+  double x0 = floor(x), y0 = floor(y);
+  double fx = x - x0, fy = y - y0;
+  long i0 = wrap_long((long)x0, w), i1 = wrap_long((long)x0 + 1, w);
+  long j0 = wrap_long((long)y0, h), j1 = wrap_long((long)y0 + 1, h);
+  double a00 = rgba[((size_t)j0 * w + (size_t)i0) * 4 + 3] / 255.0;
+  double a10 = rgba[((size_t)j0 * w + (size_t)i1) * 4 + 3] / 255.0;
+  double a01 = rgba[((size_t)j1 * w + (size_t)i0) * 4 + 3] / 255.0;
+  double a11 = rgba[((size_t)j1 * w + (size_t)i1) * 4 + 3] / 255.0;
+  return ((1 - fx) * a00 + fx * a10) * (1 - fy) + ((1 - fx) * a01 + fx * a11) * fy;
+}
+
 static uint32_t tri_texture(const or_scene* s, uint32_t i) {
   uint32_t g = s->geom_ids ? s->geom_ids[i] : 0u;
   return s->geom_texture ? s->geom_texture[g] : g;
@@ -120,6 +150,20 @@ static int filter(const or_scene* s, uint32_t i, int isect, float u, float v, fl
     int cu = (int)floorf(u * fm);
     int cv = (int)floorf(v * fm);
     return ((cu + cv) % 2) == 0;
+  }
+  if (isect == OR_ALPHA_BILIN || isect == OR_ALPHA_PROC_UV) {
+    const float* tc = s->texcoords + (size_t)i * 6;
+    float coord[2];
+    oracle_lerp2(tc, tc + 2, tc + 4, u, v, coord);
+    if (isect == OR_ALPHA_PROC_UV) {   /* checker on the texcoords (reading A28) */
+      float fm = (float)M;
+      long cs = (long)floorf(coord[0] * fm), ct = (long)floorf(coord[1] * fm);
+      return ((cs + ct) & 1L) == 0;
+    }
+    uint32_t k = tri_texture(s, i);
+    float a = oracle_tex_alpha_bilinear(s->tex_w[k], s->tex_h[k], s->tex_rgba[k], coord[0],
+                                        coord[1]);
+    return a >= thr;
   }
   return 1; /* NONE, DEFAULT, COUNT */
 }
@@ -305,6 +349,20 @@ static void trace_one(const job_t* jb, uint64_t r) {
     } else if (jb->isect == OR_ALPHA_PROC) {
       double M = (double)jb->M;
       if (dist_to_int(u * M) < 1e-6 * M || dist_to_int(v * M) < 1e-6 * M) f |= OR_X4_CHECKER_EDGE;
+    } else if (jb->isect == OR_ALPHA_BILIN || jb->isect == OR_ALPHA_PROC_UV) {
+      const float* tc = s->texcoords + (size_t)i * 6;
+      double ss = w * tc[0] + u * tc[2] + v * tc[4];
+      double tt = w * tc[1] + u * tc[3] + v * tc[5];
+      if (jb->isect == OR_ALPHA_PROC_UV) {
+        double M = (double)jb->M;
+        if (dist_to_int(ss * M) < 1e-5 * (1.0 + fabs(ss * M)) ||
+            dist_to_int(tt * M) < 1e-5 * (1.0 + fabs(tt * M)))
+          f |= OR_X4_CHECKER_EDGE;
+      } else {
+        uint32_t k = tri_texture(s, i);
+        double a = bilinear_double(s->tex_w[k], s->tex_h[k], s->tex_rgba[k], ss, tt);
+        if (fabs(a - (double)jb->thr) < 1e-4) f |= OR_X5_ALPHA_NEAR;
+      }
     }
   }
   jb->flags[r] = f;
@@ -332,8 +390,8 @@ int oracle_trace(const or_scene* s, const float* rays, uint64_t n, int query, in
                  int nthreads) {
   if (!s || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   job_t jb;
   memset(&jb, 0, sizeof jb);
   jb.s = s; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect;
@@ -345,8 +403,8 @@ int oracle_trace_multi(const or_scene* s, const float* rays, uint64_t n, uint32_
                        float thr, uint32_t M, or_hit* hits, uint32_t* nhits, uint32_t* ncut,
                        int nthreads) {
   if (!s || !rays || !hits || K < 1) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   job_t jb;
   memset(&jb, 0, sizeof jb);
   jb.s = s; jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect;

@@ -35,11 +35,14 @@ extern "C" {
 enum { OR_CLOSEST = 0, OR_ANY = 1 };
 /* intersector kinds (PAPER.md:195-219 default overload vs intersector;
    §4 listings: alpha texture :296-316, procedural :319-322, bvh_costs :332-366) */
-enum { OR_NONE = 0, OR_DEFAULT = 1, OR_ALPHA_TEX = 2, OR_ALPHA_PROC = 3, OR_COUNT = 4 };
+enum { OR_NONE = 0, OR_DEFAULT = 1, OR_ALPHA_TEX = 2, OR_ALPHA_PROC = 3, OR_COUNT = 4,
+       /* NEXT-4 sampling variants (reading A28): bilinear alpha, and the
+          procedural checker on the interpolated texcoords instead of (u, v) */
+       OR_ALPHA_BILIN = 5, OR_ALPHA_PROC_UV = 6 };
 
 /* ambiguity flags (SURVEY.md §8(c) exclusion classes), computed in double */
 enum { OR_X1_NEAR_TIE = 1u, OR_X2_EDGE_GRAZE = 2u, OR_X3_TEXEL_EDGE = 4u,
-       OR_X4_CHECKER_EDGE = 8u };
+       OR_X4_CHECKER_EDGE = 8u, OR_X5_ALPHA_NEAR = 16u /* bilinear alpha within 1e-4 of thr */ };
 
 typedef struct {
   uint32_t num_tris;
@@ -83,6 +86,10 @@ int oracle_eval_pair(const or_scene* s, const float* ray, uint32_t prim, int ise
 int oracle_mt(const float* ray, const float* v0, const float* v1, const float* v2,
               float tmax_cur, float* t, float* u, float* v);
 float oracle_tex_alpha(uint32_t w, uint32_t h, const uint8_t* rgba, float s, float t);
+/* Bilinear tex2D (reading A28): texel centres at (i+.5)/W, wrap; x = s*W - 0.5f,
+ * i0 = floor(x), fx = x - i0 (same for y); alpha = ((1-fx)*a00 + fx*a10)*(1-fy) +
+ * ((1-fx)*a01 + fx*a11)*fy with a = a8/255.0f, fp32 in exactly this order. */
+float oracle_tex_alpha_bilinear(uint32_t w, uint32_t h, const uint8_t* rgba, float s, float t);
 void oracle_lerp2(const float* a, const float* b, const float* c, float u, float v,
                   float* out);
 

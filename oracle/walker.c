@@ -318,6 +318,29 @@ static int walk_filter(const or_bvh* b, uint32_t k, int isect, float u, float v,
     int cu = (int)floorf(u * fm), cv = (int)floorf(v * fm);
     return ((cu + cv) % 2) == 0;
   }
+  if (isect == OR_ALPHA_BILIN || isect == OR_ALPHA_PROC_UV) {
+    /* reading A28 on the A8 plane through the sidecar */
+    const or_side* sd = &b->sides[k];
+    float w = (1.0f - u) - v;
+    float s = (w * sd->uv[0] + u * sd->uv[2]) + v * sd->uv[4];
+    float t = (w * sd->uv[1] + u * sd->uv[3]) + v * sd->uv[5];
+    if (isect == OR_ALPHA_PROC_UV) {
+      float fm = (float)M;
+      long cs = (long)floorf(s * fm), ct = (long)floorf(t * fm);
+      return ((cs + ct) & 1L) == 0;
+    }
+    long W = (long)(sd->dims & 0xFFFFu) + 1, H = (long)(sd->dims >> 16) + 1;
+    float x = s * (float)W - 0.5f, y = t * (float)H - 0.5f;
+    float x0 = floorf(x), y0 = floorf(y);
+    float fx = x - x0, fy = y - y0;
+    long i0 = (((long)x0 % W) + W) % W, i1 = ((((long)x0 + 1) % W) + W) % W;
+    long j0 = (((long)y0 % H) + H) % H, j1 = ((((long)y0 + 1) % H) + H) % H;
+    const uint8_t* p = b->texels + sd->offset;
+    float a00 = (float)p[j0 * W + i0] / 255.0f, a10 = (float)p[j0 * W + i1] / 255.0f;
+    float a01 = (float)p[j1 * W + i0] / 255.0f, a11 = (float)p[j1 * W + i1] / 255.0f;
+    float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;
+    return a >= thr;
+  }
   return 1;
 }
 
@@ -485,8 +508,8 @@ int walker_trace(const or_bvh* b, const float* rays, uint64_t n, int query, int 
                  float thr, uint32_t M, or_hit* hits, or_counts* counts, int nthreads) {
   if (!b || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   wjob_t jb;
   memset(&jb, 0, sizeof jb);
   jb.b = b; jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr;
@@ -498,8 +521,8 @@ int walker_trace_multi(const or_bvh* b, const float* rays, uint64_t n, uint32_t 
                        float thr, uint32_t M, or_hit* hits, uint32_t* nhits, or_counts* counts,
                        int nthreads) {
   if (!b || !rays || !hits || K < 1 || K > MAX_MULTI) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   wjob_t jb;
   memset(&jb, 0, sizeof jb);
   jb.b = b; jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect; jb.thr = thr;
@@ -512,8 +535,8 @@ int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uin
                       or_counts* counts, int nthreads) {
   if (!list || nlist < 1 || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   wjob_t jb;
   memset(&jb, 0, sizeof jb);
   jb.b = list; jb.list = list; jb.nlist = nlist; jb.which = which;
@@ -748,8 +771,8 @@ int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_
                            or_counts* counts, int nthreads) {
   if (!top || !recs || !bottoms || nbottoms < 1 || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
-  if (isect < OR_NONE || isect > OR_COUNT) return -1;
-  if (isect == OR_ALPHA_PROC && M == 0) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   ijob_t jb;
   memset(&jb, 0, sizeof jb);
   jb.top = top; jb.recs = recs; jb.bottoms = bottoms; jb.nbottoms = nbottoms;

@@ -244,6 +244,8 @@ bool valid_isect(int k) {
     case VSR_ISECT_ALPHA_PROCEDURAL:
     case VSR_ISECT_COUNT:
     case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR:
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV:
     case VSR_ISECT_RUNTIME_SWITCH_DEFAULT:
     case VSR_ISECT_RUNTIME_SWITCH_ALPHA_TEXTURE:
     case VSR_ISECT_RUNTIME_SWITCH_ALPHA_PROCEDURAL:
@@ -273,6 +275,7 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.data.texels = s->d_texels;
   p.data.a_min = alpha_min_a8(ip.alpha_threshold);
   p.data.fm = (float)ip.checker_freq;
+  p.data.thr = ip.alpha_threshold;
   int kind = 0;
   if (isect >= 200) kind = isect - 200;
   else if (isect >= 100) kind = isect - 100;
@@ -761,7 +764,7 @@ vsr_status vsr_group_create(vsr_scene* const* scenes, uint32_t count, vsr_group*
   }
   for (uint32_t k = 0; k < count; ++k) {
     list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f};
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
     for (int a = 0; a < 3; ++a) {
       g->lo[a] = std::min(g->lo[a], scenes[k]->dev.root_lo[a]);
       g->hi[a] = std::max(g->hi[a], scenes[k]->dev.root_hi[a]);
@@ -986,7 +989,7 @@ vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
   std::vector<IsectData> data(num_scenes);
   for (uint32_t k = 0; k < num_scenes; ++k) {
     list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f};
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
   }
   DeviceGuard dg(I->device);
   cudaError_t e;

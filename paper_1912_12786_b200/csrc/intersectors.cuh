@@ -328,6 +328,45 @@ __device__ __forceinline__ bool alpha_keep(const IsectData& d, uint32_t k, float
                     u, v);
 }
 
+// NEXT-4 variant (reading A28): bilinear tex2D of the A8 plane, texel centres at
+// (i+.5)/W, wrap; the filtered alpha is compared with the threshold itself.
+__device__ __forceinline__ long long wrap_ll(long long i, long long m) { return ((i % m) + m) % m; }
+
+__device__ __forceinline__ bool alpha_bilinear_keep(const IsectData& d, uint32_t k, float u,
+                                                    float v) {
+  const float4 s0 = ldg4(d.sides + k);
+  const float4 s1 = ldg4(reinterpret_cast<const float4*>(d.sides + k) + 1);
+  const float w = (1.0f - u) - v;
+  const float s = (w * s0.x + u * s0.z) + v * s1.x;
+  const float t = (w * s0.y + u * s0.w) + v * s1.y;
+  const uint32_t dims = __float_as_uint(s1.w);
+  const long long tw = (long long)(dims & 0xFFFFu) + 1, th = (long long)(dims >> 16) + 1;
+  const float x = s * (float)tw - 0.5f, y = t * (float)th - 0.5f;
+  const float x0 = floorf(x), y0 = floorf(y);
+  const float fx = x - x0, fy = y - y0;
+  const long long i0 = wrap_ll((long long)x0, tw), i1 = wrap_ll((long long)x0 + 1, tw);
+  const long long j0 = wrap_ll((long long)y0, th), j1 = wrap_ll((long long)y0 + 1, th);
+  const uint8_t* p = d.texels + __float_as_uint(s1.z);
+  const float a00 = (float)__ldg(p + j0 * tw + i0) / 255.0f;
+  const float a10 = (float)__ldg(p + j0 * tw + i1) / 255.0f;
+  const float a01 = (float)__ldg(p + j1 * tw + i0) / 255.0f;
+  const float a11 = (float)__ldg(p + j1 * tw + i1) / 255.0f;
+  const float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;
+  return a >= d.thr;
+}
+
+// NEXT-4 variant (reading A28): the procedural checker on the interpolated
+// texcoords (s, t) instead of the barycentrics.
+__device__ __forceinline__ bool checker_uv_keep(const IsectData& d, uint32_t k, float u, float v) {
+  const float4 s0 = ldg4(d.sides + k);
+  const float4 s1 = ldg4(reinterpret_cast<const float4*>(d.sides + k) + 1);
+  const float w = (1.0f - u) - v;
+  const float s = (w * s0.x + u * s0.z) + v * s1.x;
+  const float t = (w * s0.y + u * s0.w) + v * s1.y;
+  const long long cs = (long long)floorf(s * d.fm), ct = (long long)floorf(t * d.fm);
+  return ((cs + ct) & 1ll) == 0;
+}
+
 // §4 procedural mask, read as a barycentric checkerboard (readings A4/A5).
 __device__ __forceinline__ bool checker_keep(float fm, float u, float v) {
   const int cu = (int)floorf(u * fm);
@@ -362,6 +401,30 @@ struct alpha_procedural_intersector : basic_intersector<alpha_procedural_interse
                                                    float tmax_cur) {
     hit_record hr = intersect(r, t, k, tmax_cur);
     if (hr.hit) hr.hit &= checker_keep(fm, hr.u, hr.v);
+    return hr;
+  }
+};
+
+// ALPHA_TEXTURE_BILINEAR / ALPHA_PROCEDURAL_UV: the NEXT-4 sampling variants
+// (reading A28), reported apart from the headline.
+struct alpha_bilinear_intersector : basic_intersector<alpha_bilinear_intersector> {
+  using basic_intersector<alpha_bilinear_intersector>::operator();
+  IsectData d;
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) hr.hit &= alpha_bilinear_keep(d, hr.k, hr.u, hr.v);
+    return hr;
+  }
+};
+
+struct alpha_procedural_uv_intersector : basic_intersector<alpha_procedural_uv_intersector> {
+  using basic_intersector<alpha_procedural_uv_intersector>::operator();
+  IsectData d;
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) hr.hit &= checker_uv_keep(d, hr.k, hr.u, hr.v);
     return hr;
   }
 };

@@ -89,6 +89,7 @@ struct IsectData {
   const uint8_t* texels;
   uint32_t a_min;   // smallest a8 with (float)a8/255.0f >= threshold (exact, host-derived)
   float fm;         // checker frequency M as float
+  float thr;        // the alpha threshold itself (bilinear variant compares filtered alpha)
 };
 
 // Pinhole camera for rays generated inside the trace kernel (vsr.h vsr_pinhole;

@@ -319,7 +319,9 @@ __device__ __forceinline__ void finish(const TraceParams& p, const Trav& T, cons
 template <class I>
 __device__ __forceinline__ I make_isect(const TraceParams& p) {
   I isect{};
-  if constexpr (std::is_base_of<alpha_texture_intersector, I>::value) {
+  if constexpr (std::is_base_of<alpha_texture_intersector, I>::value ||
+                std::is_same<I, alpha_bilinear_intersector>::value ||
+                std::is_same<I, alpha_procedural_uv_intersector>::value) {
     isect.d = p.data;
   } else if constexpr (std::is_base_of<alpha_procedural_intersector, I>::value) {
     isect.fm = p.data.fm;
@@ -578,7 +580,9 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_multi_kernel(const Tra
 // listing's "member variables", differ per BVH).
 template <class I>
 __device__ __forceinline__ void bind_scene_data(I& isect, const IsectData& d) {
-  if constexpr (std::is_base_of<alpha_texture_intersector, I>::value) {
+  if constexpr (std::is_base_of<alpha_texture_intersector, I>::value ||
+                std::is_same<I, alpha_bilinear_intersector>::value ||
+                std::is_same<I, alpha_procedural_uv_intersector>::value) {
     isect.d.sides = d.sides;   // threshold / checker frequency stay the call's
     isect.d.descs = d.descs;
     isect.d.texels = d.texels;
@@ -862,6 +866,8 @@ cudaError_t dispatch_multi(int isect, const TraceParams& p, cudaStream_t st) {
     case VSR_ISECT_DEFAULT: return launch_multi<default_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE: return launch_multi<alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_multi<alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_multi<alpha_bilinear_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_multi<alpha_procedural_uv_intersector>(p, st);
     case VSR_ISECT_COUNT: return launch_multi<cost_intersector<default_intersector>>(p, st);
     case VSR_ISECT_COUNT_ALPHA_TEXTURE:
       return launch_multi<cost_intersector<alpha_texture_intersector>>(p, st);
@@ -896,6 +902,8 @@ cudaError_t dispatch_inst(int isect, const TraceParams& p, cudaStream_t st) {
     case VSR_ISECT_DEFAULT: return launch_inst<Q, default_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE: return launch_inst<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_inst<Q, alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_inst<Q, alpha_bilinear_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_inst<Q, alpha_procedural_uv_intersector>(p, st);
     case VSR_ISECT_COUNT: return launch_inst<Q, cost_intersector<default_intersector>>(p, st);
     case VSR_ISECT_COUNT_ALPHA_TEXTURE:
       return launch_inst<Q, cost_intersector<alpha_texture_intersector>>(p, st);
@@ -910,6 +918,8 @@ cudaError_t dispatch_list(int isect, const TraceParams& p, cudaStream_t st) {
     case VSR_ISECT_DEFAULT: return launch_list<Q, default_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE: return launch_list<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_list<Q, alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_list<Q, alpha_bilinear_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_list<Q, alpha_procedural_uv_intersector>(p, st);
     case VSR_ISECT_COUNT: return launch_list<Q, cost_intersector<default_intersector>>(p, st);
     case VSR_ISECT_COUNT_ALPHA_TEXTURE:
       return launch_list<Q, cost_intersector<alpha_texture_intersector>>(p, st);
@@ -924,6 +934,8 @@ cudaError_t dispatch_isect(int isect, const TraceParams& p, cudaStream_t st) {
     case VSR_ISECT_DEFAULT: return launch<Q, default_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE: return launch<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch<Q, alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch<Q, alpha_bilinear_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch<Q, alpha_procedural_uv_intersector>(p, st);
     case VSR_ISECT_COUNT: return launch<Q, cost_intersector<default_intersector>>(p, st);
     case VSR_ISECT_COUNT_ALPHA_TEXTURE:
       return launch<Q, cost_intersector<alpha_texture_intersector>>(p, st);

@@ -27,11 +27,14 @@ STATUS_NAMES = ["VSR_OK", "VSR_ERR_INVALID_ARG", "VSR_ERR_EMPTY_SCENE", "VSR_ERR
 CLOSEST, ANY = 0, 1
 # vsr_isect
 NONE, DEFAULT, ALPHA_TEXTURE, ALPHA_PROCEDURAL, COUNT, COUNT_ALPHA_TEXTURE = range(6)
+ALPHA_TEXTURE_BILINEAR, ALPHA_PROCEDURAL_UV = 6, 7   # NEXT-4 sampling variants
 RUNTIME_SWITCH_DEFAULT, RUNTIME_SWITCH_ALPHA_TEXTURE, RUNTIME_SWITCH_ALPHA_PROCEDURAL = 101, 102, 103
 RUNTIME_FNPTR_DEFAULT, RUNTIME_FNPTR_ALPHA_TEXTURE, RUNTIME_FNPTR_ALPHA_PROCEDURAL = 201, 202, 203
 ISECT_NAMES = {NONE: "none", DEFAULT: "default", ALPHA_TEXTURE: "alpha_texture",
                ALPHA_PROCEDURAL: "alpha_procedural", COUNT: "count",
                COUNT_ALPHA_TEXTURE: "count_alpha_texture",
+               ALPHA_TEXTURE_BILINEAR: "alpha_texture_bilinear",
+               ALPHA_PROCEDURAL_UV: "alpha_procedural_uv",
                RUNTIME_SWITCH_DEFAULT: "runtime_switch_default",
                RUNTIME_SWITCH_ALPHA_TEXTURE: "runtime_switch_alpha_texture",
                RUNTIME_SWITCH_ALPHA_PROCEDURAL: "runtime_switch_alpha_procedural",

@@ -16,7 +16,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE = os.path.join(ROOT, "oracle")
 PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py",
-        "tests/test_instances_cpu.py"]
+        "tests/test_instances_cpu.py", "tests/test_oracle_variants.py"]
 
 MUTANTS = [
     # (file, original, mutated, description)
@@ -73,6 +73,18 @@ MUTANTS = [
      "if ((S.have && !had) || S.best_t < bt) which = k;",
      "instances: leaf position reported instead of the caller's index"),
     ("walker.c", "        if (stop) goto done;", "", "instances: any-hit keeps walking after a hit"),
+    ("oracle.c", "  float x = s * (float)w - 0.5f;\n  float y = t * (float)h - 0.5f;",
+     "  float x = s * (float)w;\n  float y = t * (float)h - 0.5f;", "bilinear: texel-centre offset dropped in x"),
+    ("oracle.c", "return ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;",
+     "return ((1.0f - fx) * a00 + fx * a01) * (1.0f - fy) + ((1.0f - fx) * a10 + fx * a11) * fy;",
+     "bilinear: corner texels transposed"),
+    ("oracle.c", "long i0 = wrap_long((long)x0, w), i1 = wrap_long((long)x0 + 1, w);",
+     "long i0 = (long)x0 < 0 ? 0 : (long)x0 % w, i1 = ((long)x0 + 1) % w;", "bilinear: clamp instead of wrap at the seam"),
+    ("oracle.c", "long cs = (long)floorf(coord[0] * fm), ct = (long)floorf(coord[1] * fm);",
+     "long cs = (long)floorf(u * fm), ct = (long)floorf(coord[1] * fm);", "uv checker: barycentric u instead of s"),
+    ("walker.c", "float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;",
+     "float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fx;",
+     "walker bilinear: fx used as the row weight"),
 ]
 
 
