@@ -330,7 +330,12 @@ __device__ __forceinline__ bool alpha_keep(const IsectData& d, uint32_t k, float
 
 // NEXT-4 variant (reading A28): bilinear tex2D of the A8 plane, texel centres at
 // (i+.5)/W, wrap; the filtered alpha is compared with the threshold itself.
-__device__ __forceinline__ long long wrap_ll(long long i, long long m) { return ((i % m) + m) % m; }
+// |texcoord| <= 1024 and W <= 65536 keep every index within int32
+__device__ __forceinline__ uint32_t wrap_i(int i, uint32_t n) {
+  if ((n & (n - 1u)) == 0u) return (uint32_t)i & (n - 1u);
+  const int m = (int)n;
+  return (uint32_t)(((i % m) + m) % m);
+}
 
 __device__ __forceinline__ bool alpha_bilinear_keep(const IsectData& d, uint32_t k, float u,
                                                     float v) {
@@ -340,17 +345,17 @@ __device__ __forceinline__ bool alpha_bilinear_keep(const IsectData& d, uint32_t
   const float s = (w * s0.x + u * s0.z) + v * s1.x;
   const float t = (w * s0.y + u * s0.w) + v * s1.y;
   const uint32_t dims = __float_as_uint(s1.w);
-  const long long tw = (long long)(dims & 0xFFFFu) + 1, th = (long long)(dims >> 16) + 1;
+  const uint32_t tw = (dims & 0xFFFFu) + 1u, th = (dims >> 16) + 1u;
   const float x = s * (float)tw - 0.5f, y = t * (float)th - 0.5f;
   const float x0 = floorf(x), y0 = floorf(y);
   const float fx = x - x0, fy = y - y0;
-  const long long i0 = wrap_ll((long long)x0, tw), i1 = wrap_ll((long long)x0 + 1, tw);
-  const long long j0 = wrap_ll((long long)y0, th), j1 = wrap_ll((long long)y0 + 1, th);
+  const uint32_t i0 = wrap_i((int)x0, tw), i1 = wrap_i((int)x0 + 1, tw);
+  const uint64_t r0 = (uint64_t)wrap_i((int)y0, th) * tw, r1 = (uint64_t)wrap_i((int)y0 + 1, th) * tw;
   const uint8_t* p = d.texels + __float_as_uint(s1.z);
-  const float a00 = (float)__ldg(p + j0 * tw + i0) / 255.0f;
-  const float a10 = (float)__ldg(p + j0 * tw + i1) / 255.0f;
-  const float a01 = (float)__ldg(p + j1 * tw + i0) / 255.0f;
-  const float a11 = (float)__ldg(p + j1 * tw + i1) / 255.0f;
+  const float a00 = (float)__ldg(p + r0 + i0) / 255.0f;
+  const float a10 = (float)__ldg(p + r0 + i1) / 255.0f;
+  const float a01 = (float)__ldg(p + r1 + i0) / 255.0f;
+  const float a11 = (float)__ldg(p + r1 + i1) / 255.0f;
   const float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;
   return a >= d.thr;
 }
@@ -364,7 +369,7 @@ __device__ __forceinline__ bool checker_uv_keep(const IsectData& d, uint32_t k, 
   const float s = (w * s0.x + u * s0.z) + v * s1.x;
   const float t = (w * s0.y + u * s0.w) + v * s1.y;
   const long long cs = (long long)floorf(s * d.fm), ct = (long long)floorf(t * d.fm);
-  return ((cs + ct) & 1ll) == 0;
+  return ((cs + ct) & 1ll) == 0;   // s*M may exceed int32 (|s| <= 1024, M <= 2^24)
 }
 
 // §4 procedural mask, read as a barycentric checkerboard (readings A4/A5).
