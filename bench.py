@@ -58,8 +58,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--max-leaf", type=int, default=2, help="BVH build: max triangles per leaf")
     ap.add_argument("--sah-bins", type=int, default=16, help="BVH build: SAH bins per axis")
-    ap.add_argument("--mode", default="weak", choices=["weak", "tiles"],
-                    help="weak: a frame per rank; tiles: one frame's tiles over the ranks + gather")
+    ap.add_argument("--mode", default="weak", choices=["weak", "tiles", "tiles-nccl"],
+                    help="weak: a frame per rank; tiles: one frame's tiles over the ranks, each "
+                         "trace kernel storing its hits into rank 0's frame over CUDA IPC/NVLink "
+                         "(vsr_trace_tiles); tiles-nccl: the same with an NCCL all-gather")
     return ap.parse_args()
 
 
@@ -212,7 +214,8 @@ def run_own(args):
         scene = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf, sah_bins=args.sah_bins)
     setup_s = time.time() - t0
     stats = scene.stats()
-    tiles = args.mode == "tiles"
+    tiles = args.mode in ("tiles", "tiles-nccl")
+    fused = args.mode == "tiles"
     tile_rays = 64 * rays.spp
     if tiles:   # strong scaling: this rank's round-robin 8x8-tile shard of ONE frame
         local_rays = rays.data[shard.rank_ray_indices(rays.n, tile_rays, rank, world)]
@@ -222,7 +225,13 @@ def run_own(args):
     d_rays = torch.from_numpy(np.ascontiguousarray(local_rays)).cuda()
     hits = torch.empty((n, 4), dtype=torch.float32, device="cuda")
     gathered = None
-    if tiles and world > 1:
+    peer = None
+    if fused:   # rank 0's frame, mapped into every rank (IPC); each kernel stores its tiles there
+        peer = shard.PeerFrame(rays.n, local, dist) if world > 1 else None
+        frame_local = None if peer is not None else torch.empty((rays.n, 4), dtype=torch.float32,
+                                                                 device="cuda")
+        frame_ptr = peer.ptr if peer is not None else frame_local.data_ptr()
+    elif tiles and world > 1:
         gathered = torch.empty((world * n, 4), dtype=torch.float32, device="cuda" if backend == "nccl" else "cpu")
     counts = torch.empty((n, 4), dtype=torch.int32, device="cuda")
     l2 = torch.cuda.get_device_properties(local).L2_cache_size
@@ -245,6 +254,9 @@ def run_own(args):
         if query == "multi":   # multi-hit query, k = 4
             scene.trace_multi(d_rays, multi_k, kind, hits=multi_hits, num_hits=multi_n,
                               counts=counts, stream=sh)
+            return
+        if fused and kind not in (vsr.COUNT, vsr.COUNT_ALPHA_TEXTURE):
+            scene.trace_tiles(d_rays, tile_rays, rank, world, frame_ptr, query, kind, stream=sh)
             return
         scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
                         counts.data_ptr(), sh)
@@ -492,13 +504,17 @@ def run_own(args):
                        "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
                        "l2": "flushed before every timed step (read of a 256 MiB buffer, outside the events)",
                        "parallelism": (f"one frame's 8x8 tiles dealt round-robin over {world} rank(s), "
-                                       "hits all-gathered (NCCL) inside each step" if tiles else
+                                       + ("each trace kernel stores its hits into rank 0's frame "
+                                          "(CUDA IPC, NVLink peer stores; vsr_trace_tiles)" if fused
+                                          else "hits all-gathered (NCCL) inside each step") if tiles else
                                        f"rays sharded by frame, {world} rank(s), no data-path collective"),
                        "setup_s": round(setup_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "ms_per_step_each": [round(x, 4) for x in ms], **extra,
         }
         print(json.dumps(line))
+    if peer is not None:
+        peer.release(dist)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

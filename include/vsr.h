@@ -298,6 +298,29 @@ typedef struct {
 } vsr_instances_view;
 vsr_status vsr_instances_export(const vsr_instances* inst, vsr_instances_view* view);
 
+/* Multi-GPU frame assembly fused into the trace: this rank traces its
+ * round-robin tile shard — its j-th tile is frame tile j*world + rank, tile_rays rays per tile,
+ * n = its ray count (a multiple of tile_rays, n < 2^32) — and the kernel stores every hit (and
+ * count) straight to that ray's FRAME position in d_frame_hits / d_frame_counts.  Those are
+ * normally rank 0's frame buffers opened in this process with vsr_ipc_open, so the stores travel
+ * over NVLink / NVSwitch inside the trace kernel and no gather collective runs.  The frame is
+ * complete once every rank's stream has passed the call (the caller synchronises: stream sync +
+ * barrier).  Other arguments and errors as vsr_trace. */
+vsr_status vsr_trace_tiles(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, uint32_t tile_rays,
+                           uint32_t rank, uint32_t world, vsr_query query, vsr_isect isect,
+                           const vsr_isect_params* params, vsr_hit* d_frame_hits,
+                           vsr_counts* d_frame_counts, void* stream);
+
+/* Device buffers that other processes can map (CUDA IPC).  vsr_device_alloc: cudaMalloc on
+ * `device` (the pointer is an allocation base, as IPC requires); vsr_ipc_handle: its 64-byte
+ * handle; vsr_ipc_open: map a handle from another process on this process's `device` (peer
+ * access enabled lazily); vsr_ipc_close / vsr_device_free undo them.  Errors: INVALID_ARG, CUDA. */
+vsr_status vsr_device_alloc(uint64_t bytes, int device, void** d_ptr);
+vsr_status vsr_device_free(void* d_ptr, int device);
+vsr_status vsr_ipc_handle(const void* d_ptr, void* handle64);
+vsr_status vsr_ipc_open(const void* handle64, int device, void** d_ptr);
+vsr_status vsr_ipc_close(void* d_ptr, int device);
+
 /* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
  * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
  * overlap the kernel; returns after the stream work completed. */

@@ -601,6 +601,100 @@ vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
   return VSR_OK;
 }
 
+vsr_status vsr_trace_tiles(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint32_t tile_rays,
+                           uint32_t rank, uint32_t world, vsr_query query, vsr_isect isect,
+                           const vsr_isect_params* params, vsr_hit* d_hits, vsr_counts* d_counts,
+                           void* stream) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  TraceParams p;
+  vsr_status st = make_params(s, query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
+  if (tile_rays == 0 || world == 0 || rank >= world)
+    return fail(VSR_ERR_INVALID_ARG, "need tile_rays > 0 and rank < world");
+  if (n % tile_rays) return fail(VSR_ERR_INVALID_ARG, "n must be a whole number of tiles");
+  if (n >= (1ull << 32) || (n / tile_rays) * (uint64_t)world * tile_rays >= (1ull << 40))
+    return fail(VSR_ERR_INVALID_ARG, "shard too large");
+  if (n == 0) return VSR_OK;
+  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  if (!aligned16(d_rays) || !aligned16(d_hits))
+    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  p.rays = reinterpret_cast<const float4*>(d_rays);
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  p.out_tile = tile_rays;
+  p.out_rank = rank;
+  p.out_world = world;
+  p.sched = kSchedDirect;
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "tile trace launch");
+  return VSR_OK;
+}
+
+vsr_status vsr_device_alloc(uint64_t bytes, int device, void** d_ptr) {
+  g_err.clear();
+  if (!d_ptr || bytes == 0 || device < 0) return fail(VSR_ERR_INVALID_ARG, "bad allocation request");
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = cudaMalloc(d_ptr, bytes);
+  if (e != cudaSuccess) {
+    *d_ptr = nullptr;
+    return e == cudaErrorMemoryAllocation ? fail(VSR_ERR_OOM, "cudaMalloc") : cuda_fail(e, "cudaMalloc");
+  }
+  return VSR_OK;
+}
+
+vsr_status vsr_device_free(void* d_ptr, int device) {
+  g_err.clear();
+  if (!d_ptr) return VSR_OK;
+  DeviceGuard g(device);
+  cudaError_t e = cudaFree(d_ptr);
+  return e == cudaSuccess ? VSR_OK : cuda_fail(e, "cudaFree");
+}
+
+vsr_status vsr_ipc_handle(const void* d_ptr, void* handle64) {
+  g_err.clear();
+  if (!d_ptr || !handle64) return fail(VSR_ERR_INVALID_ARG, "NULL pointer or handle");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle64, &h, sizeof h);
+  return VSR_OK;
+}
+
+vsr_status vsr_ipc_open(const void* handle64, int device, void** d_ptr) {
+  g_err.clear();
+  if (!handle64 || !d_ptr || device < 0) return fail(VSR_ERR_INVALID_ARG, "bad IPC open request");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  DeviceGuard g(device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    *d_ptr = nullptr;
+    return cuda_fail(e, "cudaIpcOpenMemHandle");
+  }
+  return VSR_OK;
+}
+
+vsr_status vsr_ipc_close(void* d_ptr, int device) {
+  g_err.clear();
+  if (!d_ptr) return VSR_OK;
+  DeviceGuard g(device);
+  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
+  return e == cudaSuccess ? VSR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
 vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query query,
                              vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                              vsr_counts* d_counts, void* stream) {

@@ -310,9 +310,16 @@ __device__ __forceinline__ int warp_octant(const RayCtx& r) {
 
 template <class I>
 __device__ __forceinline__ void finish(const TraceParams& p, const Trav& T, const I& isect) {
-  p.hits[T.id] = make_float4(T.t, T.u, T.v, __uint_as_float(T.prim));
+  uint64_t o = T.id;
+  if (p.out_world) {   // vsr_trace_tiles: local tile j is frame tile j*world + rank
+    const uint32_t local = (uint32_t)T.id, tile = local / p.out_tile;
+    o = ((uint64_t)tile * p.out_world + p.out_rank) * p.out_tile + (local - tile * p.out_tile);
+  }
+  // hits may live in a peer GPU's frame buffer (CUDA IPC over NVLink): plain stores,
+  // complete when this kernel is
+  p.hits[o] = make_float4(T.t, T.u, T.v, __uint_as_float(T.prim));
   if constexpr (I::kCounts) {
-    p.counts[T.id] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
+    p.counts[o] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
   }
 }
 

@@ -35,6 +35,7 @@ struct TraceParams {
   uint32_t list_count;
   uint32_t* which;               // list / instance query: optional per-ray element of the hit
   const Instance* instances;     // instance query: records in top-level leaf order (p.scene = top)
+  uint32_t out_tile, out_rank, out_world;   // vsr_trace_tiles output mapping (world 0: identity)
   int gen;                       // 1: rays generated in-kernel from `cam` (rays unused)
   Pinhole cam;
   int runtime_kind;

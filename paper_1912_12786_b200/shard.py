@@ -116,3 +116,56 @@ def gather_hits(local_hits, n_total: int, rays_per_tile: int, dist, out=None, re
     # rank r's j-th tile is global tile r + j*world
     g = gathered.view(world, sizes[0] // rays_per_tile, rays_per_tile, 4)
     return g.transpose(0, 1).reshape(n_total, 4)
+
+
+def frame_index(local_ids, rays_per_tile: int, rank: int, world: int) -> np.ndarray:
+    """Frame position of this rank's local ray i (its j-th tile is frame tile j*world + rank):
+    the mapping vsr_trace_tiles applies when storing hits; inverse of rank_ray_indices."""
+    local_ids = np.asarray(local_ids, dtype=np.int64)
+    tile = local_ids // rays_per_tile
+    return (tile * world + rank) * rays_per_tile + local_ids % rays_per_tile
+
+
+class PeerFrame:
+    """A frame hit buffer on rank ``owner`` that every rank's trace kernel writes into directly
+    (vsr_trace_tiles over CUDA IPC / NVLink): the owner allocates it (vsr_device_alloc) and
+    publishes its IPC handle; the other ranks map it (vsr_ipc_open).  ``ptr`` is valid in every
+    process; ``tensor()`` (owner only) views it as a [rows, 4] float32 torch tensor."""
+
+    def __init__(self, rows: int, device: int, dist, owner: int = 0):
+        from . import vsr
+        self.vsr, self.rows, self.device, self.owner = vsr, rows, device, owner
+        self.rank = dist.get_rank()
+        box = [None]
+        if self.rank == owner:
+            self.ptr = vsr.device_alloc(rows * 16, device)
+            box = [vsr.ipc_handle(self.ptr)]
+        dist.broadcast_object_list(box, src=owner)
+        if self.rank != owner:
+            self.ptr = vsr.ipc_open(box[0], device)
+
+    def tensor(self):
+        import torch
+        assert self.rank == self.owner, "only the owner reads the frame"
+        return torch.as_tensor(self.vsr.DeviceArray(self.ptr, (self.rows, 4), "<f4"),
+                               device=f"cuda:{self.device}")
+
+    def release(self, dist):
+        """Collective teardown: peers unmap first, then the owner frees."""
+        import torch
+        torch.cuda.synchronize()
+        dist.barrier()
+        if self.rank != self.owner:
+            self.close()
+        dist.barrier()
+        if self.rank == self.owner:
+            self.close()
+
+    def close(self):
+        if self.ptr:
+            if self.rank == self.owner:
+                self.vsr.device_free(self.ptr, self.device)
+            else:
+                self.vsr.ipc_close(self.ptr, self.device)
+            self.ptr = 0
+

@@ -53,7 +53,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_set_kernel_events", "vsr_group_create", "vsr_group_destroy",
                     "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
                     "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
-                    "vsr_trace_pinhole"]
+                    "vsr_trace_pinhole", "vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free",
+                    "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close"]
 
 
 class VsrError(RuntimeError):
@@ -158,6 +159,16 @@ def lib():
         L.vsr_trace_pinhole.argtypes = [P, C.POINTER(Pinhole), C.c_int, C.c_int,
                                         C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_pinhole.restype = C.c_int
+        L.vsr_trace_tiles.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                      C.c_int, C.POINTER(IsectParams), P, P, P]
+        L.vsr_device_alloc.argtypes = [C.c_uint64, C.c_int, C.POINTER(P)]
+        L.vsr_device_free.argtypes = [P, C.c_int]
+        L.vsr_ipc_handle.argtypes = [P, P]
+        L.vsr_ipc_open.argtypes = [P, C.c_int, C.POINTER(P)]
+        L.vsr_ipc_close.argtypes = [P, C.c_int]
+        for name in ("vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free", "vsr_ipc_handle",
+                     "vsr_ipc_open", "vsr_ipc_close"):
+            getattr(L, name).restype = C.c_int
         L.vsr_bvh_build_gpu.restype = C.c_int
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
@@ -326,6 +337,16 @@ class Scene:
         _check(lib().vsr_trace_pinhole(self._h, C.byref(camera), query, isect, C.byref(prm),
                                        _ptr(hits), _ptr(counts), _stream_handle(stream)))
         return hits, counts
+
+    def trace_tiles(self, rays, tile_rays, rank, world, frame_hits_ptr, query=CLOSEST,
+                    isect=DEFAULT, frame_counts_ptr=None, stream=None, alpha_threshold=0.01,
+                    checker_freq=8):
+        """vsr_trace_tiles: trace this rank's tile shard `rays` and store each hit at its frame
+        position in the buffer at `frame_hits_ptr` (e.g. rank 0's frame via ipc_open)."""
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_tiles(self._h, _ptr(rays), rays.shape[0], tile_rays, rank, world,
+                                     query, isect, C.byref(prm), frame_hits_ptr,
+                                     frame_counts_ptr, _stream_handle(stream)))
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, hits=None, num_hits=None, counts=None,
                     stream=None, alpha_threshold=0.01, checker_freq=8):
@@ -508,6 +529,42 @@ class Instances:
         return {"root_ref": int(v.root_ref), "root_lo": np.array(v.root_lo, np.float32),
                 "root_hi": np.array(v.root_hi, np.float32), "nodes": nodes, "records": recs,
                 "max_depth": int(v.max_depth)}
+
+
+# ---- device buffers shared across processes (CUDA IPC) ----------------------------------
+def device_alloc(nbytes: int, device: int) -> int:
+    p = C.c_void_p()
+    _check(lib().vsr_device_alloc(nbytes, device, C.byref(p)))
+    return p.value
+
+
+def device_free(ptr: int, device: int):
+    _check(lib().vsr_device_free(ptr, device))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    h = (C.c_uint8 * 64)()
+    _check(lib().vsr_ipc_handle(ptr, h))
+    return bytes(h)
+
+
+def ipc_open(handle: bytes, device: int) -> int:
+    h = (C.c_uint8 * 64)(*handle)
+    p = C.c_void_p()
+    _check(lib().vsr_ipc_open(h, device, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int, device: int):
+    _check(lib().vsr_ipc_close(ptr, device))
+
+
+class DeviceArray:
+    """A raw device pointer seen by torch without a copy (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
 
 
 def hits_to_numpy(hits) -> np.ndarray:

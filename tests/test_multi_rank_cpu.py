@@ -74,3 +74,16 @@ def test_rank_indices_partition():
         allidx = np.sort(np.concatenate(parts))
         assert np.array_equal(allidx, np.arange(n))
         assert len({len(p) for p in parts}) == 1
+
+
+def test_frame_index_inverts_the_tile_deal():
+    """vsr_trace_tiles' store mapping (shard.frame_index) sends local ray i of rank r to the
+    frame position rank_ray_indices gave it, for tile counts that do and do not divide P."""
+    from paper_1912_12786_b200 import shard
+
+    for n_tiles, tile in ((32400, 64), (37, 256), (5, 64)):
+        n = n_tiles * tile
+        for P in (1, 2, 3, 8):
+            for r in range(P):
+                idx = shard.rank_ray_indices(n, tile, r, P)
+                assert np.array_equal(shard.frame_index(np.arange(idx.size), tile, r, P), idx)
