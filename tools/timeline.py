@@ -1,6 +1,10 @@
 """Diagnostic: per-warp (SM, start, end) timeline of the C2 headline trace.
 
-Run with VSR_LIB=variants/lib_timeline.so (built with -DVSR_TIMELINE)."""
+    VSR_LIB=variants/lib_timeline.so QUERY=any python tools/timeline.py
+
+(the variant is built with -DVSR_TIMELINE; the kernel then stores per-warp SM id and global-timer
+start/end in the counts buffer).  Prints the launch span, the per-SM first start / last end, the
+time SMs sit idle before the span ends (tail) and warp-duration percentiles."""
 import os
 import sys
 
@@ -17,9 +21,30 @@ d = torch.from_numpy(rays.data).cuda()
 hits = torch.empty((rays.n, 4), device="cuda")
 tl = torch.zeros((rays.n // 32 + 1, 4), dtype=torch.int32, device="cuda")
 isect = getattr(vsr, os.environ.get("ISECT", "ALPHA_TEXTURE"))
+q = vsr.ANY if os.environ.get("QUERY", "any") == "any" else vsr.CLOSEST
+flush = torch.zeros(64 << 20, device="cuda")
 for _ in range(5):
-    s.trace(d, vsr.CLOSEST, isect, hits=hits, counts=tl)
+    flush.sum()
+    s.trace(d, q, isect, hits=hits, counts=tl)
 torch.cuda.synchronize()
-out = tl.cpu().numpy().view(np.uint32)
+out = tl.cpu().numpy().view(np.uint32)[: rays.n // 32]
 np.save(os.environ.get("OUT", "gpurun_out/timeline.npy"), out)
-print("saved", out.shape)
+sm = out[:, 0].astype(np.int64)
+t0 = (out[:, 3].astype(np.int64) << 32) | out[:, 1].astype(np.int64)
+t1 = (t0 & ~0xFFFFFFFF) | out[:, 2].astype(np.int64)
+t1 = np.where(t1 < t0, t1 + (1 << 32), t1)
+base = t0.min()
+t0, t1 = (t0 - base) / 1e3, (t1 - base) / 1e3          # µs
+span = t1.max()
+first = np.array([t0[sm == k].min() for k in np.unique(sm)])
+last = np.array([t1[sm == k].max() for k in np.unique(sm)])
+dur = t1 - t0
+busy = np.zeros(len(np.unique(sm)))
+print(f"span {span:.1f} us over {len(first)} SMs, {len(t0)} warps")
+print(f"per-SM first start: min {first.min():.2f} median {np.median(first):.2f} max {first.max():.2f} us")
+print(f"per-SM last end:    min {last.min():.1f} median {np.median(last):.1f} max {last.max():.1f} us")
+print(f"mean SM idle at the tail: {np.mean(span - last):.1f} us ({100 * np.mean(span - last) / span:.1f} %)")
+for p in (50, 90, 99, 99.9, 100):
+    print(f"warp duration p{p}: {np.percentile(dur, p):.1f} us")
+late = t0 > 0.9 * span
+print(f"warps starting in the last 10 % of the span: {late.sum()}, their mean duration {dur[late].mean() if late.any() else 0:.1f} us")
