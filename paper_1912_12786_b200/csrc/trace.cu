@@ -19,7 +19,6 @@
 //
 // Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (IEEE fp32
 // contract).
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -32,7 +31,6 @@
 
 namespace vsr {
 
-namespace cg = cooperative_groups;
 #ifndef VSR_BLOCK
 #define VSR_BLOCK 128
 #endif
@@ -361,10 +359,14 @@ __device__ __forceinline__ uint64_t global_ns() {
 // The last rays to start bound a launch's tail by their own latency, so the
 // blocks whose rays cross the most of the scene are launched first.  Cost
 // proxy per 128-ray block: the longest segment of 4 sample rays inside the
-// padded root box, in 32 buckets of the root diagonal; a counting sort
+// padded root box, in 128 buckets of the root diagonal; a counting sort
 // (histogram + scatter, most expensive bucket first) gives the permutation.
 // ---------------------------------------------------------------------------
-constexpr int kOrderBuckets = 32;
+#ifndef VSR_ORDER_BUCKETS
+#define VSR_ORDER_BUCKETS 128
+#endif
+constexpr int kOrderBuckets = VSR_ORDER_BUCKETS;   // multiple of 32, <= 1024
+static_assert(kOrderBuckets % 32 == 0 && kOrderBuckets <= 1024, "bucket count");
 
 template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
   // CTA-local histogram first: a handful of buckets take almost all blocks,
   // so per-block global atomics would serialise on a few addresses.
   __shared__ uint32_t lh[kOrderBuckets], lbase[kOrderBuckets];
-  if (threadIdx.x < kOrderBuckets) lh[threadIdx.x] = 0;
+  for (int i = threadIdx.x; i < kOrderBuckets; i += 256) lh[i] = 0;
   __syncthreads();
   const bool leader = (t & 3u) == 0u && b < nblocks;
   int q = 0;
@@ -408,8 +410,8 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
     lpos = atomicAdd(lh + q, 1u);
   }
   __syncthreads();
-  if (threadIdx.x < kOrderBuckets && lh[threadIdx.x])
-    lbase[threadIdx.x] = atomicAdd(hist + threadIdx.x, lh[threadIdx.x]);
+  for (int i = threadIdx.x; i < kOrderBuckets; i += 256)
+    if (lh[i]) lbase[i] = atomicAdd(hist + i, lh[i]);
   __syncthreads();
   if (leader) slot[b] = ((uint32_t)q << 24) | (lbase[q] + lpos);
 }
@@ -420,90 +422,29 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
   asm volatile("griddepcontrol.launch_dependents;");   // the trace kernel may launch now ...
   asm volatile("griddepcontrol.wait;" ::: "memory");    // ... and this one waits for the cost pass
   if (threadIdx.x < 32) {   // exclusive scan over buckets, most expensive first
-    const unsigned lane = threadIdx.x;
-    const int q = kOrderBuckets - 1 - (int)lane;
-    const uint32_t cnt = __ldcg(hist + q);
-    uint32_t incl = cnt;
+    constexpr int R = kOrderBuckets / 32;   // consecutive buckets per lane
+    const int lane = (int)threadIdx.x;
+    uint32_t cnt[R], sum = 0;
+    for (int k = 0; k < R; ++k) {
+      cnt[k] = __ldcg(hist + (kOrderBuckets - 1 - (lane * R + k)));
+      sum += cnt[k];
+    }
+    uint32_t incl = sum;
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if ((int)lane >= o) incl += v;
+      if (lane >= o) incl += v;
     }
-    start[q] = incl - cnt;
+    uint32_t run = incl - sum;
+    for (int k = 0; k < R; ++k) {
+      start[kOrderBuckets - 1 - (lane * R + k)] = run;
+      run += cnt[k];
+    }
   }
   __syncthreads();
   const uint32_t b = blockIdx.x * 256 + threadIdx.x;
   if (b >= nblocks) return;
   const uint32_t s = __ldcg(slot + b);
   perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
-}
-
-// Both order phases in ONE cooperative launch (grid-wide barrier between the
-// histogram and the scatter); the grid is sized to be co-resident.
-__global__ void __launch_bounds__(256) order_coop_kernel(const TraceParams p, uint32_t nblocks,
-                                                         uint32_t* hist, uint32_t* slot,
-                                                         uint32_t* perm) {
-  cg::grid_group grid = cg::this_grid();
-  __shared__ uint32_t lh[kOrderBuckets], lbase[kOrderBuckets], start[kOrderBuckets];
-  const float dx = p.scene.root_hi[0] - p.scene.root_lo[0];
-  const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
-  const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
-  const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
-  const uint32_t total = 4 * nblocks;
-  const uint32_t stride = gridDim.x * 256;
-  for (uint32_t base = blockIdx.x * 256; base < total + 0; base += stride) {
-    const uint32_t t = base + threadIdx.x;
-    const uint32_t b = t >> 2;
-    float len = 0.0f;
-    if (b < nblocks) {
-      const uint64_t id = (uint64_t)b * kBlock + (t & 3u) * (uint32_t)((kBlock - 1) / 3);
-      if (id < p.n) {
-        const float4 a = __ldg(p.rays + 2 * id), d = __ldg(p.rays + 2 * id + 1);
-        RayCtx r;
-        make_ray(r, a, d);
-        const float t0x = (p.scene.root_lo[0] - r.ox) * r.ix, t1x = (p.scene.root_hi[0] - r.ox) * r.ix;
-        const float t0y = (p.scene.root_lo[1] - r.oy) * r.iy, t1y = (p.scene.root_hi[1] - r.oy) * r.iy;
-        const float t0z = (p.scene.root_lo[2] - r.oz) * r.iz, t1z = (p.scene.root_hi[2] - r.oz) * r.iz;
-        const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
-        const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
-        if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
-      }
-    }
-    len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 1));
-    len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 2));
-    if (threadIdx.x < kOrderBuckets) lh[threadIdx.x] = 0;
-    __syncthreads();
-    const bool leader = (t & 3u) == 0u && b < nblocks;
-    int q = 0;
-    uint32_t lpos = 0;
-    if (leader) {
-      q = diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
-      q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
-      lpos = atomicAdd(lh + q, 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < kOrderBuckets && lh[threadIdx.x])
-      lbase[threadIdx.x] = atomicAdd(hist + threadIdx.x, lh[threadIdx.x]);
-    __syncthreads();
-    if (leader) slot[b] = ((uint32_t)q << 24) | (lbase[q] + lpos);
-    __syncthreads();
-  }
-  grid.sync();
-  if (threadIdx.x < 32) {   // exclusive scan over buckets, most expensive first
-    const unsigned lane = threadIdx.x;
-    const int q = kOrderBuckets - 1 - (int)lane;
-    const uint32_t cnt = __ldcg(hist + q);
-    uint32_t incl = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-      if ((int)lane >= o) incl += v;
-    }
-    start[q] = incl - cnt;
-  }
-  __syncthreads();
-  for (uint32_t b = blockIdx.x * 256 + threadIdx.x; b < nblocks; b += stride) {
-    const uint32_t s = __ldcg(slot + b);
-    perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
-  }
 }
 
 // First statement of every trace kernel.  After an order pass the kernel is a
@@ -514,7 +455,8 @@ __global__ void __launch_bounds__(256) order_coop_kernel(const TraceParams p, ui
 // scratch's next use (the stream orders that after this launch).
 __device__ __forceinline__ uint64_t launch_block(const TraceParams& p) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (p.hist_reset && blockIdx.x == 0 && threadIdx.x < kOrderBuckets) p.hist_reset[threadIdx.x] = 0u;
+  if (p.hist_reset && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) p.hist_reset[i] = 0u;
   return p.perm ? (uint64_t)__ldcg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
 }
 
@@ -1016,31 +958,10 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     uint32_t* hist = static_cast<uint32_t*>(scratch);
     uint32_t* slot = hist + kOrderBuckets;
     uint32_t* perm = slot + nblocks;
-#ifdef VSR_ORDER_COOP
-    const bool zeroed = false;
-#else
     const bool zeroed = !owned;   // caller scratch: zero at entry, kept so by the trace kernel
-#endif
     if (!zeroed &&
         (e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess)
       return e;
-#ifdef VSR_ORDER_COOP
-    {
-      static int coop_blocks = 0;
-      if (coop_blocks == 0) {
-        int nb = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, order_coop_kernel, 256, 0);
-        coop_blocks = (nb > 0 ? nb : 1) * sm_count();
-        if (coop_blocks > sm_count()) coop_blocks = sm_count();   // one CTA per SM is plenty
-      }
-      uint32_t nb32 = (uint32_t)nblocks;
-      void* args[] = {&p, &nb32, &hist, &slot, &perm};
-      if ((e = cudaLaunchCooperativeKernel((const void*)order_coop_kernel, coop_blocks, 256, args, 0,
-                                           st)) != cudaSuccess)
-        return e;
-      g_launches.fetch_add(1, std::memory_order_relaxed);
-    }
-#else
     if (p.gen)
       order_cost_kernel<true><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
           p, (uint32_t)nblocks, hist, slot);
@@ -1056,7 +977,6 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     }
     g_launches.fetch_add(2, std::memory_order_relaxed);
     if (!owned) p.hist_reset = hist;   // the trace kernel re-zeroes it for the next launch
-#endif
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     p.perm = perm;
   }
