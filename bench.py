@@ -441,21 +441,24 @@ def run_own(args):
         del h_out
     if not args.no_variants:
         # NEXT-3: the same scene built by the GPU linear-BVH builder (build time, trace speed)
-        gscene = vsr.Scene.from_workload(sc, device=local)
-        gscene.build_gpu(args.max_leaf)   # first call: CUDA module / CUB setup
-        gscene.build_gpu(args.max_leaf)
-        gst = gscene.stats()
-        saved = scene
-        scene = gscene
-        mg, _ = timed(isect, max(5, args.steps // 2), 3)
-        scene = saved
-        extra["gpu_build"] = {"builder": "vsr_bvh_build_gpu (LBVH, Karras 2012)",
-                              "build_ms": round(gst["build_ms"], 2),
-                              "host_sah_build_ms": round(stats["build_ms"], 2),
-                              "nodes": gst["num_nodes"], "max_depth": gst["max_depth"],
-                              "value": round(n / (np.mean(mg) * 1e-3) / 1e6, 1),
-                              "ms": round(float(np.mean(mg)), 4)}
-        del gscene
+        gb = {"host_sah_build_ms": round(stats["build_ms"], 2)}
+        for name, how in (("lbvh", lambda s: s.build_gpu(args.max_leaf)),
+                          ("ploc", lambda s: s.build_ploc(args.max_leaf, 16))):
+            gscene = vsr.Scene.from_workload(sc, device=local)
+            how(gscene)   # first call: CUDA module / CUB setup
+            how(gscene)
+            gst = gscene.stats()
+            saved = scene
+            scene = gscene
+            mg, _ = timed(isect, max(5, args.steps // 2), 3)
+            scene = saved
+            gb[name] = {"build_ms": round(gst["build_ms"], 2), "nodes": gst["num_nodes"],
+                        "max_depth": gst["max_depth"],
+                        "value": round(n / (np.mean(mg) * 1e-3) / 1e6, 1),
+                        "ms": round(float(np.mean(mg)), 4)}
+            del gscene
+        extra["gpu_build"] = {"builders": "vsr_bvh_build_gpu (LBVH, Karras 2012), "
+                                          "vsr_bvh_build_ploc (PLOC, radius 16)", **gb}
         extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
                               "default_ms": round(float(np.median(b_ms)), 4),
                               "overhead_pct": round(100 * (np.median(b_ms) / np.median(a_ms) - 1), 2)}

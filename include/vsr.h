@@ -184,6 +184,13 @@ vsr_status vsr_bvh_build(vsr_scene* scene, const vsr_build_params* params);
  * Errors: INVALID_ARG, EMPTY_SCENE, BVH_TOO_DEEP, UNSUPPORTED (host-only scene), CUDA, OOM. */
 vsr_status vsr_bvh_build_gpu(vsr_scene* scene, uint32_t max_leaf_size);
 
+/* The same GPU build with PLOC clustering (Meister & Bittner, TVCG 2018) instead of Karras
+ * splits: on the Morton-sorted triangles, every cluster pairs with its nearest neighbour
+ * (smallest union surface area, ties to the lower position) within +-radius (1..256; 16 is
+ * typical) and mutual pairs merge, round after round — trees close to binned SAH in quality at
+ * GPU build speed.  Same layout, rules and errors as vsr_bvh_build_gpu. */
+vsr_status vsr_bvh_build_ploc(vsr_scene* scene, uint32_t max_leaf_size, uint32_t radius);
+
 /* Enqueue one trace of n rays on `stream` (a cudaStream_t; NULL = legacy default).
  * d_rays / d_hits / d_counts are caller-owned DEVICE buffers on the scene's device,
  * 16-B aligned.  d_counts is required iff isect is COUNT or COUNT_ALPHA_TEXTURE.

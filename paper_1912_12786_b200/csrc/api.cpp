@@ -536,8 +536,10 @@ vsr_status vsr_bvh_build(vsr_scene* s, const vsr_build_params* params) {
   return VSR_OK;
 }
 
-vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
-  g_err.clear();
+}  // extern "C"
+
+namespace {
+vsr_status build_on_gpu(vsr_scene* s, uint32_t max_leaf_size, int ploc_radius) {
   if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
   if (s->vertices.empty() && s->num_tris_input == 0 && s->built)
     return fail(VSR_ERR_INVALID_ARG, "imported scenes cannot be rebuilt");
@@ -584,7 +586,7 @@ vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
   }
   GpuBvh gb;
   std::string err;
-  st = build_bvh_gpu(d_v, d_tc, d_tt, d_desc, n, max_leaf_size, gb, err);
+  st = build_bvh_gpu(d_v, d_tc, d_tt, d_desc, n, max_leaf_size, gb, err, ploc_radius);
   cleanup();
   if (st != VSR_OK) return fail(st, err);
   st = upload(s, gb.root_ref, gb.root_lo, gb.root_hi, gb.nodes, gb.num_nodes, gb.tris, gb.sides,
@@ -599,6 +601,20 @@ vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
   s->stats.build_ms =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return VSR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+vsr_status vsr_bvh_build_gpu(vsr_scene* s, uint32_t max_leaf_size) {
+  g_err.clear();
+  return build_on_gpu(s, max_leaf_size, 0);
+}
+
+vsr_status vsr_bvh_build_ploc(vsr_scene* s, uint32_t max_leaf_size, uint32_t radius) {
+  g_err.clear();
+  if (radius < 1 || radius > 256) return fail(VSR_ERR_INVALID_ARG, "radius must be in [1, 256]");
+  return build_on_gpu(s, max_leaf_size, (int)radius);
 }
 
 vsr_status vsr_trace_tiles(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint32_t tile_rays,

@@ -42,7 +42,8 @@ struct GpuBvh {
 };
 vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
                          const uint32_t* d_tri_tex, const TexDesc* d_tex, uint32_t n,
-                         uint32_t max_leaf, GpuBvh& out, std::string& err);
+                         uint32_t max_leaf, GpuBvh& out, std::string& err,
+                         int ploc_radius = 0);   // 0: LBVH (Karras); > 0: PLOC, +-radius
 
 // Top level of a two-level (instanced) hierarchy: the same binned SAH over
 // instance world boxes (6 floats per instance: lo xyz, hi xyz); `order`

@@ -294,6 +294,163 @@ __global__ void root_box_kernel(const Box6* __restrict__ prim_box, const uint32_
   pad_box(b, out, out + 3);
 }
 
+// ---------------------------------------------------------------------------
+// PLOC (Meister & Bittner, TVCG 2018): parallel locally-ordered clustering on
+// the Morton-sorted leaves.  Each round every cluster finds its nearest
+// neighbour (smallest union surface area, ties -> lower index) within +-r
+// positions, mutual pairs merge into a new node, and the cluster array is
+// compacted; binned-SAH-like trees at LBVH-like cost.  The finished tree is
+// re-expressed in the Karras arrays above (root = node 0, every node a
+// contiguous range of a depth-first leaf order) so the same collapse / write
+// kernels produce the export layout.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float half_area(const Box6& b) {
+  const float dx = b.hi[0] - b.lo[0], dy = b.hi[1] - b.lo[1], dz = b.hi[2] - b.lo[2];
+  return dx * dy + dy * dz + dz * dx;
+}
+
+__global__ void ploc_init_kernel(const Box6* __restrict__ prim_box, const uint32_t* __restrict__ order,
+                                 int m, int* __restrict__ cl_node, Box6* __restrict__ cl_box) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= m) return;
+  cl_node[k] = ~k;
+  cl_box[k] = prim_box[order[k]];
+}
+
+__global__ void ploc_nn_kernel(const Box6* __restrict__ cl_box, int c, int r, int* __restrict__ nn) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= c) return;
+  // Ties are broken by a key symmetric in (i, j) — nearer position, then pairs that start
+  // at an even position, then the lower pair — so runs of equal boxes pair up (2k, 2k+1)
+  // instead of chaining onto the lowest index.
+  const Box6 bi = cl_box[i];
+  float best = INFINITY;
+  int bj = -1;
+  uint64_t bkey = ~0ull;
+  const int lo = max(0, i - r), hi = min(c - 1, i + r);
+  for (int j = lo; j <= hi; ++j) {
+    if (j == i) continue;
+    const float a = half_area(unite(bi, cl_box[j]));
+    const int lo_ij = min(i, j);
+    const uint64_t key = ((uint64_t)abs(i - j) << 33) | ((uint64_t)(lo_ij & 1) << 32) |
+                         (uint64_t)(uint32_t)lo_ij;
+    if (a < best || (a == best && key < bkey)) {
+      best = a;
+      bj = j;
+      bkey = key;
+    }
+  }
+  nn[i] = bj;
+}
+
+__global__ void ploc_flags_kernel(const int* __restrict__ nn, int c, uint32_t* __restrict__ fnew,
+                                  uint32_t* __restrict__ fkeep) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= c) return;
+  const int j = nn[i];
+  const bool mutual = j >= 0 && nn[j] == i;
+  fnew[i] = mutual && i < j;
+  fkeep[i] = !(mutual && i > j);
+}
+
+__global__ void ploc_force_kernel(int* nn) {   // no mutual pair this round: merge clusters 0 and 1
+  nn[0] = 1;
+  nn[1] = 0;
+}
+
+__global__ void ploc_apply_kernel(const int* __restrict__ nn, int c, const uint32_t* __restrict__ fnew,
+                                  const uint32_t* __restrict__ snew, const uint32_t* __restrict__ fkeep,
+                                  const uint32_t* __restrict__ skeep, const int* __restrict__ cl_node,
+                                  const Box6* __restrict__ cl_box, int node_base,
+                                  int* __restrict__ out_node, Box6* __restrict__ out_box,
+                                  int2* __restrict__ nchild, Box6* __restrict__ nbox) {
+  const int i = blockIdx.x * kT + threadIdx.x;
+  if (i >= c || !fkeep[i]) return;
+  const uint32_t pos = skeep[i];
+  if (fnew[i]) {
+    const int j = nn[i];
+    const int id = node_base + (int)snew[i];
+    const Box6 b = unite(cl_box[i], cl_box[j]);
+    nchild[id] = make_int2(cl_node[i], cl_node[j]);
+    nbox[id] = b;
+    out_node[pos] = id;
+    out_box[pos] = b;
+  } else {
+    out_node[pos] = cl_node[i];
+    out_box[pos] = cl_box[i];
+  }
+}
+
+__global__ void ploc_parents_kernel(const int2* __restrict__ nchild, int nint, int* __restrict__ parent_int,
+                                    int* __restrict__ parent_leaf) {
+  const int n = blockIdx.x * kT + threadIdx.x;
+  if (n >= nint) return;
+  const int2 c = nchild[n];
+  if (c.x >= 0) parent_int[c.x] = n; else parent_leaf[~c.x] = n;
+  if (c.y >= 0) parent_int[c.y] = n; else parent_leaf[~c.y] = n;
+}
+
+// leaves per subtree, bottom-up (the second child to arrive sums)
+__global__ void ploc_sizes_kernel(int m, const int2* __restrict__ nchild, const int* __restrict__ parent_int,
+                                  const int* __restrict__ parent_leaf, int* size, int* __restrict__ arrivals) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k >= m) return;
+  int p = parent_leaf[k];
+  const volatile int* vs = size;
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(arrivals + p, 1) == 0) return;
+    __threadfence();
+    const int2 c = nchild[p];
+    size[p] = (c.x < 0 ? 1 : vs[c.x]) + (c.y < 0 ? 1 : vs[c.y]);
+    p = parent_int[p];
+  }
+}
+
+// first leaf position of subtree x (node id, or ~leaf) in the depth-first leaf order
+__device__ __forceinline__ int dfs_start(int x, const int* parent_int, const int* parent_leaf,
+                                         const int2* nchild, const int* size) {
+  int s = 0;
+  int cur = x;
+  int p = x >= 0 ? parent_int[x] : parent_leaf[~x];
+  while (p >= 0) {
+    const int2 c = nchild[p];
+    if (c.y == cur) s += c.x < 0 ? 1 : size[c.x];
+    cur = p;
+    p = parent_int[p];
+  }
+  return s;
+}
+
+__global__ void ploc_layout_kernel(int m, const uint32_t* __restrict__ order, const int* __restrict__ parent_int,
+                                   const int* __restrict__ parent_leaf, const int2* __restrict__ nchild,
+                                   const int* __restrict__ size, int* __restrict__ pos,
+                                   uint32_t* __restrict__ order2, int* __restrict__ start) {
+  const int k = blockIdx.x * kT + threadIdx.x;
+  if (k < m) {
+    const int q = dfs_start(~k, parent_int, parent_leaf, nchild, size);
+    pos[k] = q;
+    order2[q] = order[k];
+  }
+  if (k < m - 1) start[k] = dfs_start(k, parent_int, parent_leaf, nchild, size);
+}
+
+// node n (creation order, root = m - 2) -> Karras arrays with root 0
+__global__ void ploc_export_kernel(int m, const int2* __restrict__ nchild, const Box6* __restrict__ nbox,
+                                   const int* __restrict__ size, const int* __restrict__ start,
+                                   const int* __restrict__ parent_int, const int* __restrict__ pos,
+                                   int2* __restrict__ range, int2* __restrict__ child,
+                                   int* __restrict__ parent_node, Box6* __restrict__ node_box) {
+  const int n = blockIdx.x * kT + threadIdx.x;
+  if (n >= m - 1) return;
+  const int root = m - 2, nid = root - n;
+  range[nid] = make_int2(start[n], start[n] + size[n] - 1);
+  const int2 c = nchild[n];
+  child[nid] = make_int2(c.x >= 0 ? root - c.x : ~pos[~c.x], c.y >= 0 ? root - c.y : ~pos[~c.y]);
+  parent_node[nid] = parent_int[n] >= 0 ? root - parent_int[n] : -1;
+  node_box[nid] = nbox[n];
+}
+
 template <class T>
 cudaError_t alloc(T** p, size_t count) {
   return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
@@ -303,7 +460,7 @@ cudaError_t alloc(T** p, size_t count) {
 
 vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
                          const uint32_t* d_tri_tex, const TexDesc* d_tex, uint32_t n,
-                         uint32_t max_leaf, GpuBvh& out, std::string& err) {
+                         uint32_t max_leaf, GpuBvh& out, std::string& err, int ploc_radius) {
   cudaStream_t st = nullptr;
   Box6* box = nullptr;
   float* cen = nullptr;
@@ -317,6 +474,12 @@ vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
   Box6* node_box = nullptr;
   float* root = nullptr;
   void* tmp = nullptr;
+  // PLOC scratch
+  int *cl_node[2] = {nullptr, nullptr}, *nn = nullptr, *pint = nullptr, *psize = nullptr;
+  int *ppos = nullptr, *pstart = nullptr, *parr = nullptr;
+  Box6 *cl_box[2] = {nullptr, nullptr}, *nbox = nullptr;
+  int2* nchild = nullptr;
+  uint32_t *fnew = nullptr, *fkeep = nullptr, *snew = nullptr, *skeep = nullptr, *order2 = nullptr;
   out = GpuBvh{};
   cudaError_t e = cudaSuccess;
   auto fin = [&](vsr_status s, const std::string& msg) {
@@ -324,6 +487,10 @@ vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
     cudaFree(keys); cudaFree(keys2); cudaFree(vals); cudaFree(vals2); cudaFree(live);
     cudaFree(newidx); cudaFree(range); cudaFree(child); cudaFree(parent_node);
     cudaFree(parent_leaf); cudaFree(arrivals); cudaFree(node_box); cudaFree(root); cudaFree(tmp);
+    cudaFree(cl_node[0]); cudaFree(cl_node[1]); cudaFree(nn); cudaFree(pint); cudaFree(psize);
+    cudaFree(ppos); cudaFree(pstart); cudaFree(parr); cudaFree(cl_box[0]); cudaFree(cl_box[1]);
+    cudaFree(nbox); cudaFree(nchild); cudaFree(fnew); cudaFree(fkeep); cudaFree(snew);
+    cudaFree(skeep); cudaFree(order2);
     if (s != VSR_OK) {
       cudaFree(out.nodes); cudaFree(out.tris); cudaFree(out.sides);
       out = GpuBvh{};
@@ -378,11 +545,80 @@ vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
     VSR_TRY(alloc(&newidx, m - 1));
     VSR_TRY(cudaMemsetAsync(arrivals, 0, sizeof(int) * (m - 1), st));
     VSR_TRY(cudaMemsetAsync(parent_node, 0xFF, sizeof(int) * (m - 1), st));
-    karras_kernel<<<gi, kT, 0, st>>>(keys2, m, range, child, parent_node, parent_leaf);
-    VSR_TRY(cudaGetLastError());
-    boxes_kernel<<<gl, kT, 0, st>>>(box, order, m, child, parent_node, parent_leaf, node_box,
-                                    arrivals);
-    VSR_TRY(cudaGetLastError());
+    if (ploc_radius <= 0) {   // LBVH: Karras splits on the Morton codes
+      karras_kernel<<<gi, kT, 0, st>>>(keys2, m, range, child, parent_node, parent_leaf);
+      VSR_TRY(cudaGetLastError());
+      boxes_kernel<<<gl, kT, 0, st>>>(box, order, m, child, parent_node, parent_leaf, node_box,
+                                      arrivals);
+      VSR_TRY(cudaGetLastError());
+    } else {                  // PLOC clustering, then the same arrays
+      VSR_TRY(alloc(&cl_node[0], m));
+      VSR_TRY(alloc(&cl_node[1], m));
+      VSR_TRY(alloc(&cl_box[0], m));
+      VSR_TRY(alloc(&cl_box[1], m));
+      VSR_TRY(alloc(&nn, m));
+      VSR_TRY(alloc(&fnew, m));
+      VSR_TRY(alloc(&fkeep, m));
+      VSR_TRY(alloc(&snew, m));
+      VSR_TRY(alloc(&skeep, m));
+      VSR_TRY(alloc(&nchild, m - 1));
+      VSR_TRY(alloc(&nbox, m - 1));
+      size_t sb = 0;
+      VSR_TRY(cub::DeviceScan::ExclusiveSum(nullptr, sb, fnew, snew, m, st));
+      if (sb > scan_bytes && sb > tmp_bytes) {
+        cudaFree(tmp);
+        tmp = nullptr;
+        VSR_TRY(cudaMalloc(&tmp, sb));
+        tmp_bytes = sb;
+      }
+      const size_t tb = tmp_bytes > scan_bytes ? tmp_bytes : scan_bytes;
+      ploc_init_kernel<<<gl, kT, 0, st>>>(box, order, m, cl_node[0], cl_box[0]);
+      VSR_TRY(cudaGetLastError());
+      int c = m, node_base = 0, cur = 0;
+      while (c > 1) {
+        const unsigned gc = (unsigned)((c + kT - 1) / kT);
+        ploc_nn_kernel<<<gc, kT, 0, st>>>(cl_box[cur], c, ploc_radius, nn);
+        ploc_flags_kernel<<<gc, kT, 0, st>>>(nn, c, fnew, fkeep);
+        VSR_TRY(cudaGetLastError());
+        size_t b1 = tb, b2 = tb;
+        VSR_TRY(cub::DeviceScan::ExclusiveSum(tmp, b1, fnew, snew, c, st));
+        uint32_t tail[2];
+        VSR_TRY(cudaMemcpy(&tail[0], snew + (c - 1), 4, cudaMemcpyDeviceToHost));
+        VSR_TRY(cudaMemcpy(&tail[1], fnew + (c - 1), 4, cudaMemcpyDeviceToHost));
+        int made = (int)(tail[0] + tail[1]);
+        if (made == 0) {   // cannot happen with a strict order on (area, index); stay safe
+          ploc_force_kernel<<<1, 1, 0, st>>>(nn);
+          ploc_flags_kernel<<<gc, kT, 0, st>>>(nn, c, fnew, fkeep);
+          VSR_TRY(cudaGetLastError());
+          VSR_TRY(cub::DeviceScan::ExclusiveSum(tmp, b1, fnew, snew, c, st));
+          made = 1;
+        }
+        VSR_TRY(cub::DeviceScan::ExclusiveSum(tmp, b2, fkeep, skeep, c, st));
+        ploc_apply_kernel<<<gc, kT, 0, st>>>(nn, c, fnew, snew, fkeep, skeep, cl_node[cur],
+                                             cl_box[cur], node_base, cl_node[cur ^ 1],
+                                             cl_box[cur ^ 1], nchild, nbox);
+        VSR_TRY(cudaGetLastError());
+        node_base += made;
+        c -= made;
+        cur ^= 1;
+      }
+      VSR_TRY(alloc(&pint, m - 1));
+      VSR_TRY(alloc(&psize, m - 1));
+      VSR_TRY(alloc(&ppos, m));
+      VSR_TRY(alloc(&pstart, m - 1));
+      VSR_TRY(alloc(&parr, m - 1));
+      VSR_TRY(alloc(&order2, m));
+      VSR_TRY(cudaMemsetAsync(pint, 0xFF, sizeof(int) * (m - 1), st));
+      VSR_TRY(cudaMemsetAsync(parr, 0, sizeof(int) * (m - 1), st));
+      ploc_parents_kernel<<<gi, kT, 0, st>>>(nchild, m - 1, pint, parent_leaf);
+      ploc_sizes_kernel<<<gl, kT, 0, st>>>(m, nchild, pint, parent_leaf, psize, parr);
+      ploc_layout_kernel<<<gl, kT, 0, st>>>(m, order, pint, parent_leaf, nchild, psize, ppos, order2,
+                                            pstart);
+      ploc_export_kernel<<<gi, kT, 0, st>>>(m, nchild, nbox, psize, pstart, pint, ppos, range, child,
+                                            parent_node, node_box);
+      VSR_TRY(cudaGetLastError());
+      order = order2;
+    }
     live_kernel<<<gi, kT, 0, st>>>(range, m, max_leaf, live);
     VSR_TRY(cudaGetLastError());
     VSR_TRY(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, live, newidx, m - 1, st));

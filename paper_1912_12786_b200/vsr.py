@@ -54,7 +54,7 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
                     "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
                     "vsr_trace_pinhole", "vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free",
-                    "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close"]
+                    "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close", "vsr_bvh_build_ploc"]
 
 
 class VsrError(RuntimeError):
@@ -170,6 +170,8 @@ def lib():
                      "vsr_ipc_open", "vsr_ipc_close"):
             getattr(L, name).restype = C.c_int
         L.vsr_bvh_build_gpu.restype = C.c_int
+        L.vsr_bvh_build_ploc.argtypes = [P, C.c_uint32, C.c_uint32]
+        L.vsr_bvh_build_ploc.restype = C.c_int
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                      P, P, P]
@@ -298,6 +300,11 @@ class Scene:
     def build_gpu(self, max_leaf_size=2):
         """vsr_bvh_build_gpu: linear BVH built on the scene's GPU (NEXT-3)."""
         _check(lib().vsr_bvh_build_gpu(self._h, max_leaf_size))
+        return self
+
+    def build_ploc(self, max_leaf_size=2, radius=16):
+        """vsr_bvh_build_ploc: GPU build by PLOC clustering (NEXT-3)."""
+        _check(lib().vsr_bvh_build_ploc(self._h, max_leaf_size, radius))
         return self
 
     def stats(self) -> dict:

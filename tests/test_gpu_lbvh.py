@@ -1,6 +1,7 @@
-"""GPU linear-BVH builder (vsr_bvh_build_gpu): the exported tree is
-structurally valid (tests/bvh_check.py), walker C on it equals the brute force, and the GPU
-trace on it is bit-exact vs walker C (hits and counts) and equals the SAH tree's results."""
+"""GPU BVH builders: linear BVH (vsr_bvh_build_gpu) and PLOC clustering
+(vsr_bvh_build_ploc).  The exported tree is structurally valid (tests/bvh_check.py), walker C on
+it equals the brute force, and the GPU trace on it is bit-exact vs walker C (hits and counts) and
+equals the SAH tree's results."""
 import numpy as np
 import pytest
 
@@ -29,12 +30,18 @@ def trace(V, scene, rays, q, k):
     return V.hits_to_numpy(h), (V.counts_to_numpy(c) if c is not None else None)
 
 
+def build(V, sc, how, max_leaf):
+    s = V.Scene.from_workload(sc)
+    return s.build_gpu(max_leaf) if how == "lbvh" else s.build_ploc(max_leaf, 8 if how == "ploc8" else 16)
+
+
+@pytest.mark.parametrize("how", ["lbvh", "ploc", "ploc8"])
 @pytest.mark.parametrize("max_leaf", [1, 2, 4, 32])
-def test_lbvh_valid_and_exact(V, oracle_lib, max_leaf):
+def test_lbvh_valid_and_exact(V, oracle_lib, max_leaf, how):
     o = oracle_lib
     sc = W.random_soup(5000, seed=70 + max_leaf, size=1.5)
     rays = W.random_rays(5001, seed=71).data
-    g = V.Scene.from_workload(sc).build_gpu(max_leaf)
+    g = build(V, sc, how, max_leaf)
     e = g.export()
     depth = bvh_check.validate(e, sc.vertices, max_leaf)
     st = g.stats()
@@ -56,10 +63,11 @@ def test_lbvh_valid_and_exact(V, oracle_lib, max_leaf):
     assert np.array_equal(h[ok], ref[ok])
 
 
-def test_lbvh_equals_sah_on_forest(V):
+@pytest.mark.parametrize("how", ["lbvh", "ploc"])
+def test_lbvh_equals_sah_on_forest(V, how):
     sc, rays = W.config("C2", 480, 272)
     a = V.Scene.from_workload(sc).build()
-    g = V.Scene.from_workload(sc).build_gpu(2)
+    g = build(V, sc, how, 2)
     bvh_check.validate(g.export(), sc.vertices, 2)
     for q in (V.CLOSEST, V.ANY):
         ha, _ = trace(V, a, rays.data, q, V.ALPHA_TEXTURE)
@@ -69,23 +77,27 @@ def test_lbvh_equals_sah_on_forest(V):
             assert np.array_equal(ha["t"], hg["t"])
 
 
-def test_lbvh_edge_cases(V, oracle_lib):
+@pytest.mark.parametrize("how", ["lbvh", "ploc"])
+def test_lbvh_edge_cases(V, oracle_lib, how):
     o = oracle_lib
     # one triangle; all-coincident centroids (equal Morton codes); degenerate triangles
     one = W.stacked_quads(1)
     one.vertices, one.geom_ids, one.texcoords = one.vertices[:1], one.geom_ids[:1], one.texcoords[:1]
-    s1 = V.Scene.from_workload(one).build_gpu(2)
+    s1 = build(V, one, how, 2)
     e1 = s1.export()
     assert e1["nodes"].shape[0] == 0 and e1["root_ref"] & 0x80000000
+    two = W.stacked_quads(1)     # two triangles, max_leaf 1: one inner node
+    s1b = build(V, two, how, 1)
+    bvh_check.validate(s1b.export(), two.vertices, 1)
     same = W.stacked_quads(64, z0=1.0, dz=0.0)     # 128 triangles, pairwise-equal centroids
-    s2 = V.Scene.from_workload(same).build_gpu(1)
+    s2 = build(V, same, how, 1)
     bvh_check.validate(s2.export(), same.vertices, 1)
     assert s2.stats()["max_depth"] <= 64
     sc = W.random_soup(300, seed=72)
     v = sc.vertices.copy()
     v[5, 3:6] = v[5, 0:3]
     v[9, 6:9] = v[9, 0:3]
-    d = V.Scene(v, sc.geom_ids, sc.texcoords, sc.geom_texture, sc.textures).build_gpu(2)
+    d = build(V, W.Scene("d", v, sc.geom_ids, sc.texcoords, sc.geom_texture, sc.textures), how, 2)
     st = d.stats()
     assert st["num_degenerate"] == 2 and st["num_tris"] == 298
     prims = set(d.export()["tris"][:, 3].tolist())
@@ -97,5 +109,7 @@ def test_lbvh_edge_cases(V, oracle_lib):
     assert np.array_equal(h["t"], ref["t"])
     with pytest.raises(V.VsrError):
         V.Scene.from_workload(sc).build_gpu(0)
+    with pytest.raises(V.VsrError):
+        V.Scene.from_workload(sc).build_ploc(2, 0)
     with pytest.raises(V.VsrError):
         V.Scene.from_workload(sc, device=-1).build_gpu(2)
