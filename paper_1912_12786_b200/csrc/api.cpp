@@ -72,6 +72,30 @@ cudaError_t to_host(void* dst, const void* src, size_t bytes) {
 
 }  // namespace
 
+// Per-stream scratch of the longest-first order pass, owned by whatever is
+// traced (scene, group, instances): reused in stream order behind an event, so
+// launches on other streams never share it and steady-state launches allocate
+// nothing.
+struct ScratchSet {
+  struct OrderScratch {
+    cudaStream_t st;
+    void* ptr;
+    size_t cap;
+    cudaEvent_t ev;   // last use; the next use waits on it (stream-ordered reuse)
+  };
+  std::mutex mu;
+  std::vector<OrderScratch> v;
+
+  void release() {
+    for (OrderScratch& o : v) {
+      cudaEventSynchronize(o.ev);
+      cudaFree(o.ptr);
+      cudaEventDestroy(o.ev);
+    }
+    v.clear();
+  }
+};
+
 struct vsr_scene {
   int device = 0;
   // ---- host copies (vsr_scene_create) ----
@@ -109,24 +133,7 @@ struct vsr_scene {
   cudaEvent_t ev_done[kSlots] = {};
   void* fn_cache[4] = {};
   bool fn_cached[4] = {};
-  // ---- per-stream scratch of the longest-first order pass ----
-  struct OrderScratch {
-    cudaStream_t st;
-    void* ptr;
-    size_t cap;
-    cudaEvent_t ev;   // last use; the next use waits on it (stream-ordered reuse)
-  };
-  std::mutex order_mu;
-  std::vector<OrderScratch> order_scratch;
-
-  void free_order_scratch() {
-    for (OrderScratch& o : order_scratch) {
-      cudaEventSynchronize(o.ev);
-      cudaFree(o.ptr);
-      cudaEventDestroy(o.ev);
-    }
-    order_scratch.clear();
-  }
+  ScratchSet scratch;   // per-stream scratch of the longest-first order pass
 
   void free_device() {
     cudaFree(d_nodes);
@@ -303,22 +310,22 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   return VSR_OK;
 }
 
-// Launch with the scene's scratch for stream `st` (created or grown on first
+// Launch with the owner's scratch for stream `st` (created or grown on first
 // use; the launch waits for the scratch's previous use, then records its own).
 // Caller holds no lock; n must be the launch's ray count.
-cudaError_t launch_with_scratch(vsr_scene* s, int query, int isect, TraceParams& p,
+cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TraceParams& p,
                                 cudaStream_t st) {
-  std::lock_guard<std::mutex> lk(s->order_mu);
+  std::lock_guard<std::mutex> lk(set.mu);
   const size_t bytes = order_scratch_bytes(p.n);
-  vsr_scene::OrderScratch* o = nullptr;
-  for (auto& e : s->order_scratch)
+  ScratchSet::OrderScratch* o = nullptr;
+  for (auto& e : set.v)
     if (e.st == st) o = &e;
   cudaError_t e = cudaSuccess;
-  if (!o && s->order_scratch.size() < 16) {
-    vsr_scene::OrderScratch n{st, nullptr, 0, nullptr};
+  if (!o && set.v.size() < 16) {
+    ScratchSet::OrderScratch n{st, nullptr, 0, nullptr};
     if ((e = cudaEventCreateWithFlags(&n.ev, cudaEventDisableTiming)) != cudaSuccess) return e;
-    s->order_scratch.push_back(n);
-    o = &s->order_scratch.back();
+    set.v.push_back(n);
+    o = &set.v.back();
   }
   p.order_scratch = nullptr;
   p.order_scratch_bytes = 0;
@@ -651,7 +658,7 @@ vsr_status vsr_trace_tiles(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   p.sched = kSchedDirect;
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "tile trace launch");
   return VSR_OK;
 }
@@ -766,7 +773,7 @@ vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query que
   p.n = n;
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "pinhole trace launch");
   return VSR_OK;
 }
@@ -796,7 +803,7 @@ vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query 
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   p.counter = next_counter(s);
-  cudaError_t e = launch_with_scratch(s, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "trace kernel launch");
   return VSR_OK;
 }
@@ -833,7 +840,7 @@ vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
   p.counter = next_counter(s);
-  cudaError_t e = launch_with_scratch(s, 2 /* multi */, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(s->scratch, 2 /* multi */, isect, p, reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "multi-hit trace launch");
   return VSR_OK;
 }
@@ -842,6 +849,7 @@ vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
 
 struct vsr_group {
   int device = 0;
+  ScratchSet scratch;
   std::vector<vsr_scene*> scenes;
   DevScene* d_list = nullptr;
   IsectData* d_data = nullptr;
@@ -902,6 +910,7 @@ vsr_status vsr_group_destroy(vsr_group* g) {
   if (!g) return VSR_OK;
   {
     DeviceGuard dg(g->device);
+    g->scratch.release();
     cudaFree(g->d_list);
     cudaFree(g->d_data);
   }
@@ -943,7 +952,8 @@ vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_
   p.which = d_which;
   DeviceGuard dg(g->device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-  cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(g->scratch, query, isect, p,
+                                      reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "list trace launch");
   return VSR_OK;
 }
@@ -954,6 +964,7 @@ vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_
 // referenced, not owned.
 struct vsr_instances {
   int device = 0;
+  ScratchSet scratch;
   std::vector<vsr_scene*> scenes;
   HostBvh top;                       // host copy of the top-level nodes (export)
   std::vector<Instance> records;     // leaf order (export)
@@ -1017,6 +1028,7 @@ bool instance_world_box(const float* m, const float* lo, const float* hi, float*
 void free_instances(vsr_instances* I) {
   if (I->device < 0) return;
   DeviceGuard dg(I->device);
+  I->scratch.release();
   cudaFree(I->d_nodes);
   cudaFree(I->d_records);
   cudaFree(I->d_list);
@@ -1183,7 +1195,8 @@ vsr_status vsr_trace_instances(vsr_instances* I, const vsr_ray* d_rays, uint64_t
   p.which = d_inst;
   DeviceGuard dg(I->device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-  cudaError_t e = launch_trace(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = launch_with_scratch(I->scratch, query, isect, p,
+                                      reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "instanced trace launch");
   return VSR_OK;
 }
@@ -1250,7 +1263,7 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
     p.counts = s->d_cnt[k];
     p.n = m;
     p.counter = next_counter(s);
-    if ((e = launch_with_scratch(s, query, isect, p, ss)) != cudaSuccess)
+    if ((e = launch_with_scratch(s->scratch, query, isect, p, ss)) != cudaSuccess)
       return cuda_fail(e, "trace launch");
     if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
         cudaSuccess)
@@ -1275,7 +1288,7 @@ vsr_status vsr_destroy(vsr_scene* s) {
   if (s->device >= 0) {
     DeviceGuard g(s->device);
     s->free_stage();
-    s->free_order_scratch();
+    s->scratch.release();
     s->free_device();
   }
   delete s;

@@ -735,16 +735,17 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 
 int sm_count() {
-  static int cache[64] = {0};
+  static std::atomic<int> cache[64];   // zero-initialised (static storage)
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64) dev = 0;
-  if (!cache[dev]) {
-    int n = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (!n) {
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    cache[dev] = n > 0 ? n : 148;
+    n = n > 0 ? n : 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
-  return cache[dev];
+  return n;
 }
 
 // <<<grid, block, 0, st>>>, as a programmatic dependent launch when `pdl`
@@ -768,13 +769,15 @@ template <int Q, class I>
 cudaError_t launch(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
   if (p.sched == kSchedPersistent) {
-    static int per_sm = 0;   // resident blocks per SM for this instantiation
+    static std::atomic<int> per_sm_cache{0};   // resident blocks per SM for this instantiation
+    int per_sm = per_sm_cache.load(std::memory_order_relaxed);
     if (per_sm == 0) {
       int nb = 0;
       cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
           &nb, trace_kernel_persistent<Q, I>, kBlock, 0);
       if (e != cudaSuccess) return e;
       per_sm = nb > 0 ? nb : 1;
+      per_sm_cache.store(per_sm, std::memory_order_relaxed);
     }
     const uint64_t full = (uint64_t)per_sm * sm_count();
     const unsigned blocks = (unsigned)(need < full ? need : full);
@@ -933,20 +936,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
   void* scratch = nullptr;
   bool owned = false;
   if (p.order && p.sched == kSchedDirect && nblocks >= 2ull * sm_count() && nblocks < (1u << 24)) {
-    // stream-ordered scratch: safe for concurrent launches on other streams.
-    // Keep freed blocks in the device's default pool (release threshold = max)
-    // so steady-state launches never map memory.
-    static bool pool_set[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64 && !pool_set[dev]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      pool_set[dev] = true;
-    }
+    // the owner's per-stream scratch (api.cpp ScratchSet); a stream-ordered
+    // allocation only past 16 streams per owner
     const size_t bytes = order_scratch_bytes(p.n);
     cudaError_t e = cudaSuccess;
     if (p.order_scratch && p.order_scratch_bytes >= bytes) {
