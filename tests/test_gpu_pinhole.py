@@ -51,3 +51,18 @@ def test_pinhole_validation(V):
     cam = V.pinhole_camera((0, 0, -5), (0, 0, 0), (0, 1, 0), 45.0, 64, 64)
     with pytest.raises(V.VsrError):
         scene.trace_pinhole(cam, V.CLOSEST, V.RUNTIME_SWITCH_DEFAULT)
+
+
+def test_c_program_traces_on_the_gpu(V, tmp_path):
+    """examples/c_trace_host.c: the whole path (create, build, vsr_trace_host with the alpha
+    intersector) driven from plain C."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.dirname(V.LIB_PATH)
+    exe = tmp_path / "vsr_ct"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "examples", "c_trace_host.c"), "-L", libdir, "-lvsr",
+                    f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stdout + out.stderr
