@@ -68,3 +68,14 @@ def test_intersector_code_only_where_used(sass, q):
     assert not any(indirect.match(i) for i in default)
     assert not any(indirect.match(i) for i in alpha)
     assert any(indirect.match(i) for i in fnptr)
+
+
+def test_no_packed_fma_contraction(sass):
+    """The arithmetic contract forbids FMA contraction.  ptxas fuses a packed
+    f32x2 multiply feeding a packed add into FFMA2 even under --fmad=false, so the kernels only
+    use packed products whose consumers are not packed adds (slab: sub then mul; MT: FMUL2 then
+    scalar sums).  Any FFMA2 in the library would break bit-exact parity."""
+    bad = [name for name, ins in sass.items() if any(i.split()[0].lstrip("@!P0123456789 ")
+                                                     .startswith("FFMA2") or " FFMA2 " in f" {i} "
+                                                     for i in ins)]
+    assert not bad, bad[:3]
