@@ -328,6 +328,7 @@ def run_own(args):
     achieved = bytes_launch / (ms_kernel * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": peak_src,
+                "frac_nominal_8TBs": round(achieved / 8000.0, 4),
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "bytes_per_ray": round(bytes_launch / n, 1), "work_per_ray": work,
                 "kernel": f"trace_kernel<{args.query}, {args.isect}>",
@@ -342,6 +343,9 @@ def run_own(args):
             if tr:
                 roofline["traffic"] = tr["dram_bytes_per_launch"]
                 roofline["traffic_source"] = tr.get("source")
+                # measured DRAM bytes (ncu, per launch) over the live kernel time
+                roofline["dram_frac"] = round(tr["dram_bytes_per_launch"] / (ms_kernel * 1e-3)
+                                              / 1e9 / peak, 4)
                 # issue roofline: ncu's warp-instruction count per launch over the live
                 # kernel time, against 148 SMs x 4 schedulers x 1 inst/clk at the sampled clock
                 mhz = sampler.summary().get("sm_mhz") or 1965.0
