@@ -517,7 +517,9 @@ def run_own(args):
                                        f"rays sharded by frame, {world} rank(s), no data-path collective"),
                        "setup_s": round(setup_s, 2)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "ms_per_step_each": [round(x, 4) for x in ms], **extra,
+            "clocks": clocks, "ms_per_step_each": [round(x, 4) for x in ms],
+            "ms_median": round(float(np.median(ms)), 4), "ms_min": round(float(np.min(ms)), 4),
+            **extra,
         }
         print(json.dumps(line))
     if peer is not None:
