@@ -63,13 +63,11 @@ __device__ __forceinline__ hit_record tri_hook(I& isect, const RayCtx& r, const 
 // Per-lane traversal state of one ray.
 struct Trav {
   RayCtx r;
-  float best_t;
-  bool have;
-  float t, u, v;
-  uint32_t prim;
+  float best_t;   // tmax of the moment; the kept hit's t once prim != kMissPrim
+  float u, v;
+  uint32_t prim;  // kMissPrim until a hit is kept (the "have" flag)
   uint32_t cur;
   int sp;
-  uint64_t id;
 };
 
 // Pop the next entry not farther than the current best (reading A14).
@@ -140,13 +138,10 @@ __device__ __forceinline__ bool start_ray(const TraceParams& p, Trav& T, I& isec
   fetch_ray<GEN>(p, id, a, b);
   make_ray(T.r, a, b);
   T.best_t = b.w;
-  T.have = false;
-  T.t = __int_as_float(0x7f800000);
   T.u = 0.0f;
   T.v = 0.0f;
   T.prim = kMissPrim;
   T.sp = 0;
-  T.id = id;
   T.cur = p.scene.root_ref;
   isect.reset();
   const Aabb root{p.scene.root_lo[0], p.scene.root_lo[1], p.scene.root_lo[2],
@@ -242,17 +237,15 @@ __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb
       }
     } else if (Q == kAny) {
       if (hr.hit) {   // any-hit: the first accepted hit ends the query
-        T.t = hr.t;
+        T.best_t = hr.t;
         T.u = hr.u;
         T.v = hr.v;
         T.prim = __float_as_uint(td.a.w);
         return true;
       }
-    } else if (hr.hit && (!T.have || hr.t < T.best_t)) {
+    } else if (hr.hit && (T.prim == kMissPrim || hr.t < T.best_t)) {
       // closest-hit: accepted hits shrink tmax; vetoed ones do not
       T.best_t = hr.t;
-      T.have = true;
-      T.t = hr.t;
       T.u = hr.u;
       T.v = hr.v;
       T.prim = __float_as_uint(td.a.w);
@@ -307,15 +300,17 @@ __device__ __forceinline__ int warp_octant(const RayCtx& r) {
 }
 
 template <class I>
-__device__ __forceinline__ void finish(const TraceParams& p, const Trav& T, const I& isect) {
-  uint64_t o = T.id;
+__device__ __forceinline__ void finish(const TraceParams& p, const Trav& T, const I& isect,
+                                       uint64_t id) {
+  uint64_t o = id;
   if (p.out_world) {   // vsr_trace_tiles: local tile j is frame tile j*world + rank
-    const uint32_t local = (uint32_t)T.id, tile = local / p.out_tile;
+    const uint32_t local = (uint32_t)id, tile = local / p.out_tile;
     o = ((uint64_t)tile * p.out_world + p.out_rank) * p.out_tile + (local - tile * p.out_tile);
   }
   // hits may live in a peer GPU's frame buffer (CUDA IPC over NVLink): plain stores,
   // complete when this kernel is
-  p.hits[o] = make_float4(T.t, T.u, T.v, __uint_as_float(T.prim));
+  const float t = T.prim != kMissPrim ? T.best_t : __int_as_float(0x7f800000);
+  p.hits[o] = make_float4(t, T.u, T.v, __uint_as_float(T.prim));
   if constexpr (I::kCounts) {
     p.counts[o] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
   }
@@ -481,7 +476,10 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
     const int woct = __match_any_sync(live, oct) == live ? oct : 8;
     NoMulti none;
     if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
-    finish(p, T, isect);
+    // the ray index is recomputed (perm re-read through L2) rather than kept live
+    // across the traversal: one register less in the hot loop
+    const uint64_t blk2 = p.perm ? (uint64_t)__ldcg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
+    finish(p, T, isect, blk2 * kBlock + threadIdx.x);
   }
 #ifdef VSR_TIMELINE
   // diagnostic build only: per-warp (SM id, start ns, end ns) into counts[warp]
@@ -570,15 +568,15 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const Trac
     const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
     float tn;
     if (!box_hook(isect, T.r, root, T.best_t, tn)) continue;
-    const float t_before = T.t;
+    const float t_before = T.best_t;
     const uint32_t prim_before = T.prim;
     T.cur = S.root_ref;
     T.sp = 0;
     traverse<Q>(S, T, isect, stack, woct, none);
-    if (T.t != t_before || T.prim != prim_before) hit_in = s;
+    if (T.best_t != t_before || T.prim != prim_before) hit_in = s;
     if (Q == kAny && T.prim != kMissPrim) break;   // any-hit: the first accepted hit ends it
   }
-  finish(p, T, isect);
+  finish(p, T, isect, id);
   if (which) which[id] = hit_in;
 }
 
@@ -624,11 +622,10 @@ __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& 
   if (!box_hook(isect, B.r, root, B.best_t, tn)) return false;
   NoMulti none;
   traverse<Q>(S, B, isect, stack, warp_octant(B.r), none);
-  const bool better = Q == kAny ? B.prim != kMissPrim : ((B.have && !T.have) || B.best_t < T.best_t);
+  const bool better = Q == kAny ? B.prim != kMissPrim
+                                : (B.prim != kMissPrim && (T.prim == kMissPrim || B.best_t < T.best_t));
   if (better) {
     T.best_t = B.best_t;
-    T.have = B.have;
-    T.t = B.t;
     T.u = B.u;
     T.v = B.v;
     T.prim = B.prim;
@@ -658,7 +655,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_kernel(const
       if (done || !pop(T, stack)) break;
     }
   }
-  finish(p, T, isect);
+  finish(p, T, isect, id);
   if (p.which) p.which[id] = hit_in;
 }
 
@@ -679,6 +676,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(cons
   // warp-uniform work queue: [next, next + left) of the warp's claimed chunk
   unsigned long long next = 0;
   unsigned left = 0;
+  uint64_t my_id = 0;
   bool drained = false;      // the global counter ran past n
   for (;;) {
     // converged refill point: ballot/popc compaction of the idle lanes
@@ -696,8 +694,9 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(cons
       if (!active) {
         const unsigned rank = __popc(idle & below);
         if (rank < take) {
-          active = start_ray(p, T, isect, next + rank);
-          if (!active) finish(p, T, isect);   // missed the root box: a miss record
+          my_id = next + rank;
+          active = start_ray(p, T, isect, my_id);
+          if (!active) finish(p, T, isect, my_id);   // missed the root box: a miss record
         }
       }
       next += take;
@@ -706,7 +705,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(cons
       break;
     }
     if (active && advance<Q, -1>(p.scene, T, isect, stack)) {
-      finish(p, T, isect);
+      finish(p, T, isect, my_id);
       active = false;
     }
   }
