@@ -328,6 +328,25 @@ vsr_status vsr_ipc_handle(const void* d_ptr, void* handle64);
 vsr_status vsr_ipc_open(const void* handle64, int device, void** d_ptr);
 vsr_status vsr_ipc_close(void* d_ptr, int device);
 
+/* Multi-hit query over a list of BVHs / over instances (closest_hit, any_hit
+ * and multi_hit iterate over lists whose elements may be BVHs): one buffer of the max_hits
+ * (1..16) smallest-t accepted hits across all elements, in ascending t (equal t: the order
+ * traversal found them), with the group's single running best_t (the worst kept t once full).
+ * d_hits: n*max_hits ray-major as vsr_trace_multi; d_num_hits (optional): n; d_which / d_inst
+ * (optional): n*max_hits, the list index / caller's instance index of each kept hit
+ * (0xFFFFFFFF in unused slots).  Counting as vsr_trace_group / vsr_trace_instances.
+ * RUNTIME_* controls: VSR_ERR_UNSUPPORTED. */
+vsr_status vsr_trace_group_multi(vsr_group* group, const vsr_ray* d_rays, uint64_t n,
+                                 uint32_t max_hits, vsr_isect isect,
+                                 const vsr_isect_params* params, vsr_hit* d_hits,
+                                 uint32_t* d_num_hits, uint32_t* d_which, vsr_counts* d_counts,
+                                 void* stream);
+vsr_status vsr_trace_instances_multi(vsr_instances* inst, const vsr_ray* d_rays, uint64_t n,
+                                     uint32_t max_hits, vsr_isect isect,
+                                     const vsr_isect_params* params, vsr_hit* d_hits,
+                                     uint32_t* d_num_hits, uint32_t* d_inst,
+                                     vsr_counts* d_counts, void* stream);
+
 /* End-to-end variant over HOST buffers (pinned memory recommended): copies rays in,
  * traces, copies hits (and counts) out, all on `stream`, in chunks so that copies
  * overlap the kernel; returns after the stream work completed. */

@@ -110,6 +110,15 @@ def lib():
                                              C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
                                              C.c_int]
         L.oracle_ray_to_object.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.walker_trace_list_multi.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64,
+                                              C.c_uint32, C.c_int, C.c_float, C.c_uint32,
+                                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                              C.c_int]
+        L.walker_trace_instances_multi.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_void_p,
+                                                   C.c_uint32, C.c_void_p, C.c_uint64, C.c_int,
+                                                   C.c_uint32, C.c_int, C.c_float, C.c_uint32,
+                                                   C.c_void_p, C.c_void_p, C.c_void_p,
+                                                   C.c_void_p, C.c_int]
         _lib = L
     return _lib
 
@@ -435,4 +444,46 @@ def walk_instances(top, records, bottoms, rays, query=CLOSEST, isect=DEFAULT, al
     if rc != 0:
         raise ValueError(f"walker_trace_instances failed ({rc})")
     return hits, inst, counts
+
+
+def walk_list_multi(bvhs, rays, k, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8,
+                    nthreads=None):
+    """Walker C, multi-hit over a LIST of BVHs: (hits [n, k], nhits, which [n, k], counts)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    hits = np.empty((n, k), dtype=HIT_DTYPE)
+    nh = np.zeros(n, dtype=np.uint32)
+    which = np.empty((n, k), dtype=np.uint32)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    arr = (_Bvh * len(bvhs))(*[b.c_struct() for b in bvhs])
+    rc = lib().walker_trace_list_multi(arr, len(bvhs), _ptr(r), n, k, isect, alpha_threshold,
+                                       checker_freq, _ptr(hits), _ptr(nh), _ptr(which),
+                                       _ptr(counts), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_list_multi failed ({rc})")
+    return hits, nh, which, counts
+
+
+def walk_instances_multi(top, records, bottoms, rays, k, isect=DEFAULT, alpha_threshold=0.01,
+                         checker_freq=8, nthreads=None):
+    """Walker C, multi-hit over instances: (hits [n, k], nhits, inst [n, k], counts)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    recs = np.ascontiguousarray(records, dtype=np.uint32).reshape(-1, 16)
+    nodes = np.ascontiguousarray(top["nodes"], dtype=np.uint32).reshape(-1, 16)
+    tb = _Bvh(int(top["root_ref"]), (C.c_float * 3)(*[float(x) for x in top["root_lo"]]),
+              (C.c_float * 3)(*[float(x) for x in top["root_hi"]]), nodes.shape[0], recs.shape[0],
+              0, _ptr(nodes) if nodes.shape[0] else None, None, None, None, None)
+    arr = (_Bvh * len(bottoms))(*[b.c_struct() for b in bottoms])
+    hits = np.empty((n, k), dtype=HIT_DTYPE)
+    nh = np.zeros(n, dtype=np.uint32)
+    inst = np.empty((n, k), dtype=np.uint32)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    rc = lib().walker_trace_instances_multi(C.byref(tb), _ptr(recs), arr, len(bottoms), _ptr(r), n,
+                                            CLOSEST, k, isect, alpha_threshold, checker_freq,
+                                            _ptr(hits), _ptr(nh), _ptr(inst), _ptr(counts),
+                                            nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_instances_multi failed ({rc})")
+    return hits, nh, inst, counts
 

@@ -166,6 +166,19 @@ int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_
                            int isect, float alpha_threshold, uint32_t checker_freq,
                            or_hit* hits, uint32_t* inst, or_counts* counts, int nthreads);
 
+/* Multi-hit over a list of BVHs / over instances: one K-entry buffer across
+ * all elements (walk_one's acceptance rule), which / inst get K entries per ray: the list index /
+ * caller instance index of each kept hit (0xFFFFFFFF in unused slots); nhits may be NULL. */
+int walker_trace_list_multi(const or_bvh* list, uint32_t nlist, const float* rays, uint64_t n,
+                            uint32_t K, int isect, float alpha_threshold, uint32_t checker_freq,
+                            or_hit* hits, uint32_t* nhits, uint32_t* which, or_counts* counts,
+                            int nthreads);
+int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
+                                 const or_bvh* bottoms, uint32_t nbottoms, const float* rays,
+                                 uint64_t n, int query, uint32_t K, int isect,
+                                 float alpha_threshold, uint32_t checker_freq, or_hit* hits,
+                                 uint32_t* nhits, uint32_t* inst, or_counts* counts, int nthreads);
+
 /* The ray map of reading A27 on its own (pins): out = 8 floats (o', tmin, d', tmax). */
 void oracle_ray_to_object(const float* m, const float* ray, float* out);
 

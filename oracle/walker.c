@@ -387,6 +387,7 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
   /* multi-hit buffer: ascending t, equal t in the order found; a full buffer
      drops its worst and tmax shrinks to its last entry */
   or_hit mb[MAX_MULTI];
+  uint32_t mbw[MAX_MULTI]; /* list index of each kept hit (lists + multi-hit) */
   uint32_t nk = 0;
   const uint32_t K = jb->K;
 
@@ -444,9 +445,11 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
             uint32_t pos = nk < K ? nk : K - 1;
             while (pos > 0 && mb[pos - 1].t > t) {
               mb[pos] = mb[pos - 1];
+              mbw[pos] = mbw[pos - 1];
               pos--;
             }
             mb[pos].t = t; mb[pos].u = u; mb[pos].v = v; mb[pos].prim = tr->prim;
+            mbw[pos] = li;
             if (nk < K) nk++;
             if (nk == K) best_t = mb[K - 1].t;
           }
@@ -477,12 +480,15 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
   next_bvh:;
   }
 done:
-  if (jb->which) jb->which[r] = which;
   if (K) {
     const or_hit miss = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
-    for (uint32_t j = 0; j < K; ++j) jb->hits[r * K + j] = j < nk ? mb[j] : miss;
+    for (uint32_t j = 0; j < K; ++j) {
+      jb->hits[r * K + j] = j < nk ? mb[j] : miss;
+      if (jb->which) jb->which[r * K + j] = j < nk ? mbw[j] : 0xFFFFFFFFu;
+    }
     if (jb->nhits) jb->nhits[r] = nk;
   } else {
+    if (jb->which) jb->which[r] = which;
     jb->hits[r] = best;
   }
   if (jb->counts) jb->counts[r] = c;
@@ -545,6 +551,20 @@ int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uin
   return walker_run(&jb, nthreads);
 }
 
+int walker_trace_list_multi(const or_bvh* list, uint32_t nlist, const float* rays, uint64_t n,
+                            uint32_t K, int isect, float thr, uint32_t M, or_hit* hits,
+                            uint32_t* nhits, uint32_t* which, or_counts* counts, int nthreads) {
+  if (!list || nlist < 1 || !rays || !hits || K < 1 || K > MAX_MULTI) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
+  wjob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.b = list; jb.list = list; jb.nlist = nlist; jb.which = which;
+  jb.rays = rays; jb.n = n; jb.query = OR_CLOSEST; jb.isect = isect; jb.thr = thr;
+  jb.M = M; jb.hits = hits; jb.counts = counts; jb.K = K; jb.nhits = nhits;
+  return walker_run(&jb, nthreads);
+}
+
 static int walker_run(wjob_t* jb, int nthreads) {
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) {
@@ -578,6 +598,10 @@ typedef struct {
   int have;
   or_counts c;
   int bad;
+  /* multi-hit (K > 0): the kept hits, ascending t, with their instance index */
+  or_hit mb[MAX_MULTI];
+  uint32_t mbw[MAX_MULTI];
+  uint32_t nk, K, src;
 } istate_t;
 
 typedef struct {
@@ -593,6 +617,8 @@ typedef struct {
   or_hit* hits;
   uint32_t* inst;
   or_counts* counts;
+  uint32_t K;        /* multi-hit: hits kept per ray (0 = closest / any) */
+  uint32_t* nhits;
   uint64_t next;
   int err;
 } ijob_t;
@@ -649,6 +675,21 @@ static int walk_bottom(const ijob_t* jb, const or_bvh* b, const float* ray, ista
         if (!mt_tri(tr, o, d, tmin, S->best_t, &t, &u, &v)) continue;
         if (jb->isect == OR_ALPHA_TEX) S->c.alpha++;
         if (!walk_filter(b, k, jb->isect, u, v, jb->thr, jb->M)) continue;
+        if (S->K) {   /* multi-hit: as walk_one, the instance index kept beside each hit */
+          if (S->nk < S->K || t < S->best_t) {
+            uint32_t pos = S->nk < S->K ? S->nk : S->K - 1;
+            while (pos > 0 && S->mb[pos - 1].t > t) {
+              S->mb[pos] = S->mb[pos - 1];
+              S->mbw[pos] = S->mbw[pos - 1];
+              pos--;
+            }
+            S->mb[pos].t = t; S->mb[pos].u = u; S->mb[pos].v = v; S->mb[pos].prim = tr->prim;
+            S->mbw[pos] = S->src;
+            if (S->nk < S->K) S->nk++;
+            if (S->nk == S->K) S->best_t = S->mb[S->K - 1].t;
+          }
+          continue;
+        }
         if (jb->query == OR_ANY) {
           S->best.t = t; S->best.u = u; S->best.v = v; S->best.prim = tr->prim;
           S->have = 1;
@@ -688,6 +729,7 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
   S.best.t = INFINITY;
   S.best.prim = 0xFFFFFFFFu;
   S.best_t = ray[7];
+  S.K = jb->K;
   uint32_t which = 0xFFFFFFFFu;
   uint32_t st_ref[MAX_STACK];
   float st_tn[MAX_STACK];
@@ -731,6 +773,7 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
         oracle_ray_to_object(in->m, ray, oray);
         const int had = S.have;
         const float bt = S.best_t;
+        S.src = in->index;
         const int stop = walk_bottom(jb, &jb->bottoms[in->bvh], oray, &S);
         if (S.bad) goto done;
         if ((S.have && !had) || S.best_t < bt) which = in->index;
@@ -747,8 +790,17 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
     }
   }
 done:
-  jb->hits[r] = S.best;
-  if (jb->inst) jb->inst[r] = which;
+  if (S.K) {
+    const or_hit miss = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
+    for (uint32_t j = 0; j < S.K; ++j) {
+      jb->hits[r * S.K + j] = j < S.nk ? S.mb[j] : miss;
+      if (jb->inst) jb->inst[r * S.K + j] = j < S.nk ? S.mbw[j] : 0xFFFFFFFFu;
+    }
+    if (jb->nhits) jb->nhits[r] = S.nk;
+  } else {
+    jb->hits[r] = S.best;
+    if (jb->inst) jb->inst[r] = which;
+  }
   if (jb->counts) jb->counts[r] = S.c;
   if (S.bad) __atomic_store_n(&jb->err, 1, __ATOMIC_RELAXED);
 }
@@ -769,15 +821,25 @@ int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_
                            uint32_t nbottoms, const float* rays, uint64_t n, int query,
                            int isect, float thr, uint32_t M, or_hit* hits, uint32_t* inst,
                            or_counts* counts, int nthreads) {
+  return walker_trace_instances_multi(top, recs, bottoms, nbottoms, rays, n, query, 0, isect, thr,
+                                      M, hits, NULL, inst, counts, nthreads);
+}
+
+int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
+                                 const or_bvh* bottoms, uint32_t nbottoms, const float* rays,
+                                 uint64_t n, int query, uint32_t K, int isect, float thr,
+                                 uint32_t M, or_hit* hits, uint32_t* nhits, uint32_t* inst,
+                                 or_counts* counts, int nthreads) {
   if (!top || !recs || !bottoms || nbottoms < 1 || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
+  if (K > MAX_MULTI) return -1;
   if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
   if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
   ijob_t jb;
   memset(&jb, 0, sizeof jb);
   jb.top = top; jb.recs = recs; jb.bottoms = bottoms; jb.nbottoms = nbottoms;
   jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr; jb.M = M;
-  jb.hits = hits; jb.inst = inst; jb.counts = counts;
+  jb.hits = hits; jb.inst = inst; jb.counts = counts; jb.K = K; jb.nhits = nhits;
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) {
     iworker(&jb);

@@ -918,17 +918,29 @@ vsr_status vsr_group_destroy(vsr_group* g) {
   return VSR_OK;
 }
 
-vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_query query,
-                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                           uint32_t* d_which, vsr_counts* d_counts, void* stream) {
+}  // extern "C"
+
+namespace {
+// query: 0 closest, 1 any, 2 multi-hit (max_hits per ray, d_which max_hits per ray)
+vsr_status group_trace(vsr_group* g, const vsr_ray* d_rays, uint64_t n, int query,
+                       uint32_t max_hits, vsr_isect isect, const vsr_isect_params* params,
+                       vsr_hit* d_hits, uint32_t* d_num_hits, uint32_t* d_which,
+                       vsr_counts* d_counts, void* stream) {
   g_err.clear();
   if (!g) return fail(VSR_ERR_INVALID_ARG, "NULL group");
   if ((int)isect >= 100 && valid_isect(isect))
     return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for list queries");
+  if (query == 2 && (max_hits < 1 || max_hits > 16))
+    return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
   TraceParams p;
-  vsr_status st = make_params(g->scenes[0], query, isect, params, p);
+  vsr_status st = make_params(g->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
+                              isect, params, p);
   if (st != VSR_OK) return st;
   if (n == 0) return VSR_OK;
+  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
+    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
+  p.max_hits = (int)max_hits;
+  p.num_hits = d_num_hits;
   if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
   if (!aligned16(d_rays) || !aligned16(d_hits))
     return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
@@ -956,6 +968,29 @@ vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_
                                       reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "list trace launch");
   return VSR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                           uint32_t* d_which, vsr_counts* d_counts, void* stream) {
+  if ((int)query != VSR_QUERY_CLOSEST && (int)query != VSR_QUERY_ANY) {
+    g_err.clear();
+    return fail(VSR_ERR_INVALID_ARG, "invalid query");
+  }
+  return group_trace(g, d_rays, n, (int)query, 0, isect, params, d_hits, nullptr, d_which,
+                     d_counts, stream);
+}
+
+vsr_status vsr_trace_group_multi(vsr_group* g, const vsr_ray* d_rays, uint64_t n,
+                                 uint32_t max_hits, vsr_isect isect,
+                                 const vsr_isect_params* params, vsr_hit* d_hits,
+                                 uint32_t* d_num_hits, uint32_t* d_which, vsr_counts* d_counts,
+                                 void* stream) {
+  return group_trace(g, d_rays, n, 2, max_hits, isect, params, d_hits, d_num_hits, d_which,
+                     d_counts, stream);
 }
 
 }  // extern "C"
@@ -1161,17 +1196,27 @@ vsr_status vsr_instances_export(const vsr_instances* I, vsr_instances_view* v) {
   return VSR_OK;
 }
 
-vsr_status vsr_trace_instances(vsr_instances* I, const vsr_ray* d_rays, uint64_t n,
-                               vsr_query query, vsr_isect isect, const vsr_isect_params* params,
-                               vsr_hit* d_hits, uint32_t* d_inst, vsr_counts* d_counts,
-                               void* stream) {
+}  // extern "C"
+
+namespace {
+vsr_status instances_trace(vsr_instances* I, const vsr_ray* d_rays, uint64_t n, int query,
+                           uint32_t max_hits, vsr_isect isect, const vsr_isect_params* params,
+                           vsr_hit* d_hits, uint32_t* d_num_hits, uint32_t* d_inst,
+                           vsr_counts* d_counts, void* stream) {
   g_err.clear();
   if (!I) return fail(VSR_ERR_INVALID_ARG, "NULL instances");
   if ((int)isect >= 100 && valid_isect(isect))
     return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for instanced queries");
+  if (query == 2 && (max_hits < 1 || max_hits > 16))
+    return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
   TraceParams p;
-  vsr_status st = make_params(I->scenes[0], query, isect, params, p);
+  vsr_status st = make_params(I->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
+                              isect, params, p);
   if (st != VSR_OK) return st;
+  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
+    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
+  p.max_hits = (int)max_hits;
+  p.num_hits = d_num_hits;
   if (I->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only instances cannot be traced");
   if (n == 0) return VSR_OK;
   if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
@@ -1199,6 +1244,30 @@ vsr_status vsr_trace_instances(vsr_instances* I, const vsr_ray* d_rays, uint64_t
                                       reinterpret_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "instanced trace launch");
   return VSR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+vsr_status vsr_trace_instances(vsr_instances* I, const vsr_ray* d_rays, uint64_t n,
+                               vsr_query query, vsr_isect isect, const vsr_isect_params* params,
+                               vsr_hit* d_hits, uint32_t* d_inst, vsr_counts* d_counts,
+                               void* stream) {
+  if ((int)query != VSR_QUERY_CLOSEST && (int)query != VSR_QUERY_ANY) {
+    g_err.clear();
+    return fail(VSR_ERR_INVALID_ARG, "invalid query");
+  }
+  return instances_trace(I, d_rays, n, (int)query, 0, isect, params, d_hits, nullptr, d_inst,
+                         d_counts, stream);
+}
+
+vsr_status vsr_trace_instances_multi(vsr_instances* I, const vsr_ray* d_rays, uint64_t n,
+                                     uint32_t max_hits, vsr_isect isect,
+                                     const vsr_isect_params* params, vsr_hit* d_hits,
+                                     uint32_t* d_num_hits, uint32_t* d_inst,
+                                     vsr_counts* d_counts, void* stream) {
+  return instances_trace(I, d_rays, n, 2, max_hits, isect, params, d_hits, d_num_hits, d_inst,
+                         d_counts, stream);
 }
 
 vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_query query,

@@ -200,10 +200,13 @@ __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, fl
 // S:285-293): the maxk smallest-t accepted hits, ascending t, equal t in
 // discovery order; once full, tmax shrinks to the worst kept t.
 struct NoMulti {};
-template <int K>
+template <int K, bool SRC = false>
 struct MultiBuf {
+  static constexpr bool kSrc = SRC;
   float t[K], u[K], v[K];
   uint32_t prim[K];
+  uint32_t src[SRC ? K : 1];   // list / instance index of each kept hit (compound queries)
+  uint32_t cur_src;            // the element being traversed
   int n;
   int maxk;
 };
@@ -226,12 +229,14 @@ __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb
           mb.u[pos] = mb.u[pos - 1];
           mb.v[pos] = mb.v[pos - 1];
           mb.prim[pos] = mb.prim[pos - 1];
+          if constexpr (M::kSrc) mb.src[pos] = mb.src[pos - 1];
           --pos;
         }
         mb.t[pos] = hr.t;
         mb.u[pos] = hr.u;
         mb.v[pos] = hr.v;
         mb.prim[pos] = __float_as_uint(td.a.w);
+        if constexpr (M::kSrc) mb.src[pos] = mb.cur_src;
         if (mb.n < mb.maxk) ++mb.n;
         if (mb.n == mb.maxk) T.best_t = mb.t[mb.maxk - 1];
       }
@@ -659,6 +664,99 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_kernel(const
   if (p.which) p.which[id] = hit_in;
 }
 
+// Multi-hit query over a LIST of BVHs / over instances (the
+// visibility queries closest_hit, any_hit AND multi_hit iterate over lists
+// whose elements may be BVHs): one K-entry buffer across all elements, each
+// kept hit tagged with its element (list index, or the caller's instance
+// index); output as trace_multi_kernel plus `which` per kept hit.
+template <class I, int K>
+__device__ __forceinline__ void write_multi(const TraceParams& p, uint64_t id,
+                                            const MultiBuf<K, true>& mb, const I& isect) {
+  float4* out = p.hits + id * (uint64_t)p.max_hits;
+  uint32_t* wout = p.which ? p.which + id * (uint64_t)p.max_hits : nullptr;
+  for (int j = 0; j < mb.maxk; ++j) {
+    const bool kept = j < mb.n;
+    out[j] = kept ? make_float4(mb.t[j], mb.u[j], mb.v[j], __uint_as_float(mb.prim[j]))
+                  : make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f, __uint_as_float(kMissPrim));
+    if (wout) wout[j] = kept ? mb.src[j] : kMissPrim;
+  }
+  if (p.num_hits) p.num_hits[id] = (uint32_t)mb.n;
+  if constexpr (I::kCounts) {
+    p.counts[id] = make_uint4(isect.num_boxes, isect.num_tris, isect.lookups(), 0u);
+  }
+}
+
+template <class I, int K>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_multi_kernel(const TraceParams p) {
+  const uint64_t blk = launch_block(p);
+  const uint64_t id = blk * kBlock + threadIdx.x;
+  if (id >= p.n) return;
+  I isect = make_isect<I>(p);
+  Trav T;
+  float2 stack[kMaxStack];
+  MultiBuf<K, true> mb;
+  mb.n = 0;
+  mb.maxk = p.max_hits;
+  start_ray(p, T, isect, id);   // loads the ray (the list's roots are tested below)
+  isect.reset();
+  const int woct = warp_octant(T.r);
+  for (uint32_t s = 0; s < p.list_count; ++s) {
+    const DevScene S = p.list[s];
+    bind_scene_data(isect, p.list_data[s]);
+    const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
+    float tn;
+    if (!box_hook(isect, T.r, root, T.best_t, tn)) continue;
+    T.cur = S.root_ref;
+    T.sp = 0;
+    mb.cur_src = s;
+    traverse<kMulti>(S, T, isect, stack, woct, mb);
+  }
+  write_multi<I, K>(p, id, mb, isect);
+}
+
+template <class I, int K>
+__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_multi_kernel(const TraceParams p) {
+  const uint64_t blk = launch_block(p);
+  const uint64_t id = blk * kBlock + threadIdx.x;
+  if (id >= p.n) return;
+  I isect = make_isect<I>(p);
+  Trav T;
+  float2 stack[kInstStack];
+  MultiBuf<K, true> mb;
+  mb.n = 0;
+  mb.maxk = p.max_hits;
+  if (start_ray(p, T, isect, id)) {   // world ray; counted test of the top-level root box
+    const int woct = warp_octant(T.r);
+    for (;;) {
+      if (!descend_oct(p.scene, T, isect, stack, woct)) break;
+      const uint32_t first = T.cur & kLeafFirstMask;
+      const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
+      for (uint32_t k = first; k < end; ++k) {
+        const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
+        const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
+        const uint32_t b = __float_as_uint(ex.x);
+        const DevScene& S = p.list[b];
+        bind_scene_data(isect, p.list_data[b]);
+        Trav B = T;
+        float4 oa, ob;
+        to_object(r0, r1, r2, T.r, oa, ob);
+        make_ray(B.r, oa, ob);
+        B.sp = 0;
+        B.cur = S.root_ref;
+        const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1],
+                        S.root_hi[2]};
+        float tn;
+        if (!box_hook(isect, B.r, root, B.best_t, tn)) continue;
+        mb.cur_src = __float_as_uint(ex.y);
+        traverse<kMulti>(S, B, isect, stack + T.sp, warp_octant(B.r), mb);
+        T.best_t = B.best_t;   // a full buffer's worst kept t prunes the rest
+      }
+      if (!pop(T, stack)) break;
+    }
+  }
+  write_multi<I, K>(p, id, mb, isect);
+}
+
 // Persistent schedule (VSR_SCHED=persistent): grid sized to residency; warps
 // claim kChunk rays per atomicAdd and refill idle lanes after each leaf once
 // `refill` lanes are idle.  Measured slower than the direct schedule on the
@@ -836,6 +934,38 @@ cudaError_t launch_list(const TraceParams& p, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <class I>
+cudaError_t launch_compound_multi(const TraceParams& p, cudaStream_t st) {
+  const uint64_t need = (p.n + kBlock - 1) / kBlock;
+  if (need > 0x7FFFFFFFull) return cudaErrorInvalidValue;
+  const bool pdl = p.perm && p.pdl;
+  cudaError_t e;
+  if (p.instances)
+    e = p.max_hits <= 4 ? launch_k(trace_instances_multi_kernel<I, 4>, need, kBlock, pdl, st, p)
+                        : launch_k(trace_instances_multi_kernel<I, 16>, need, kBlock, pdl, st, p);
+  else
+    e = p.max_hits <= 4 ? launch_k(trace_list_multi_kernel<I, 4>, need, kBlock, pdl, st, p)
+                        : launch_k(trace_list_multi_kernel<I, 16>, need, kBlock, pdl, st, p);
+  if (e != cudaSuccess) return e;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_compound_multi(int isect, const TraceParams& p, cudaStream_t st) {
+  switch (isect) {
+    case VSR_ISECT_NONE: return launch_compound_multi<no_intersector>(p, st);
+    case VSR_ISECT_DEFAULT: return launch_compound_multi<default_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE: return launch_compound_multi<alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL: return launch_compound_multi<alpha_procedural_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_compound_multi<alpha_bilinear_intersector>(p, st);
+    case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_compound_multi<alpha_procedural_uv_intersector>(p, st);
+    case VSR_ISECT_COUNT: return launch_compound_multi<cost_intersector<default_intersector>>(p, st);
+    case VSR_ISECT_COUNT_ALPHA_TEXTURE:
+      return launch_compound_multi<cost_intersector<alpha_texture_intersector>>(p, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 template <int Q, class I>
 cudaError_t launch_inst(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
@@ -971,7 +1101,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     p.perm = perm;
   }
   if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
-  cudaError_t e = p.instances ? (query == kAny ? dispatch_inst<kAny>(isect, p, st)
+  cudaError_t e = (p.list && query == kMulti) ? dispatch_compound_multi(isect, p, st)
+                  : p.instances ? (query == kAny ? dispatch_inst<kAny>(isect, p, st)
                                                 : dispatch_inst<kClosest>(isect, p, st))
                   : p.list ? (query == kAny ? dispatch_list<kAny>(isect, p, st)
                                           : dispatch_list<kClosest>(isect, p, st))

@@ -54,7 +54,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_trace_group", "vsr_instances_create", "vsr_instances_destroy",
                     "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
                     "vsr_trace_pinhole", "vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free",
-                    "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close", "vsr_bvh_build_ploc"]
+                    "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close", "vsr_bvh_build_ploc",
+                    "vsr_trace_group_multi", "vsr_trace_instances_multi"]
 
 
 class VsrError(RuntimeError):
@@ -172,6 +173,10 @@ def lib():
         L.vsr_bvh_build_gpu.restype = C.c_int
         L.vsr_bvh_build_ploc.argtypes = [P, C.c_uint32, C.c_uint32]
         L.vsr_bvh_build_ploc.restype = C.c_int
+        for name in ("vsr_trace_group_multi", "vsr_trace_instances_multi"):
+            getattr(L, name).argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int,
+                                         C.POINTER(IsectParams), P, P, P, P, P]
+            getattr(L, name).restype = C.c_int
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                      P, P, P]
@@ -474,6 +479,26 @@ class Group:
                                      _stream_handle(stream)))
         return hits, which, counts
 
+    def trace_multi(self, rays, max_hits, isect=DEFAULT, stream=None, alpha_threshold=0.01,
+                    checker_freq=8):
+        """vsr_trace_group_multi: (hits [n, k, 4], num_hits [n], which [n, k], counts or None)."""
+        return _compound_multi(lib().vsr_trace_group_multi, self._h, rays, max_hits, isect,
+                               stream, alpha_threshold, checker_freq)
+
+
+def _compound_multi(fn, handle, rays, max_hits, isect, stream, alpha_threshold, checker_freq):
+    import torch
+    n = rays.shape[0]
+    hits = torch.empty((n, max_hits, 4), dtype=torch.float32, device=rays.device)
+    num = torch.empty((n,), dtype=torch.int32, device=rays.device)
+    which = torch.empty((n, max_hits), dtype=torch.int32, device=rays.device)
+    counts = (torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+              if isect in (COUNT, COUNT_ALPHA_TEXTURE) else None)
+    prm = IsectParams(alpha_threshold, checker_freq)
+    _check(fn(handle, _ptr(rays), n, max_hits, isect, C.byref(prm), _ptr(hits), _ptr(num),
+              _ptr(which), _ptr(counts), _stream_handle(stream)))
+    return hits, num, which, counts
+
 
 class Instances:
     """Two-level instancing (vsr_instances_create / vsr_trace_instances): a top-level BVH
@@ -522,6 +547,12 @@ class Instances:
                                          _ptr(hits), _ptr(inst), _ptr(counts),
                                          _stream_handle(stream)))
         return hits, inst, counts
+
+    def trace_multi(self, rays, max_hits, isect=DEFAULT, stream=None, alpha_threshold=0.01,
+                    checker_freq=8):
+        """vsr_trace_instances_multi: (hits [n, k, 4], num_hits [n], inst [n, k], counts)."""
+        return _compound_multi(lib().vsr_trace_instances_multi, self._h, rays, max_hits, isect,
+                               stream, alpha_threshold, checker_freq)
 
     def export(self) -> dict:
         """Host copies of the top level: nodes [num_nodes, 16] uint32 (pair nodes) and

@@ -130,3 +130,25 @@ def test_instances_edge_cases(V, oracle_lib):
     # run-time controls are not provided for instanced queries
     with pytest.raises(V.VsrError):
         inst.trace(rt, V.CLOSEST, V.RUNTIME_SWITCH_DEFAULT)
+
+
+@pytest.mark.parametrize("k", [1, 4])
+def test_instances_multi_vs_walker(V, oracle_lib, k):
+    o = oracle_lib
+    models = [W.random_soup(150, seed=s, extent=3.0, size=1.5) for s in (71, 72)]
+    m = random_affine(32, 73, extent=12.0)
+    bvh = np.arange(32) % 2
+    rays = W.random_rays(4001, seed=74, extent=30.0, target=12.0).data
+    scenes, inst, top, bottoms = setup(V, models, bvh, m)
+    r = torch.from_numpy(rays).cuda()
+    for kind, ok in ((V.ALPHA_TEXTURE, o.ALPHA_TEX), (V.COUNT_ALPHA_TEXTURE, o.ALPHA_TEX)):
+        h, n, ii, c = inst.trace_multi(r, k, kind)
+        torch.cuda.synchronize()
+        wh, wn, wi, wc = o.walk_instances_multi(top, top["records"], bottoms, rays, k, ok)
+        assert np.array_equal(V.hits_to_numpy(h.reshape(-1, 4)).view(np.uint32),
+                              wh.reshape(-1).view(np.uint32))
+        assert np.array_equal(n.cpu().numpy().astype(np.uint32), wn)
+        assert np.array_equal(ii.cpu().numpy().astype(np.uint32), wi)
+        if c is not None:
+            cc = V.counts_to_numpy(c)
+            assert np.array_equal(cc["boxes"], wc["boxes"]) and np.array_equal(cc["tris"], wc["tris"])

@@ -103,3 +103,29 @@ def test_group_errors(V):
     with pytest.raises(V.VsrError) as e:
         g.trace(r, V.CLOSEST, V.RUNTIME_SWITCH_DEFAULT)
     assert e.value.status == V.ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("k", [1, 4, 16])
+def test_group_multi_vs_walker(V, oracle_lib, k):
+    """vsr_trace_group_multi: hits, kept counts, per-hit list index and counts bit-exact vs
+    walker C's multi-hit over the list."""
+    o = oracle_lib
+    sc = W.random_soup(1500, seed=90, size=3.0)
+    rays = W.random_rays(3001, seed=91)
+    subs = W.split_scene(sc, 4)
+    scenes = [V.Scene.from_workload(s).build() for s in subs]
+    g = V.Group(scenes)
+    bs = [bvh_check.to_oracle(s.export()) for s in scenes]
+    r = torch.from_numpy(rays.data).cuda()
+    for kind, ok in ((V.ALPHA_TEXTURE, o.ALPHA_TEX), (V.COUNT, o.DEFAULT),
+                     (V.ALPHA_PROCEDURAL, o.ALPHA_PROC)):
+        h, n, w, c = g.trace_multi(r, k, kind)
+        torch.cuda.synchronize()
+        wh, wn, ww, wc = o.walk_list_multi(bs, rays.data, k, ok)
+        assert np.array_equal(V.hits_to_numpy(h.reshape(-1, 4)).view(np.uint32),
+                              wh.reshape(-1).view(np.uint32))
+        assert np.array_equal(n.cpu().numpy().astype(np.uint32), wn)
+        assert np.array_equal(w.cpu().numpy().astype(np.uint32), ww)
+        if c is not None:
+            cc = V.counts_to_numpy(c)
+            assert np.array_equal(cc["boxes"], wc["boxes"]) and np.array_equal(cc["tris"], wc["tris"])

@@ -288,3 +288,36 @@ def test_instances_validation(vsr):
                                        None, None)
     assert st == vsr.ERR_UNSUPPORTED     # host-only instances are not traceable
     del C
+
+
+def test_instances_multi_walker(vsr, oracle_lib):
+    """Multi-hit over instances: k = 1 is the closest query; for k = 4 the kept t lists equal the
+    k smallest accepted t over all instances by brute force."""
+    o = oracle_lib
+    models = [W.random_soup(120, seed=s, extent=3.0) for s in (51, 52)]
+    m = random_affine(24, 53, extent=12.0)
+    bvh = np.arange(24) % 2
+    rays = W.random_rays(2000, seed=54, extent=30.0, target=12.0)
+    scenes, inst = _host_instances(vsr, models, bvh, m)
+    top = inst.export()
+    bottoms = [bvh_check.to_oracle(s.export()) for s in scenes]
+    h1, n1, i1, c1 = o.walk_instances_multi(top, top["records"], bottoms, rays, 1, o.ALPHA_TEX)
+    hc, ic, cc = o.walk_instances(top, top["records"], bottoms, rays, o.CLOSEST, o.ALPHA_TEX)
+    assert np.array_equal(h1[:, 0], hc) and np.array_equal(i1[:, 0], ic) and np.array_equal(c1, cc)
+    k = 4
+    h, nh, ii, c = o.walk_instances_multi(top, top["records"], bottoms, rays, k, o.ALPHA_TEX)
+    all_t = []
+    for j in range(len(bvh)):
+        hm, nm, _ = o.trace_multi(models[bvh[j]], o.rays_to_object(rays, m[j]), k, o.ALPHA_TEX)
+        all_t.append(np.where(hm["prim"] != MISS, hm["t"], np.inf))
+    best = np.sort(np.concatenate(all_t, axis=1), axis=1)[:, :k]
+    assert np.array_equal(np.where(h["prim"] != MISS, h["t"], np.inf), best.astype(np.float32))
+    assert np.array_equal(nh, (best < np.inf).sum(axis=1))
+    assert np.all(ii[h["prim"] == MISS] == MISS)
+    # every kept (instance, prim) is an accepted pair with exactly the kept (t, u, v)
+    for i in range(0, rays.n, 7):
+        for j in range(int(nh[i])):
+            q = int(ii[i, j])
+            ro = o.rays_to_object(rays.data[i:i + 1], m[q])[0]
+            acc, t, u, v = o.eval_pair(models[bvh[q]], ro, int(h["prim"][i, j]), o.ALPHA_TEX)
+            assert acc and (t, u, v) == (h["t"][i, j], h["u"][i, j], h["v"][i, j])

@@ -60,3 +60,39 @@ def test_counts_add_over_the_list_and_which(oracle_lib):
     # reversed list: the near quad first prunes the far BVH's root (tn 2 > best_t 1)
     h, which, c = o.walk_list(bs[::-1], rays, o.CLOSEST, o.COUNT)
     assert which[0] == 0 and (c["boxes"][0], c["tris"][0]) == (2, 2)
+
+
+@pytest.mark.parametrize("parts,k", [(1, 4), (3, 4), (5, 16)])
+def test_list_multi_walker_equals_bruteforce(oracle_lib, parts, k):
+    """Multi-hit over a list: the walker's k smallest-t accepted hits across
+    all elements equal the brute force's on the concatenated triangles (t lists exact, prims up
+    to exact ties), and each kept hit's list index maps it back to its element."""
+    o = oracle_lib
+    sc = W.random_soup(600, seed=30 + parts, size=3.0)
+    rays = W.random_rays(2000, seed=31)
+    subs = W.split_scene(sc, parts)
+    cat, offs = W.concat_scenes(subs)
+    bs = [o.build_bvh(s, 2) for s in subs]
+    for isect in (o.DEFAULT, o.ALPHA_TEX):
+        ref, rn, rc = o.trace_multi(cat, rays, k, isect)
+        h, nh, which, c = o.walk_list_multi(bs, rays, k, isect)
+        assert np.array_equal(nh, rn)
+        assert np.array_equal(h["t"], ref["t"])
+        kept = h["prim"] != MISS
+        glob = np.where(kept, offs[np.minimum(which, parts - 1)] + h["prim"], MISS)
+        # equal t may come in another order: compare per-ray sets of (t, prim)
+        for i in np.nonzero((glob != ref["prim"]).any(axis=1))[0]:
+            assert sorted(zip(h["t"][i][kept[i]], glob[i][kept[i]])) == \
+                sorted(zip(ref["t"][i][kept[i]], ref["prim"][i][kept[i]])) or rc[i] > 0, i
+        assert np.all(which[~kept] == MISS)
+
+
+def test_single_element_list_multi_is_walk_multi(oracle_lib):
+    o = oracle_lib
+    sc = W.random_soup(500, seed=33)
+    rays = W.random_rays(1500, seed=34)
+    b = o.build_bvh(sc, 2)
+    h1, n1, c1 = o.walk_multi(b, rays, 4, o.ALPHA_TEX)
+    h2, n2, w2, c2 = o.walk_list_multi([b], rays, 4, o.ALPHA_TEX)
+    assert np.array_equal(h1, h2) and np.array_equal(n1, n2) and np.array_equal(c1, c2)
+    assert np.all(w2[h2["prim"] != MISS] == 0)

@@ -85,6 +85,12 @@ MUTANTS = [
     ("walker.c", "float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;",
      "float a = ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fx;",
      "walker bilinear: fx used as the row weight"),
+    ("walker.c", "              mbw[pos] = mbw[pos - 1];\n", "",
+     "list multi-hit: list index not moved with its hit"),
+    ("walker.c", "              S->mbw[pos] = S->mbw[pos - 1];\n", "",
+     "instance multi-hit: instance index not moved with its hit"),
+    ("walker.c", "            if (S->nk == S->K) S->best_t = S->mb[S->K - 1].t;\n", "",
+     "instance multi-hit: a full buffer does not shrink tmax"),
 ]
 
 
