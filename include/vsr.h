@@ -200,6 +200,18 @@ vsr_status vsr_trace(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_qu
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream);
 
+/* Query on the scene's triangles as a plain LIST, without the BVH ("the user
+ * might decide that a BVH is not required and just pass iterators to a linear list of primitives
+ * to the query routines"; the intersector then replaces the primitive test inside the loop).
+ * Every ray tests every triangle in caller order (degenerate ones excluded, as by the build):
+ * closest keeps the lowest index among equal t, any-hit returns the lowest accepted index — the
+ * brute-force definition.  O(rays x triangles): for small scenes and as the BVH's reference.
+ * COUNT kinds count triangle tests (num_boxes = 0).  Other arguments as vsr_trace; RUNTIME_*
+ * controls: VSR_ERR_UNSUPPORTED. */
+vsr_status vsr_trace_primitives(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n,
+                                vsr_query query, vsr_isect isect, const vsr_isect_params* params,
+                                vsr_hit* d_hits, vsr_counts* d_counts, void* stream);
+
 /* Primary rays generated INSIDE the trace kernel (SURVEY.md §8(f) NEXT-4 "fused camera ray
  * generator": no ray buffer, no 32 B/ray read).  Ray i is the i-th of the input recipe's
  * (8x8 tile, sample, y, x) order and is bit-identical to the host recipe:

@@ -115,6 +115,11 @@ struct vsr_scene {
   PairNode* d_nodes = nullptr;
   Tri* d_tris = nullptr;
   Side* d_sides = nullptr;
+  // caller-order copies for vsr_trace_primitives (built on first use)
+  std::mutex caller_mu;
+  Tri* d_tris_caller = nullptr;
+  Side* d_sides_caller = nullptr;
+  uint32_t num_caller = 0;
   TexDesc* d_texdescs = nullptr;
   uint8_t* d_texels = nullptr;
   unsigned long long* d_counters = nullptr;   // persistent-kernel work counters
@@ -139,6 +144,11 @@ struct vsr_scene {
     cudaFree(d_nodes);
     cudaFree(d_tris);
     cudaFree(d_sides);
+    cudaFree(d_tris_caller);
+    cudaFree(d_sides_caller);
+    d_tris_caller = nullptr;
+    d_sides_caller = nullptr;
+    num_caller = 0;
     cudaFree(d_texdescs);
     cudaFree(d_texels);
     cudaFree(d_counters);
@@ -716,6 +726,79 @@ vsr_status vsr_ipc_close(void* d_ptr, int device) {
   DeviceGuard g(device);
   cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
   return e == cudaSuccess ? VSR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+}
+
+}  // extern "C"
+
+namespace {
+// The scene's triangles and sidecars in caller order (prim id order), for the
+// primitive-list query; ids the build excluded (degenerate) keep prim = ~0.
+vsr_status ensure_caller_order(vsr_scene* s) {
+  std::lock_guard<std::mutex> lk(s->caller_mu);
+  if (s->d_tris_caller) return VSR_OK;
+  const uint32_t m = s->dev.num_tris;
+  std::vector<Tri> tris(m);
+  std::vector<Side> sides(m);
+  cudaError_t e;
+  if ((e = cudaMemcpy(tris.data(), s->d_tris, sizeof(Tri) * m, cudaMemcpyDeviceToHost)) !=
+          cudaSuccess ||
+      (e = cudaMemcpy(sides.data(), s->d_sides, sizeof(Side) * m, cudaMemcpyDeviceToHost)) !=
+          cudaSuccess)
+    return cuda_fail(e, "caller-order copy");
+  uint32_t P = s->num_tris_input;
+  for (const Tri& t : tris) P = std::max(P, t.prim + 1u);
+  Tri none{};
+  none.prim = 0xFFFFFFFFu;
+  std::vector<Tri> ct(P, none);
+  std::vector<Side> cs(P, Side{});
+  for (uint32_t k = 0; k < m; ++k) {
+    ct[tris[k].prim] = tris[k];
+    cs[tris[k].prim] = sides[k];
+  }
+  vsr_status st;
+  if ((st = dev_upload(&s->d_tris_caller, ct.data(), P, "caller-order triangles")) != VSR_OK ||
+      (st = dev_upload(&s->d_sides_caller, cs.data(), P, "caller-order sidecars")) != VSR_OK)
+    return st;
+  s->num_caller = P;
+  return VSR_OK;
+}
+}  // namespace
+
+extern "C" {
+
+vsr_status vsr_trace_primitives(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                                vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                                vsr_counts* d_counts, void* stream) {
+  g_err.clear();
+  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
+  if ((int)isect >= 100 && valid_isect(isect))
+    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for primitive lists");
+  TraceParams p;
+  vsr_status st = make_params(s, query, isect, params, p);
+  if (st != VSR_OK) return st;
+  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
+  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no triangles on the device: build first");
+  if (n == 0) return VSR_OK;
+  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
+  if (!aligned16(d_rays) || !aligned16(d_hits))
+    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
+  if (needs_counts(isect)) {
+    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
+    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
+  }
+  DeviceGuard g(s->device);
+  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+  if ((st = ensure_caller_order(s)) != VSR_OK) return st;
+  p.scene.tris = s->d_tris_caller;
+  p.scene.num_tris = s->num_caller;
+  p.data.sides = s->d_sides_caller;
+  p.rays = reinterpret_cast<const float4*>(d_rays);
+  p.hits = reinterpret_cast<float4*>(d_hits);
+  p.counts = reinterpret_cast<uint4*>(d_counts);
+  p.n = n;
+  cudaError_t e = launch_prims(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "primitive-list trace launch");
+  return VSR_OK;
 }
 
 vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query query,

@@ -47,5 +47,8 @@ size_t order_scratch_bytes(uint64_t n);
 void set_kernel_events(void* start, void* stop);
 cudaError_t filter_fn_pointer(int kind, void** out);
 uint64_t launch_count();
+// Query on the scene's triangles as a plain list (no BVH); p.scene.tris / p.data.sides in
+// caller order (vsr_trace_primitives).
+cudaError_t launch_prims(int query, int isect, const TraceParams& p, cudaStream_t st);
 
 }  // namespace vsr

@@ -55,7 +55,7 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
                     "vsr_trace_pinhole", "vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free",
                     "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close", "vsr_bvh_build_ploc",
-                    "vsr_trace_group_multi", "vsr_trace_instances_multi"]
+                    "vsr_trace_group_multi", "vsr_trace_instances_multi", "vsr_trace_primitives"]
 
 
 class VsrError(RuntimeError):
@@ -180,6 +180,9 @@ def lib():
         L.vsr_trace.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams), P, P, P]
         L.vsr_trace_host.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
                                      P, P, P]
+        L.vsr_trace_primitives.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int,
+                                           C.POINTER(IsectParams), P, P, P]
+        L.vsr_trace_primitives.restype = C.c_int
         L.vsr_trace_multi.argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int,
                                       C.POINTER(IsectParams), P, P, P, P]
         L.vsr_destroy.argtypes = [P]
@@ -359,6 +362,19 @@ class Scene:
         _check(lib().vsr_trace_tiles(self._h, _ptr(rays), rays.shape[0], tile_rays, rank, world,
                                      query, isect, C.byref(prm), frame_hits_ptr,
                                      frame_counts_ptr, _stream_handle(stream)))
+
+    def trace_primitives(self, rays, query=CLOSEST, isect=DEFAULT, stream=None,
+                         alpha_threshold=0.01, checker_freq=8):
+        """vsr_trace_primitives: the query on the triangles as a plain list (no BVH)."""
+        import torch
+        n = rays.shape[0]
+        hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
+        counts = (torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+                  if isect in (COUNT, COUNT_ALPHA_TEXTURE) else None)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_primitives(self._h, _ptr(rays), n, query, isect, C.byref(prm),
+                                          _ptr(hits), _ptr(counts), _stream_handle(stream)))
+        return hits, counts
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, hits=None, num_hits=None, counts=None,
                     stream=None, alpha_threshold=0.01, checker_freq=8):
