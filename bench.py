@@ -106,7 +106,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
                0x100: "display_clock_setting"}
 
-    def __init__(self, device_index=0, period=0.0003):
+    def __init__(self, device_index=0, period=0.0):   # back-to-back NVML reads (~0.1 ms each)
         self.samples = []
         self.reasons = 0
         self.max_mhz = None
