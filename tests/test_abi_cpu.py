@@ -188,3 +188,25 @@ def test_import_validation(vsr):
     bad = dict(e)
     bad["root_ref"] = 0x80000000 | (3 << 26) | 198   # leaf range past the end
     assert _err(vsr, lambda: vsr.Scene.import_arrays(bad)) == vsr.ERR_INVALID_ARG
+
+
+def test_checkpoint_roundtrip(vsr, tmp_path):
+    """checkpoint.save_scene / checkpoint.load_scene: a saved host-only scene re-imports (re-validated) to the
+    identical export arrays; a corrupted file is rejected by the importer's validation."""
+    from paper_1912_12786_b200 import checkpoint as io
+    sc = W.random_soup(400, seed=81)
+    s = vsr.Scene.from_workload(sc, device=-1).build()
+    p = str(tmp_path / "s.npz")
+    io.save_scene(s, p)
+    t = io.load_scene(p, device=-1)
+    a, b = s.export(), t.export()
+    for k in ("nodes", "tris", "sides", "texdescs", "texels", "root_lo", "root_hi"):
+        assert np.array_equal(a[k], b[k]), k
+    assert a["root_ref"] == b["root_ref"]
+    z = dict(np.load(p))
+    z["nodes"] = z["nodes"].copy()
+    z["nodes"][0, 12] = 10 ** 6            # an out-of-range child reference
+    bad = str(tmp_path / "bad.npz")
+    np.savez(bad, **z)
+    with pytest.raises(vsr.VsrError):
+        io.load_scene(bad, device=-1)

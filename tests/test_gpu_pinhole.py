@@ -66,3 +66,19 @@ def test_c_program_traces_on_the_gpu(V, tmp_path):
                     f"-Wl,-rpath,{libdir}", "-lm", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_checkpoint_restores_a_traceable_scene(V, tmp_path):
+    """A scene saved with checkpoint.save_scene and restored on the GPU traces bit-identically."""
+    from paper_1912_12786_b200 import checkpoint
+    sc, rays = W.config("C2", 128, 64)
+    s = V.Scene.from_workload(sc).build()
+    p = str(tmp_path / "c2.npz")
+    checkpoint.save_scene(s, p)
+    t = checkpoint.load_scene(p, device=0)
+    d = torch.from_numpy(rays.data).cuda()
+    for q in (V.CLOSEST, V.ANY):
+        a, _ = s.trace(d, q, V.ALPHA_TEXTURE)
+        b, _ = t.trace(d, q, V.ALPHA_TEXTURE)
+        torch.cuda.synchronize()
+        assert torch.equal(a.view(torch.int32), b.view(torch.int32))
