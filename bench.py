@@ -302,6 +302,8 @@ def run_own(args):
     # ---- headline ----
     sampler = ClockSampler(local)
     ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler)
+    torch.cuda.synchronize()
+    head_hits = vsr.hits_to_numpy(hits).copy() if not tiles else None   # for the parity summary
     # the trace kernel alone (roofline denominator), in a second pass: events
     # between the order pass and the trace kernel would break their PDL overlap
     kms = []
@@ -494,7 +496,8 @@ def run_own(args):
     # ---- cpu baseline (rank 0, N = 1 only) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(sc, rays, args, target_s=args.cpu_seconds, scene=scene)
+        cpu = cpu_baseline(sc, rays, args, target_s=args.cpu_seconds, scene=scene,
+                           gpu_hits=head_hits)
 
     if rank == 0:
         clocks = sampler.summary()
@@ -547,8 +550,10 @@ def _oracle_kind(name):
             "alpha_procedural": oracle.ALPHA_PROC, "count": oracle.DEFAULT}[base]
 
 
-def cpu_baseline(sc, rays, args, target_s=12.0, scene=None):
-    """Oracle S as it stands (brute force, all host cores) on a bounded seeded sample."""
+def cpu_baseline(sc, rays, args, target_s=12.0, scene=None, gpu_hits=None):
+    """Oracle S as it stands (brute force, all host cores) on a bounded seeded sample; with
+    the headline frame's GPU hits it also reports a parity summary against the oracle on that
+    sample and against walker C on the whole frame."""
     import oracle
     oq = oracle.CLOSEST if args.query == "closest" else oracle.ANY
     ok = _oracle_kind(args.isect)
@@ -561,9 +566,10 @@ def cpu_baseline(sc, rays, args, target_s=12.0, scene=None):
     per_ray = (time.perf_counter() - t0) / probe.shape[0]
     m = int(min(rays.n, max(256, target_s / max(per_ray, 1e-9))))
     for _ in range(4):   # re-calibrate until the sample takes about target_s
-        sample = rays.data[np.sort(rng.choice(rays.n, m, replace=False))]
+        idx = np.sort(rng.choice(rays.n, m, replace=False))
+        sample = rays.data[idx]
         t0 = time.perf_counter()
-        oracle.trace(osc, sample, oq, ok, nthreads=cores)
+        ref = oracle.trace(osc, sample, oq, ok, nthreads=cores)
         dt = time.perf_counter() - t0
         if dt >= 0.5 * target_s or m >= rays.n:
             break
@@ -583,6 +589,27 @@ def cpu_baseline(sc, rays, args, target_s=12.0, scene=None):
         out["walker"] = {"value": round(rays.n / wdt / 1e6, 3), "unit": UNIT, "cores": cores,
                          "kind": "oracle walker C (BVH traversal, CPU)",
                          "sample": f"full {rays.n}-ray frame, {wdt:.2f} s"}
+    if gpu_hits is not None:
+        # parity of the timed headline frame (the GPU hits of the last timed step)
+        g = gpu_hits[idx]
+        ghit, rhit = g["prim"] != 0xFFFFFFFF, ref["prim"] != 0xFFFFFFFF
+        par = {"oracle_sample_rays": int(m), "hit_miss_mismatches": int((ghit != rhit).sum())}
+        if oq == oracle.CLOSEST:
+            same = (g.view(np.uint32).reshape(-1, 4) == ref.view(np.uint32).reshape(-1, 4)).all(axis=1)
+            par["bit_exact_rays"] = int(same.sum())
+            par["differing_rays"] = int((~same).sum())   # allowed only on exact t ties
+        else:
+            bad = 0
+            for i in np.nonzero(ghit)[0][:2000]:
+                acc, t, u, v = oracle.eval_pair(osc, sample[i], int(g["prim"][i]), ok)
+                bad += not (acc and (t, u, v) == (g["t"][i], g["u"][i], g["v"][i]))
+            par["any_hit_checked"] = int(min(int(ghit.sum()), 2000))
+            par["any_hit_invalid"] = int(bad)
+        if scene is not None:
+            wh, _ = oracle.walk(b, rays.data, oq, ok, nthreads=cores)
+            par["walker_full_frame_bit_exact"] = bool(np.array_equal(wh.view(np.uint32),
+                                                                     gpu_hits.view(np.uint32)))
+        out["parity"] = par
     return out
 
 
