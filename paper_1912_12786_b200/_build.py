@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvsr.so")
-SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu", "lbvh.cu"]
-HEADERS = ["layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh"]
+SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu", "compound.cu", "prims.cu", "lbvh.cu"]
+HEADERS = ["layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh", "traverse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -48,7 +48,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     tmp = target + ".tmp"
     cmd = [nvcc(), "-O3", "-std=c++17", "-shared", "-Xcompiler", "-fPIC", "-Xcompiler",
            "-ffp-contract=off", *ARCH, "-lineinfo", "-fmad=false", "-prec-div=true",
-           "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"),
+           "-prec-sqrt=true", "-ftz=false", "-Xptxas", "-v", "-Xfatbin", "-compress-all", "-I", os.path.join(ROOT, "include"),
            *[f"-D{d}" for d in defines],
            "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES] + ["-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)

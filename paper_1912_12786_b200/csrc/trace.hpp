@@ -50,5 +50,7 @@ uint64_t launch_count();
 // Query on the scene's triangles as a plain list (no BVH); p.scene.tris / p.data.sides in
 // caller order (vsr_trace_primitives).
 cudaError_t launch_prims(int query, int isect, const TraceParams& p, cudaStream_t st);
+// Lists of BVHs and instances (p.list set; compound.cu), closest / any / multi.
+cudaError_t launch_compound(int query, int isect, const TraceParams& p, cudaStream_t st);
 
 }  // namespace vsr
