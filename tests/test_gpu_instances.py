@@ -152,3 +152,17 @@ def test_instances_multi_vs_walker(V, oracle_lib, k):
         if c is not None:
             cc = V.counts_to_numpy(c)
             assert np.array_equal(cc["boxes"], wc["boxes"]) and np.array_equal(cc["tris"], wc["tris"])
+
+
+def test_instanced_forest_full_frame_vs_walker(V, oracle_lib):
+    """The NEXT-2 bench workload at full size (1080p, 10k instances): ANY + alpha texture as the
+    bench times it, hits and instance ids bit-exact vs walker C on the whole frame."""
+    o = oracle_lib
+    models, bvh, m = W.instanced_forest()
+    rays = W.rays_for("C2").data
+    scenes, inst, top, bottoms = setup(V, models, bvh, m)
+    h, ii, _ = run(V, inst, rays, V.ANY, V.ALPHA_TEXTURE)
+    wh, wi, _ = o.walk_instances(top, top["records"], bottoms, rays, o.ANY, o.ALPHA_TEX)
+    assert np.array_equal(h.view(np.uint32), wh.view(np.uint32))
+    assert np.array_equal(ii, wi)
+    assert (h["prim"] != MISS).mean() > 0.3
