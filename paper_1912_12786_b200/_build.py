@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvsr.so")
-SOURCES = ["api.cpp", "bvh_build.cpp", "trace.cu", "compound.cu", "prims.cu", "lbvh.cu"]
-HEADERS = ["layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh", "traverse.cuh"]
+SOURCES = ["api.cpp", "api_trace.cpp", "api_compound.cpp", "bvh_build.cpp", "trace.cu", "compound.cu", "prims.cu", "lbvh.cu"]
+HEADERS = ["api_internal.hpp", "layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh", "traverse.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -5,26 +5,13 @@
 // flattened structure for multi-GPU replication, and the host dispatch that
 // maps (query, intersector) to ONE kernel instantiation per call (PAPER.md:
 // 74-78: the choice is made once, outside the innermost loop).
-#include <cuda_runtime.h>
+//
+// The trace entry points live in api_trace.cpp, lists and instancing in
+// api_compound.cpp; the state they share is in api_internal.hpp.
+#include "api_internal.hpp"
 
-#include <chrono>
-#include <cmath>
-#include <cstring>
-#include <atomic>
-#include <cstdlib>
-#include <mutex>
-#include <new>
-#include <string>
-#include <vector>
+namespace vsr_api {
 
-#include "../../include/vsr.h"
-#include "builder.hpp"
-#include "layout.hpp"
-#include "trace.hpp"
-
-using namespace vsr;
-
-namespace {
 thread_local std::string g_err;
 
 vsr_status fail(vsr_status s, const std::string& msg) {
@@ -35,27 +22,6 @@ vsr_status fail(vsr_status s, const std::string& msg) {
 vsr_status cuda_fail(cudaError_t e, const char* what) {
   return fail(VSR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
-
-struct DeviceGuard {
-  int prev = -1;
-  cudaError_t err = cudaSuccess;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) err = cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    cudaGetDevice(&cur);
-    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-  }
-};
-
-struct HostTexture {
-  uint32_t w, h;
-  std::vector<uint8_t> texels;    // alpha channel (A8)
-};
-
-bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // Copy `bytes` from src (host or device memory) into host memory.
 cudaError_t to_host(void* dst, const void* src, size_t bytes) {
@@ -68,134 +34,6 @@ cudaError_t to_host(void* dst, const void* src, size_t bytes) {
     return cudaSuccess;
   }
   return cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
-}
-
-}  // namespace
-
-// Per-stream scratch of the longest-first order pass, owned by whatever is
-// traced (scene, group, instances): reused in stream order behind an event, so
-// launches on other streams never share it and steady-state launches allocate
-// nothing.
-struct ScratchSet {
-  struct OrderScratch {
-    cudaStream_t st;
-    void* ptr;
-    size_t cap;
-    cudaEvent_t ev;   // last use; the next use waits on it (stream-ordered reuse)
-  };
-  std::mutex mu;
-  std::vector<OrderScratch> v;
-
-  void release() {
-    for (OrderScratch& o : v) {
-      cudaEventSynchronize(o.ev);
-      cudaFree(o.ptr);
-      cudaEventDestroy(o.ev);
-    }
-    v.clear();
-  }
-};
-
-struct vsr_scene {
-  int device = 0;
-  // ---- host copies (vsr_scene_create) ----
-  uint32_t num_tris_input = 0;
-  std::vector<float> vertices, texcoords;
-  std::vector<uint32_t> tri_tex;
-  std::vector<HostTexture> textures;
-  bool has_texcoords = false;
-  // ---- device state (vsr_bvh_build / vsr_scene_import) ----
-  bool built = false;
-  // host-only scenes (device == -1) keep the flattened arrays here instead
-  bool host_built = false;
-  HostBvh host_bvh;
-  std::vector<TexDesc> host_descs;
-  std::vector<uint8_t> host_pool;
-  DevScene dev{};
-  PairNode* d_nodes = nullptr;
-  Tri* d_tris = nullptr;
-  Side* d_sides = nullptr;
-  // caller-order copies for vsr_trace_primitives (built on first use)
-  std::mutex caller_mu;
-  Tri* d_tris_caller = nullptr;
-  Side* d_sides_caller = nullptr;
-  uint32_t num_caller = 0;
-  TexDesc* d_texdescs = nullptr;
-  uint8_t* d_texels = nullptr;
-  unsigned long long* d_counters = nullptr;   // persistent-kernel work counters
-  std::atomic<uint32_t> launch_seq{0};
-  uint64_t num_texels = 0;
-  vsr_stats stats{};
-  // ---- vsr_trace_host staging ----
-  std::mutex stage_mu;
-  static constexpr int kSlots = 3;
-  uint64_t stage_cap = 0;   // rays per slot
-  float4* d_in[kSlots] = {};
-  float4* d_out[kSlots] = {};
-  uint4* d_cnt[kSlots] = {};
-  cudaStream_t streams[kSlots] = {};
-  cudaEvent_t ev_start = nullptr;
-  cudaEvent_t ev_done[kSlots] = {};
-  void* fn_cache[4] = {};
-  bool fn_cached[4] = {};
-  ScratchSet scratch;   // per-stream scratch of the longest-first order pass
-
-  void free_device() {
-    cudaFree(d_nodes);
-    cudaFree(d_tris);
-    cudaFree(d_sides);
-    cudaFree(d_tris_caller);
-    cudaFree(d_sides_caller);
-    d_tris_caller = nullptr;
-    d_sides_caller = nullptr;
-    num_caller = 0;
-    cudaFree(d_texdescs);
-    cudaFree(d_texels);
-    cudaFree(d_counters);
-    d_nodes = nullptr;
-    d_tris = nullptr;
-    d_sides = nullptr;
-    d_texdescs = nullptr;
-    d_texels = nullptr;
-    d_counters = nullptr;
-    built = false;
-  }
-  void free_stage() {
-    for (int s = 0; s < kSlots; ++s) {
-      cudaFree(d_in[s]);
-      cudaFree(d_out[s]);
-      cudaFree(d_cnt[s]);
-      d_in[s] = nullptr;
-      d_out[s] = nullptr;
-      d_cnt[s] = nullptr;
-      if (streams[s]) cudaStreamDestroy(streams[s]);
-      if (ev_done[s]) cudaEventDestroy(ev_done[s]);
-      streams[s] = nullptr;
-      ev_done[s] = nullptr;
-    }
-    if (ev_start) cudaEventDestroy(ev_start);
-    ev_start = nullptr;
-    stage_cap = 0;
-  }
-};
-
-namespace {
-
-template <class T>
-vsr_status dev_upload(T** dst, const void* src, size_t count, const char* what) {
-  size_t bytes = count * sizeof(T);
-  if (bytes == 0) bytes = sizeof(T);   // keep a valid pointer for empty arrays
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(dst), bytes);
-  if (e != cudaSuccess) {
-    *dst = nullptr;
-    return e == cudaErrorMemoryAllocation ? fail(VSR_ERR_OOM, std::string("cudaMalloc ") + what)
-                                          : cuda_fail(e, what);
-  }
-  if (count) {
-    e = cudaMemcpy(*dst, src, count * sizeof(T), cudaMemcpyDefault);
-    if (e != cudaSuccess) return cuda_fail(e, what);
-  }
-  return VSR_OK;
 }
 
 // Upload flattened arrays (host or device sources) and fill scene->dev.
@@ -272,8 +110,6 @@ bool valid_isect(int k) {
     default: return false;
   }
 }
-
-bool needs_counts(int k) { return k == VSR_ISECT_COUNT || k == VSR_ISECT_COUNT_ALPHA_TEXTURE; }
 
 vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
                        const vsr_isect_params* params, TraceParams& p) {
@@ -366,7 +202,7 @@ unsigned long long* next_counter(vsr_scene* s) {
   return s->d_counters + 2 * (size_t)slot;
 }
 
-}  // namespace
+}  // namespace vsr_api
 
 extern "C" {
 
@@ -634,805 +470,9 @@ vsr_status vsr_bvh_build_ploc(vsr_scene* s, uint32_t max_leaf_size, uint32_t rad
   return build_on_gpu(s, max_leaf_size, (int)radius);
 }
 
-vsr_status vsr_trace_tiles(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint32_t tile_rays,
-                           uint32_t rank, uint32_t world, vsr_query query, vsr_isect isect,
-                           const vsr_isect_params* params, vsr_hit* d_hits, vsr_counts* d_counts,
-                           void* stream) {
-  g_err.clear();
-  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
-  TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
-  if (tile_rays == 0 || world == 0 || rank >= world)
-    return fail(VSR_ERR_INVALID_ARG, "need tile_rays > 0 and rank < world");
-  if (n % tile_rays) return fail(VSR_ERR_INVALID_ARG, "n must be a whole number of tiles");
-  if (n >= (1ull << 32) || (n / tile_rays) * (uint64_t)world * tile_rays >= (1ull << 40))
-    return fail(VSR_ERR_INVALID_ARG, "shard too large");
-  if (n == 0) return VSR_OK;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  p.out_tile = tile_rays;
-  p.out_rank = rank;
-  p.out_world = world;
-  p.sched = kSchedDirect;
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "tile trace launch");
-  return VSR_OK;
-}
-
-vsr_status vsr_device_alloc(uint64_t bytes, int device, void** d_ptr) {
-  g_err.clear();
-  if (!d_ptr || bytes == 0 || device < 0) return fail(VSR_ERR_INVALID_ARG, "bad allocation request");
-  DeviceGuard g(device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = cudaMalloc(d_ptr, bytes);
-  if (e != cudaSuccess) {
-    *d_ptr = nullptr;
-    return e == cudaErrorMemoryAllocation ? fail(VSR_ERR_OOM, "cudaMalloc") : cuda_fail(e, "cudaMalloc");
-  }
-  return VSR_OK;
-}
-
-vsr_status vsr_device_free(void* d_ptr, int device) {
-  g_err.clear();
-  if (!d_ptr) return VSR_OK;
-  DeviceGuard g(device);
-  cudaError_t e = cudaFree(d_ptr);
-  return e == cudaSuccess ? VSR_OK : cuda_fail(e, "cudaFree");
-}
-
-vsr_status vsr_ipc_handle(const void* d_ptr, void* handle64) {
-  g_err.clear();
-  if (!d_ptr || !handle64) return fail(VSR_ERR_INVALID_ARG, "NULL pointer or handle");
-  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle is 64 bytes");
-  cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
-  std::memcpy(handle64, &h, sizeof h);
-  return VSR_OK;
-}
-
-vsr_status vsr_ipc_open(const void* handle64, int device, void** d_ptr) {
-  g_err.clear();
-  if (!handle64 || !d_ptr || device < 0) return fail(VSR_ERR_INVALID_ARG, "bad IPC open request");
-  cudaIpcMemHandle_t h;
-  std::memcpy(&h, handle64, sizeof h);
-  DeviceGuard g(device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess);
-  if (e != cudaSuccess) {
-    *d_ptr = nullptr;
-    return cuda_fail(e, "cudaIpcOpenMemHandle");
-  }
-  return VSR_OK;
-}
-
-vsr_status vsr_ipc_close(void* d_ptr, int device) {
-  g_err.clear();
-  if (!d_ptr) return VSR_OK;
-  DeviceGuard g(device);
-  cudaError_t e = cudaIpcCloseMemHandle(d_ptr);
-  return e == cudaSuccess ? VSR_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
-}
-
 }  // extern "C"
 
-namespace {
-// The scene's triangles and sidecars in caller order (prim id order), for the
-// primitive-list query; ids the build excluded (degenerate) keep prim = ~0.
-vsr_status ensure_caller_order(vsr_scene* s) {
-  std::lock_guard<std::mutex> lk(s->caller_mu);
-  if (s->d_tris_caller) return VSR_OK;
-  const uint32_t m = s->dev.num_tris;
-  std::vector<Tri> tris(m);
-  std::vector<Side> sides(m);
-  cudaError_t e;
-  if ((e = cudaMemcpy(tris.data(), s->d_tris, sizeof(Tri) * m, cudaMemcpyDeviceToHost)) !=
-          cudaSuccess ||
-      (e = cudaMemcpy(sides.data(), s->d_sides, sizeof(Side) * m, cudaMemcpyDeviceToHost)) !=
-          cudaSuccess)
-    return cuda_fail(e, "caller-order copy");
-  uint32_t P = s->num_tris_input;
-  for (const Tri& t : tris) P = std::max(P, t.prim + 1u);
-  Tri none{};
-  none.prim = 0xFFFFFFFFu;
-  std::vector<Tri> ct(P, none);
-  std::vector<Side> cs(P, Side{});
-  for (uint32_t k = 0; k < m; ++k) {
-    ct[tris[k].prim] = tris[k];
-    cs[tris[k].prim] = sides[k];
-  }
-  vsr_status st;
-  if ((st = dev_upload(&s->d_tris_caller, ct.data(), P, "caller-order triangles")) != VSR_OK ||
-      (st = dev_upload(&s->d_sides_caller, cs.data(), P, "caller-order sidecars")) != VSR_OK)
-    return st;
-  s->num_caller = P;
-  return VSR_OK;
-}
-}  // namespace
-
 extern "C" {
-
-vsr_status vsr_trace_primitives(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
-                                vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                                vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
-  if ((int)isect >= 100 && valid_isect(isect))
-    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for primitive lists");
-  TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no triangles on the device: build first");
-  if (n == 0) return VSR_OK;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  if ((st = ensure_caller_order(s)) != VSR_OK) return st;
-  p.scene.tris = s->d_tris_caller;
-  p.scene.num_tris = s->num_caller;
-  p.data.sides = s->d_sides_caller;
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  cudaError_t e = launch_prims(query, isect, p, reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "primitive-list trace launch");
-  return VSR_OK;
-}
-
-vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query query,
-                             vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                             vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!s || !cam) return fail(VSR_ERR_INVALID_ARG, "NULL scene or camera");
-  if ((int)isect >= 100 && valid_isect(isect))
-    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided with in-kernel ray generation");
-  TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
-  if (cam->width == 0 || cam->height == 0 || cam->width % 8 || cam->height % 8)
-    return fail(VSR_ERR_INVALID_ARG, "width and height must be positive multiples of 8");
-  uint32_t side = 1;
-  while (side * side < cam->spp && side < 65536) ++side;
-  if (cam->spp == 0 || side * side != cam->spp)
-    return fail(VSR_ERR_INVALID_ARG, "spp must be a perfect square >= 1");
-  const double* vals[] = {cam->eye, cam->w, cam->u, cam->v};
-  for (const double* vv : vals)
-    for (int k = 0; k < 3; ++k)
-      if (!std::isfinite(vv[k])) return fail(VSR_ERR_INVALID_ARG, "non-finite camera");
-  if (!std::isfinite(cam->tan_half_vfov) || !std::isfinite(cam->aspect) || std::isnan(cam->tmin) ||
-      std::isnan(cam->tmax))
-    return fail(VSR_ERR_INVALID_ARG, "non-finite camera");
-  const uint64_t n = (uint64_t)cam->width * cam->height * cam->spp;
-  if (!d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL hits buffer");
-  if (!aligned16(d_hits)) return fail(VSR_ERR_INVALID_ARG, "hits buffer must be 16-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  p.gen = 1;
-  for (int k = 0; k < 3; ++k) {
-    p.cam.eye[k] = cam->eye[k];
-    p.cam.w[k] = cam->w[k];
-    p.cam.u[k] = cam->u[k];
-    p.cam.v[k] = cam->v[k];
-  }
-  p.cam.tan_half = cam->tan_half_vfov;
-  p.cam.aspect = cam->aspect;
-  p.cam.width = cam->width;
-  p.cam.height = cam->height;
-  p.cam.spp = cam->spp;
-  p.cam.seed = cam->jitter_seed;
-  p.cam.side = side;
-  p.cam.tmin = cam->tmin;
-  p.cam.tmax = cam->tmax;
-  p.sched = kSchedDirect;   // the persistent schedule reads a ray buffer
-  p.rays = nullptr;
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "pinhole trace launch");
-  return VSR_OK;
-}
-
-vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query query,
-                     vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                     vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
-  TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
-  if (n == 0) return VSR_OK;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  p.counter = next_counter(s);
-  cudaError_t e = launch_with_scratch(s->scratch, query, isect, p, reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "trace kernel launch");
-  return VSR_OK;
-}
-
-vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint32_t max_hits,
-                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                           uint32_t* d_num_hits, vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
-  if (max_hits < 1 || max_hits > 16) return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
-  if ((int)isect >= 100 && valid_isect(isect))
-    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for the multi-hit query");
-  TraceParams p;
-  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
-  if (n == 0) return VSR_OK;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
-    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  p.max_hits = (int)max_hits;
-  p.num_hits = d_num_hits;
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  p.counter = next_counter(s);
-  cudaError_t e = launch_with_scratch(s->scratch, 2 /* multi */, isect, p, reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "multi-hit trace launch");
-  return VSR_OK;
-}
-
-}  // extern "C"
-
-struct vsr_group {
-  int device = 0;
-  ScratchSet scratch;
-  std::vector<vsr_scene*> scenes;
-  DevScene* d_list = nullptr;
-  IsectData* d_data = nullptr;
-  float lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};   // union of the roots (order-pass proxy)
-};
-
-extern "C" {
-
-vsr_status vsr_group_create(vsr_scene* const* scenes, uint32_t count, vsr_group** out) {
-  g_err.clear();
-  if (!scenes || !out) return fail(VSR_ERR_INVALID_ARG, "NULL scenes or out");
-  *out = nullptr;
-  if (count < 1 || count > 1024) return fail(VSR_ERR_INVALID_ARG, "count must be in [1, 1024]");
-  for (uint32_t k = 0; k < count; ++k) {
-    if (!scenes[k]) return fail(VSR_ERR_INVALID_ARG, "NULL scene in list");
-    if (scenes[k]->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene in list");
-    if (!scenes[k]->built) return fail(VSR_ERR_NOT_BUILT, "scene " + std::to_string(k) + " not built");
-    if (scenes[k]->device != scenes[0]->device)
-      return fail(VSR_ERR_INVALID_ARG, "all scenes of a group must be on one device");
-  }
-  vsr_group* g = new (std::nothrow) vsr_group();
-  if (!g) return fail(VSR_ERR_OOM, "group allocation");
-  g->device = scenes[0]->device;
-  g->scenes.assign(scenes, scenes + count);
-  std::vector<DevScene> list(count);
-  std::vector<IsectData> data(count);
-  for (int a = 0; a < 3; ++a) {
-    g->lo[a] = INFINITY;
-    g->hi[a] = -INFINITY;
-  }
-  for (uint32_t k = 0; k < count; ++k) {
-    list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
-    for (int a = 0; a < 3; ++a) {
-      g->lo[a] = std::min(g->lo[a], scenes[k]->dev.root_lo[a]);
-      g->hi[a] = std::max(g->hi[a], scenes[k]->dev.root_hi[a]);
-    }
-  }
-  DeviceGuard dg(g->device);
-  cudaError_t e;
-  if ((e = cudaMalloc(&g->d_list, sizeof(DevScene) * count)) != cudaSuccess ||
-      (e = cudaMalloc(&g->d_data, sizeof(IsectData) * count)) != cudaSuccess ||
-      (e = cudaMemcpy(g->d_list, list.data(), sizeof(DevScene) * count, cudaMemcpyHostToDevice)) !=
-          cudaSuccess ||
-      (e = cudaMemcpy(g->d_data, data.data(), sizeof(IsectData) * count, cudaMemcpyHostToDevice)) !=
-          cudaSuccess) {
-    cudaFree(g->d_list);
-    cudaFree(g->d_data);
-    delete g;
-    return cuda_fail(e, "group upload");
-  }
-  *out = g;
-  return VSR_OK;
-}
-
-vsr_status vsr_group_destroy(vsr_group* g) {
-  g_err.clear();
-  if (!g) return VSR_OK;
-  {
-    DeviceGuard dg(g->device);
-    g->scratch.release();
-    cudaFree(g->d_list);
-    cudaFree(g->d_data);
-  }
-  delete g;
-  return VSR_OK;
-}
-
-}  // extern "C"
-
-namespace {
-// query: 0 closest, 1 any, 2 multi-hit (max_hits per ray, d_which max_hits per ray)
-vsr_status group_trace(vsr_group* g, const vsr_ray* d_rays, uint64_t n, int query,
-                       uint32_t max_hits, vsr_isect isect, const vsr_isect_params* params,
-                       vsr_hit* d_hits, uint32_t* d_num_hits, uint32_t* d_which,
-                       vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!g) return fail(VSR_ERR_INVALID_ARG, "NULL group");
-  if ((int)isect >= 100 && valid_isect(isect))
-    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for list queries");
-  if (query == 2 && (max_hits < 1 || max_hits > 16))
-    return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
-  TraceParams p;
-  vsr_status st = make_params(g->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
-                              isect, params, p);
-  if (st != VSR_OK) return st;
-  if (n == 0) return VSR_OK;
-  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
-    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
-  p.max_hits = (int)max_hits;
-  p.num_hits = d_num_hits;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (d_which && (reinterpret_cast<uintptr_t>(d_which) & 3u))
-    return fail(VSR_ERR_INVALID_ARG, "which buffer must be 4-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  for (int a = 0; a < 3; ++a) {   // the order pass's cost proxy uses the union of the roots
-    p.scene.root_lo[a] = g->lo[a];
-    p.scene.root_hi[a] = g->hi[a];
-  }
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  p.list = g->d_list;
-  p.list_data = g->d_data;
-  p.list_count = (uint32_t)g->scenes.size();
-  p.which = d_which;
-  DeviceGuard dg(g->device);
-  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(g->scratch, query, isect, p,
-                                      reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "list trace launch");
-  return VSR_OK;
-}
-}  // namespace
-
-extern "C" {
-
-vsr_status vsr_trace_group(vsr_group* g, const vsr_ray* d_rays, uint64_t n, vsr_query query,
-                           vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
-                           uint32_t* d_which, vsr_counts* d_counts, void* stream) {
-  if ((int)query != VSR_QUERY_CLOSEST && (int)query != VSR_QUERY_ANY) {
-    g_err.clear();
-    return fail(VSR_ERR_INVALID_ARG, "invalid query");
-  }
-  return group_trace(g, d_rays, n, (int)query, 0, isect, params, d_hits, nullptr, d_which,
-                     d_counts, stream);
-}
-
-vsr_status vsr_trace_group_multi(vsr_group* g, const vsr_ray* d_rays, uint64_t n,
-                                 uint32_t max_hits, vsr_isect isect,
-                                 const vsr_isect_params* params, vsr_hit* d_hits,
-                                 uint32_t* d_num_hits, uint32_t* d_which, vsr_counts* d_counts,
-                                 void* stream) {
-  return group_trace(g, d_rays, n, 2, max_hits, isect, params, d_hits, d_num_hits, d_which,
-                     d_counts, stream);
-}
-
-}  // extern "C"
-
-// Two-level instancing: the top level lives here; the instanced scenes are
-// referenced, not owned.
-struct vsr_instances {
-  int device = 0;
-  ScratchSet scratch;
-  std::vector<vsr_scene*> scenes;
-  HostBvh top;                       // host copy of the top-level nodes (export)
-  std::vector<Instance> records;     // leaf order (export)
-  DevScene dev{};                    // top level: nodes, root ref / box
-  PairNode* d_nodes = nullptr;
-  Instance* d_records = nullptr;
-  DevScene* d_list = nullptr;
-  IsectData* d_data = nullptr;
-};
-
-namespace {
-
-// World box of an instance: the 8 corners of the scene's (padded) root box
-// mapped by the fp64 inverse of [A | b], then padded by 2^-10 (diagonal +
-// max |coordinate|) and rounded outward (reading A27).  False if A is singular.
-bool instance_world_box(const float* m, const float* lo, const float* hi, float* out) {
-  const double a[3][3] = {{m[0], m[1], m[2]}, {m[4], m[5], m[6]}, {m[8], m[9], m[10]}};
-  const double bv[3] = {m[3], m[7], m[11]};
-  const double det = a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
-                     a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
-                     a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
-  if (!(std::fabs(det) > 1e-30) || !std::isfinite(det)) return false;
-  double inv[3][3];
-  inv[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) / det;
-  inv[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) / det;
-  inv[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) / det;
-  inv[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) / det;
-  inv[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) / det;
-  inv[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) / det;
-  inv[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) / det;
-  inv[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) / det;
-  inv[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) / det;
-  double wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int c = 0; c < 8; ++c) {
-    const double p[3] = {(c & 1) ? hi[0] : lo[0], (c & 2) ? hi[1] : lo[1], (c & 4) ? hi[2] : lo[2]};
-    for (int i = 0; i < 3; ++i) {
-      const double w = inv[i][0] * (p[0] - bv[0]) + inv[i][1] * (p[1] - bv[1]) +
-                       inv[i][2] * (p[2] - bv[2]);
-      wlo[i] = std::min(wlo[i], w);
-      whi[i] = std::max(whi[i], w);
-    }
-  }
-  double diag = 0.0, mag = 0.0;
-  for (int i = 0; i < 3; ++i) {
-    diag += (whi[i] - wlo[i]) * (whi[i] - wlo[i]);
-    mag = std::max(mag, std::max(std::fabs(wlo[i]), std::fabs(whi[i])));
-  }
-  const double pad = std::ldexp(std::sqrt(diag) + mag, -10);
-  for (int i = 0; i < 3; ++i) {
-    const double l = wlo[i] - pad, h = whi[i] + pad;
-    float lf = (float)l, hf = (float)h;
-    if ((double)lf > l) lf = std::nextafter(lf, -INFINITY);
-    if ((double)hf < h) hf = std::nextafter(hf, INFINITY);
-    if (!std::isfinite(lf) || !std::isfinite(hf)) return false;
-    out[i] = lf;
-    out[3 + i] = hf;
-  }
-  return true;
-}
-
-void free_instances(vsr_instances* I) {
-  if (I->device < 0) return;
-  DeviceGuard dg(I->device);
-  I->scratch.release();
-  cudaFree(I->d_nodes);
-  cudaFree(I->d_records);
-  cudaFree(I->d_list);
-  cudaFree(I->d_data);
-}
-
-}  // namespace
-
-extern "C" {
-
-vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
-                                const vsr_instance* instances, uint32_t num_instances,
-                                const vsr_build_params* params, vsr_instances** out) {
-  g_err.clear();
-  if (!scenes || !instances || !out) return fail(VSR_ERR_INVALID_ARG, "NULL scenes, instances or out");
-  *out = nullptr;
-  if (num_scenes < 1 || num_scenes > 1024)
-    return fail(VSR_ERR_INVALID_ARG, "num_scenes must be in [1, 1024]");
-  if (num_instances < 1 || num_instances > kMaxTris)
-    return fail(VSR_ERR_INVALID_ARG, "num_instances must be in [1, 2^26]");
-  for (uint32_t k = 0; k < num_scenes; ++k) {
-    if (!scenes[k]) return fail(VSR_ERR_INVALID_ARG, "NULL scene in list");
-    const bool host = scenes[k]->device < 0;   // host-only: build + export, no trace
-    if (!(host ? scenes[k]->host_built : scenes[k]->built))
-      return fail(VSR_ERR_NOT_BUILT, "scene " + std::to_string(k) + " not built");
-    if (scenes[k]->device != scenes[0]->device)
-      return fail(VSR_ERR_INVALID_ARG, "all scenes must be on one device");
-  }
-  vsr_build_params prm{1u, 16u, 1.0f, 1.0f};
-  if (params) prm = *params;
-  if (prm.max_leaf_size < 1 || prm.max_leaf_size > kMaxLeafSize || prm.sah_bins < 2 ||
-      prm.sah_bins > 256 || !(prm.traversal_cost >= 0.0f) || !(prm.intersection_cost > 0.0f))
-    return fail(VSR_ERR_INVALID_ARG, "invalid build params");
-  std::vector<float> boxes(6 * (size_t)num_instances);
-  for (uint32_t i = 0; i < num_instances; ++i) {
-    const vsr_instance& in = instances[i];
-    if (in.bvh >= num_scenes)
-      return fail(VSR_ERR_INVALID_ARG, "instance " + std::to_string(i) + ": bvh index out of range");
-    for (float x : in.object_from_world)
-      if (!std::isfinite(x))
-        return fail(VSR_ERR_INVALID_ARG, "instance " + std::to_string(i) + ": non-finite matrix");
-    const DevScene& d = scenes[in.bvh]->dev;
-    if (!instance_world_box(in.object_from_world, d.root_lo, d.root_hi, boxes.data() + 6 * (size_t)i))
-      return fail(VSR_ERR_INVALID_ARG, "instance " + std::to_string(i) + ": singular matrix");
-  }
-  vsr_instances* I = new (std::nothrow) vsr_instances();
-  if (!I) return fail(VSR_ERR_OOM, "instances allocation");
-  I->device = scenes[0]->device;
-  I->scenes.assign(scenes, scenes + num_scenes);
-  std::vector<uint32_t> order;
-  std::string err;
-  vsr_status st = build_top(boxes.data(), num_instances, prm, I->top, order, err);
-  if (st != VSR_OK) {
-    delete I;
-    return fail(st, err);
-  }
-  I->records.resize(num_instances);
-  for (uint32_t k = 0; k < num_instances; ++k) {
-    const vsr_instance& in = instances[order[k]];
-    Instance& r = I->records[k];
-    std::memcpy(r.m, in.object_from_world, sizeof r.m);
-    r.bvh = in.bvh;
-    r.index = order[k];
-    r.pad[0] = r.pad[1] = 0;
-  }
-  const size_t nn = I->top.nodes.size();
-  I->dev = DevScene{};
-  I->dev.root_ref = I->top.root_ref;
-  for (int a = 0; a < 3; ++a) {
-    I->dev.root_lo[a] = I->top.root_lo[a];
-    I->dev.root_hi[a] = I->top.root_hi[a];
-  }
-  I->dev.num_nodes = (uint32_t)nn;
-  I->dev.num_tris = num_instances;
-  if (I->device < 0) {   // host-only: nothing to upload
-    *out = I;
-    return VSR_OK;
-  }
-  std::vector<DevScene> list(num_scenes);
-  std::vector<IsectData> data(num_scenes);
-  for (uint32_t k = 0; k < num_scenes; ++k) {
-    list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
-  }
-  DeviceGuard dg(I->device);
-  cudaError_t e;
-  if ((nn && (e = cudaMalloc(&I->d_nodes, nn * sizeof(PairNode))) != cudaSuccess) ||
-      (e = cudaMalloc(&I->d_records, num_instances * sizeof(Instance))) != cudaSuccess ||
-      (e = cudaMalloc(&I->d_list, sizeof(DevScene) * num_scenes)) != cudaSuccess ||
-      (e = cudaMalloc(&I->d_data, sizeof(IsectData) * num_scenes)) != cudaSuccess ||
-      (nn && (e = cudaMemcpy(I->d_nodes, I->top.nodes.data(), nn * sizeof(PairNode),
-                             cudaMemcpyHostToDevice)) != cudaSuccess) ||
-      (e = cudaMemcpy(I->d_records, I->records.data(), num_instances * sizeof(Instance),
-                      cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemcpy(I->d_list, list.data(), sizeof(DevScene) * num_scenes,
-                      cudaMemcpyHostToDevice)) != cudaSuccess ||
-      (e = cudaMemcpy(I->d_data, data.data(), sizeof(IsectData) * num_scenes,
-                      cudaMemcpyHostToDevice)) != cudaSuccess) {
-    free_instances(I);
-    delete I;
-    return cuda_fail(e, "instances upload");
-  }
-  I->dev.nodes = I->d_nodes;
-  *out = I;
-  return VSR_OK;
-}
-
-vsr_status vsr_instances_destroy(vsr_instances* I) {
-  g_err.clear();
-  if (!I) return VSR_OK;
-  free_instances(I);
-  delete I;
-  return VSR_OK;
-}
-
-vsr_status vsr_instances_export(const vsr_instances* I, vsr_instances_view* v) {
-  g_err.clear();
-  if (!I || !v) return fail(VSR_ERR_INVALID_ARG, "NULL instances or view");
-  v->root_ref = I->top.root_ref;
-  for (int a = 0; a < 3; ++a) {
-    v->root_lo[a] = I->top.root_lo[a];
-    v->root_hi[a] = I->top.root_hi[a];
-  }
-  v->num_nodes = (uint32_t)I->top.nodes.size();
-  v->num_instances = (uint32_t)I->records.size();
-  v->max_depth = I->top.max_depth;
-  if (v->nodes && !I->top.nodes.empty())
-    std::memcpy(v->nodes, I->top.nodes.data(), I->top.nodes.size() * sizeof(PairNode));
-  if (v->records) std::memcpy(v->records, I->records.data(), I->records.size() * sizeof(Instance));
-  return VSR_OK;
-}
-
-}  // extern "C"
-
-namespace {
-vsr_status instances_trace(vsr_instances* I, const vsr_ray* d_rays, uint64_t n, int query,
-                           uint32_t max_hits, vsr_isect isect, const vsr_isect_params* params,
-                           vsr_hit* d_hits, uint32_t* d_num_hits, uint32_t* d_inst,
-                           vsr_counts* d_counts, void* stream) {
-  g_err.clear();
-  if (!I) return fail(VSR_ERR_INVALID_ARG, "NULL instances");
-  if ((int)isect >= 100 && valid_isect(isect))
-    return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for instanced queries");
-  if (query == 2 && (max_hits < 1 || max_hits > 16))
-    return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
-  TraceParams p;
-  vsr_status st = make_params(I->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
-                              isect, params, p);
-  if (st != VSR_OK) return st;
-  if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
-    return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");
-  p.max_hits = (int)max_hits;
-  p.num_hits = d_num_hits;
-  if (I->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only instances cannot be traced");
-  if (n == 0) return VSR_OK;
-  if (!d_rays || !d_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  if (!aligned16(d_rays) || !aligned16(d_hits))
-    return fail(VSR_ERR_INVALID_ARG, "rays/hits buffers must be 16-byte aligned");
-  if (d_inst && (reinterpret_cast<uintptr_t>(d_inst) & 3u))
-    return fail(VSR_ERR_INVALID_ARG, "instance buffer must be 4-byte aligned");
-  if (needs_counts(isect)) {
-    if (!d_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs a counts buffer");
-    if (!aligned16(d_counts)) return fail(VSR_ERR_INVALID_ARG, "counts buffer not 16-B aligned");
-  }
-  p.scene = I->dev;   // top level (the order pass's cost proxy uses its root box)
-  p.rays = reinterpret_cast<const float4*>(d_rays);
-  p.hits = reinterpret_cast<float4*>(d_hits);
-  p.counts = reinterpret_cast<uint4*>(d_counts);
-  p.n = n;
-  p.list = I->d_list;
-  p.list_data = I->d_data;
-  p.list_count = (uint32_t)I->scenes.size();
-  p.instances = I->d_records;
-  p.which = d_inst;
-  DeviceGuard dg(I->device);
-  if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");
-  cudaError_t e = launch_with_scratch(I->scratch, query, isect, p,
-                                      reinterpret_cast<cudaStream_t>(stream));
-  if (e != cudaSuccess) return cuda_fail(e, "instanced trace launch");
-  return VSR_OK;
-}
-}  // namespace
-
-extern "C" {
-
-vsr_status vsr_trace_instances(vsr_instances* I, const vsr_ray* d_rays, uint64_t n,
-                               vsr_query query, vsr_isect isect, const vsr_isect_params* params,
-                               vsr_hit* d_hits, uint32_t* d_inst, vsr_counts* d_counts,
-                               void* stream) {
-  if ((int)query != VSR_QUERY_CLOSEST && (int)query != VSR_QUERY_ANY) {
-    g_err.clear();
-    return fail(VSR_ERR_INVALID_ARG, "invalid query");
-  }
-  return instances_trace(I, d_rays, n, (int)query, 0, isect, params, d_hits, nullptr, d_inst,
-                         d_counts, stream);
-}
-
-vsr_status vsr_trace_instances_multi(vsr_instances* I, const vsr_ray* d_rays, uint64_t n,
-                                     uint32_t max_hits, vsr_isect isect,
-                                     const vsr_isect_params* params, vsr_hit* d_hits,
-                                     uint32_t* d_num_hits, uint32_t* d_inst,
-                                     vsr_counts* d_counts, void* stream) {
-  return instances_trace(I, d_rays, n, 2, max_hits, isect, params, d_hits, d_num_hits, d_inst,
-                         d_counts, stream);
-}
-
-vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_query query,
-                          vsr_isect isect, const vsr_isect_params* params, vsr_hit* h_hits,
-                          vsr_counts* h_counts, void* stream) {
-  g_err.clear();
-  if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
-  TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
-  if (st != VSR_OK) return st;
-  if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
-  if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
-  if (n == 0) return VSR_OK;
-  if (!h_rays || !h_hits) return fail(VSR_ERR_INVALID_ARG, "NULL rays or hits buffer");
-  const bool cnt = needs_counts(isect);
-  if (cnt && !h_counts) return fail(VSR_ERR_INVALID_ARG, "COUNT intersector needs counts");
-  std::lock_guard<std::mutex> lk(s->stage_mu);
-  DeviceGuard g(s->device);
-  if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  // Chunked pipeline over kSlots streams: chunk c's H2D copy, kernel and D2H
-  // copy run on stream c % kSlots, so copies of one chunk overlap the kernel
-  // of another (copy engines and SMs work concurrently).
-  const char* ec = std::getenv("VSR_HOST_CHUNKS");   // tuning knob: chunks per call
-  // 4 chunks measured best on C2 (2/4/8/16/32: 1.64/1.44/1.51/1.61/1.81 ms per frame)
-  const uint64_t nchunks = ec ? std::max(1, std::atoi(ec)) : 4;
-  const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(65536, (n + nchunks - 1) / nchunks));
-  cudaError_t e;
-  if (s->stage_cap < chunk || (cnt && !s->d_cnt[0])) {
-    s->free_stage();
-    for (int k = 0; k < vsr_scene::kSlots; ++k) {
-      if ((e = cudaMalloc(&s->d_in[k], chunk * 32)) != cudaSuccess ||
-          (e = cudaMalloc(&s->d_out[k], chunk * 16)) != cudaSuccess ||
-          (e = cudaMalloc(&s->d_cnt[k], chunk * 16)) != cudaSuccess ||
-          (e = cudaStreamCreateWithFlags(&s->streams[k], cudaStreamNonBlocking)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&s->ev_done[k], cudaEventDisableTiming)) != cudaSuccess) {
-        s->free_stage();
-        return cuda_fail(e, "staging allocation");
-      }
-    }
-    if ((e = cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming)) != cudaSuccess)
-      return cuda_fail(e, "event");
-    s->stage_cap = chunk;
-  }
-  cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
-  if ((e = cudaEventRecord(s->ev_start, user)) != cudaSuccess) return cuda_fail(e, "event");
-  for (int k = 0; k < vsr_scene::kSlots; ++k)
-    if ((e = cudaStreamWaitEvent(s->streams[k], s->ev_start, 0)) != cudaSuccess)
-      return cuda_fail(e, "stream wait");
-  const char* src = reinterpret_cast<const char*>(h_rays);
-  char* dst = reinterpret_cast<char*>(h_hits);
-  char* cdst = reinterpret_cast<char*>(h_counts);
-  uint64_t c = 0;
-  for (uint64_t b = 0; b < n; b += chunk, ++c) {
-    const int k = (int)(c % vsr_scene::kSlots);
-    const uint64_t m = std::min(chunk, n - b);
-    cudaStream_t ss = s->streams[k];
-    if ((e = cudaMemcpyAsync(s->d_in[k], src + b * 32, m * 32, cudaMemcpyHostToDevice, ss)) !=
-        cudaSuccess)
-      return cuda_fail(e, "H2D rays");
-    p.rays = s->d_in[k];
-    p.hits = s->d_out[k];
-    p.counts = s->d_cnt[k];
-    p.n = m;
-    p.counter = next_counter(s);
-    if ((e = launch_with_scratch(s->scratch, query, isect, p, ss)) != cudaSuccess)
-      return cuda_fail(e, "trace launch");
-    if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
-        cudaSuccess)
-      return cuda_fail(e, "D2H hits");
-    if (cnt && (e = cudaMemcpyAsync(cdst + b * 16, s->d_cnt[k], m * 16, cudaMemcpyDeviceToHost,
-                                    ss)) != cudaSuccess)
-      return cuda_fail(e, "D2H counts");
-  }
-  for (int k = 0; k < vsr_scene::kSlots; ++k) {
-    if ((e = cudaEventRecord(s->ev_done[k], s->streams[k])) != cudaSuccess)
-      return cuda_fail(e, "event");
-    if ((e = cudaStreamWaitEvent(user, s->ev_done[k], 0)) != cudaSuccess)
-      return cuda_fail(e, "stream wait");
-  }
-  if ((e = cudaStreamSynchronize(user)) != cudaSuccess) return cuda_fail(e, "trace (host)");
-  return VSR_OK;
-}
 
 vsr_status vsr_destroy(vsr_scene* s) {
   g_err.clear();

@@ -1,5 +1,5 @@
 """ASan + UBSan runs of everything that executes on the host: the oracle
-(oracle.c, walker.c) and the product's host code (api.cpp, bvh_build.cpp: scene creation,
+(oracle.c, walker.c) and the product's host code (api*.cpp, bvh_build.cpp: scene creation,
 validation, SAH build, export/import, instances top level) — each built with
 -fsanitize=address,undefined into /tmp and driven by the CPU test suites under LD_PRELOAD.
 (compute-sanitizer for the kernels is closed on this GPU pool.)
@@ -12,6 +12,8 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_1912_12786_b200 import _build  # noqa: E402  (source list only; nothing is built)
 SAN = ["-fsanitize=address", "-fsanitize=undefined", "-fno-omit-frame-pointer"]
 
 
@@ -33,8 +35,7 @@ def main():
                    "-fPIC", "-Xcompiler", "-ffp-contract=off", *xc, "-gencode",
                    "arch=compute_100a,code=sm_100a", "-fmad=false", "-prec-div=true",
                    "-prec-sqrt=true", "-ftz=false", "-I", "include", "-o", lib,
-                   "paper_1912_12786_b200/csrc/api.cpp", "paper_1912_12786_b200/csrc/bvh_build.cpp",
-                   "paper_1912_12786_b200/csrc/trace.cu", "paper_1912_12786_b200/csrc/lbvh.cu",
+                   *[os.path.join("paper_1912_12786_b200/csrc", f) for f in _build.SOURCES],
                    "-lcudart"])
     assert rc == 0, out
     pre = " ".join(subprocess.check_output(["gcc", f"-print-file-name={n}"], text=True).strip()
