@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TracePara
   if (id < p.n) {
     I isect = make_isect<I>(p);
     Trav T;
-    float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
+    StackEntry<Q> stack[kMaxStack];   // (ref[, tnear]); depth <= 64 guaranteed by build/import
     const bool go = start_ray<GEN>(p, T, isect, id);
     // warp-uniform octant: specialised slab test when all live lanes agree
     const unsigned live = __activemask();
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel_persistent(cons
   unsigned long long* ctr = p.counter;
   I isect = make_isect<I>(p);
   Trav T;
-  float2 stack[kMaxStack];   // (ref bits, tnear); depth <= 64 guaranteed by build/import
+  StackEntry<Q> stack[kMaxStack];   // (ref[, tnear]); depth <= 64 guaranteed by build/import
   bool active = false;
   // warp-uniform work queue: [next, next + left) of the warp's claimed chunk
   unsigned long long next = 0;

@@ -69,6 +69,31 @@ __device__ __forceinline__ bool pop(Trav& T, const float2* stack) {
   return false;
 }
 
+// Any-hit stack: ref only.  Until the first accepted hit ends an any-hit query
+// its tmax never shrinks, and every entry was pushed with tnear <= that tmax,
+// so the cull above can never fire: dropping tnear changes no result (reading
+// A14) and halves the stack's local-memory traffic.
+__device__ __forceinline__ bool pop(Trav& T, const uint32_t* stack) {
+  if (T.sp == 0) return false;
+  T.cur = stack[--T.sp];
+  return true;
+}
+
+__device__ __forceinline__ void push(float2* stack, int sp, uint32_t ref, float tn) {
+  stack[sp] = make_float2(__uint_as_float(ref), tn);
+}
+__device__ __forceinline__ void push(uint32_t* stack, int sp, uint32_t ref, float) {
+  stack[sp] = ref;
+}
+
+// Stack entry of a query: any-hit keeps refs only (see pop above).
+#ifndef VSR_ANY_REFSTACK
+#define VSR_ANY_REFSTACK 1
+#endif
+template <int Q>
+using StackEntry =
+    typename std::conditional<Q == kAny && VSR_ANY_REFSTACK, uint32_t, float2>::type;
+
 // ---- fused primary-ray generation (vsr.h vsr_pinhole) ----
 // Ray `id` of the (8x8 tile, sample, y, x) order, computed with exactly the
 // fp64 operations of the input recipe (workloads.pinhole_rays)
@@ -152,8 +177,8 @@ __device__ __forceinline__ void prefetch_ref(const DevScene& S, uint32_t ref) {
 #endif
 }
 
-template <int OCT, class I>
-__device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, float2* stack) {
+template <int OCT, class I, class SE>
+__device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, SE* stack) {
   while (!(T.cur & kLeafBit)) {
     const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
     const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2), nr = __ldg(np + 3);
@@ -168,7 +193,7 @@ __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, fl
     const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
     if (h.h0 && h.h1) {
       const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
-      stack[T.sp] = make_float2(__uint_as_float(swap ? r0 : r1), swap ? h.tn0 : h.tn1);
+      push(stack, T.sp, swap ? r0 : r1, swap ? h.tn0 : h.tn1);
       ++T.sp;
       T.cur = swap ? r1 : r0;
     } else if (h.h0) {
@@ -247,8 +272,8 @@ __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb
 
 // One outer iteration of "while ray not terminated": descend
 // to the next leaf, run its primitives, pop.  Returns true when the ray is done.
-template <int Q, int OCT, class I>
-__device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, float2* stack) {
+template <int Q, int OCT, class I, class SE>
+__device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, SE* stack) {
   NoMulti none;
   if (!descend<OCT>(S, T, isect, stack)) return true;
   if (leaf<Q>(S, T, isect, none)) return true;
@@ -258,8 +283,8 @@ __device__ __forceinline__ bool advance(const DevScene& S, Trav& T, I& isect, fl
 // Whole traversal of one ray.  `oct` is warp-uniform: 0..7 if every lane of
 // the warp has that octant (primary rays: all but the centre row/column
 // tiles), 8 otherwise; the switch is taken once per leaf, uniformly.
-template <class I>
-__device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect, float2* stack,
+template <class I, class SE>
+__device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect, SE* stack,
                                             int oct) {
   switch (oct) {
     case 0: return descend<0>(S, T, isect, stack);
@@ -274,8 +299,8 @@ __device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect
   }
 }
 
-template <int Q, class I, class M = NoMulti>
-__device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, float2* stack,
+template <int Q, class I, class SE, class M = NoMulti>
+__device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, SE* stack,
                                          int oct, M& mb) {
   for (;;) {
     const bool at_leaf = descend_oct(S, T, isect, stack, oct);
