@@ -79,11 +79,11 @@ __device__ __forceinline__ bool pop(Trav& T, const uint32_t* stack) {
   return true;
 }
 
-__device__ __forceinline__ void push(float2* stack, int sp, uint32_t ref, float tn) {
-  stack[sp] = make_float2(__uint_as_float(ref), tn);
+__device__ __forceinline__ void push(Trav& T, float2* stack, uint32_t ref, float tn) {
+  stack[T.sp++] = make_float2(__uint_as_float(ref), tn);
 }
-__device__ __forceinline__ void push(uint32_t* stack, int sp, uint32_t ref, float) {
-  stack[sp] = ref;
+__device__ __forceinline__ void push(Trav& T, uint32_t* stack, uint32_t ref, float) {
+  stack[T.sp++] = ref;
 }
 
 // Stack entry of a query: any-hit keeps refs only (see pop above).
@@ -193,8 +193,7 @@ __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, SE
     const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
     if (h.h0 && h.h1) {
       const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
-      push(stack, T.sp, swap ? r0 : r1, swap ? h.tn0 : h.tn1);
-      ++T.sp;
+      push(T, stack, swap ? r0 : r1, swap ? h.tn0 : h.tn1);
       T.cur = swap ? r1 : r0;
     } else if (h.h0) {
       T.cur = r0;
