@@ -5,6 +5,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -111,14 +112,17 @@ struct vsr_scene {
   vsr_stats stats{};
   // ---- vsr_trace_host staging ----
   std::mutex stage_mu;
-  static constexpr int kSlots = 3;
+  // ring of kSlots chunk buffers; copy-in, trace and copy-out each on their
+  // own stream, chained per chunk by events (vsr_trace_host)
+  static constexpr int kSlots = 8;
   uint64_t stage_cap = 0;   // rays per slot
+  bool stage_counts = false;
   float4* d_in[kSlots] = {};
   float4* d_out[kSlots] = {};
   uint4* d_cnt[kSlots] = {};
-  cudaStream_t streams[kSlots] = {};
+  cudaStream_t s_in = nullptr, s_run = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr;
-  cudaEvent_t ev_done[kSlots] = {};
+  cudaEvent_t ev_in[kSlots] = {}, ev_run[kSlots] = {}, ev_out[kSlots] = {};
   void* fn_cache[4] = {};
   bool fn_cached[4] = {};
   vsr_api::ScratchSet scratch;   // per-stream scratch of the longest-first order pass
@@ -144,6 +148,7 @@ struct vsr_scene {
     built = false;
   }
   void free_stage() {
+    if (s_out) cudaStreamSynchronize(s_out);
     for (int s = 0; s < kSlots; ++s) {
       cudaFree(d_in[s]);
       cudaFree(d_out[s]);
@@ -151,13 +156,18 @@ struct vsr_scene {
       d_in[s] = nullptr;
       d_out[s] = nullptr;
       d_cnt[s] = nullptr;
-      if (streams[s]) cudaStreamDestroy(streams[s]);
-      if (ev_done[s]) cudaEventDestroy(ev_done[s]);
-      streams[s] = nullptr;
-      ev_done[s] = nullptr;
+      for (cudaEvent_t* ev : {&ev_in[s], &ev_run[s], &ev_out[s]}) {
+        if (*ev) cudaEventDestroy(*ev);
+        *ev = nullptr;
+      }
+    }
+    for (cudaStream_t* st : {&s_in, &s_run, &s_out}) {
+      if (*st) cudaStreamDestroy(*st);
+      *st = nullptr;
     }
     if (ev_start) cudaEventDestroy(ev_start);
     ev_start = nullptr;
+    stage_counts = false;
     stage_cap = 0;
   }
 };

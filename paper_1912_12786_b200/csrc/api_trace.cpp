@@ -322,34 +322,44 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
   std::lock_guard<std::mutex> lk(s->stage_mu);
   DeviceGuard g(s->device);
   if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-  // Chunked pipeline over kSlots streams: chunk c's H2D copy, kernel and D2H
-  // copy run on stream c % kSlots, so copies of one chunk overlap the kernel
-  // of another (copy engines and SMs work concurrently).
-  const char* ec = std::getenv("VSR_HOST_CHUNKS");   // tuning knob: chunks per call
-  // 4 chunks measured best on C2 (2/4/8/16/32: 1.64/1.44/1.51/1.61/1.81 ms per frame)
-  const uint64_t nchunks = ec ? std::max(1, std::atoi(ec)) : 4;
-  const uint64_t chunk = std::min<uint64_t>(n, std::max<uint64_t>(65536, (n + nchunks - 1) / nchunks));
+  // Chunked pipeline on three streams: every chunk's H2D copy goes on s_in,
+  // its trace on s_run, its D2H copy on s_out, chained by per-chunk events, so
+  // the host-to-device copy engine never waits behind a device-to-host copy or
+  // a kernel (both directions of the link and the SMs work at once). Chunk
+  // buffers form a ring of kSlots; a slot's next H2D waits for its last D2H.
+  // Chunk size: n/8 within [256 Ki, 1 Mi] rays (measured, profiles/r01_tuning.md).
+  const char* ec = std::getenv("VSR_HOST_CHUNK");   // tuning knob: rays per chunk
+  const uint64_t want = ec ? std::max<uint64_t>(4096, std::strtoull(ec, nullptr, 10))
+                           : std::min<uint64_t>(1u << 20, std::max<uint64_t>(1u << 18, n / 8));
+  const uint64_t chunk = std::min<uint64_t>(n, want);
   cudaError_t e;
-  if (s->stage_cap < chunk || (cnt && !s->d_cnt[0])) {
+  if (s->stage_cap < chunk || (cnt && !s->stage_counts)) {
     s->free_stage();
-    for (int k = 0; k < vsr_scene::kSlots; ++k) {
-      if ((e = cudaMalloc(&s->d_in[k], chunk * 32)) != cudaSuccess ||
-          (e = cudaMalloc(&s->d_out[k], chunk * 16)) != cudaSuccess ||
-          (e = cudaMalloc(&s->d_cnt[k], chunk * 16)) != cudaSuccess ||
-          (e = cudaStreamCreateWithFlags(&s->streams[k], cudaStreamNonBlocking)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&s->ev_done[k], cudaEventDisableTiming)) != cudaSuccess) {
-        s->free_stage();
-        return cuda_fail(e, "staging allocation");
-      }
+    bool ok = true;
+    for (int k = 0; k < vsr_scene::kSlots && ok; ++k) {
+      ok = (e = cudaMalloc(&s->d_in[k], chunk * 32)) == cudaSuccess &&
+           (e = cudaMalloc(&s->d_out[k], chunk * 16)) == cudaSuccess &&
+           (!cnt || (e = cudaMalloc(&s->d_cnt[k], chunk * 16)) == cudaSuccess) &&
+           (e = cudaEventCreateWithFlags(&s->ev_in[k], cudaEventDisableTiming)) == cudaSuccess &&
+           (e = cudaEventCreateWithFlags(&s->ev_run[k], cudaEventDisableTiming)) == cudaSuccess &&
+           (e = cudaEventCreateWithFlags(&s->ev_out[k], cudaEventDisableTiming)) == cudaSuccess;
     }
-    if ((e = cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming)) != cudaSuccess)
-      return cuda_fail(e, "event");
+    ok = ok && (e = cudaStreamCreateWithFlags(&s->s_in, cudaStreamNonBlocking)) == cudaSuccess &&
+         (e = cudaStreamCreateWithFlags(&s->s_run, cudaStreamNonBlocking)) == cudaSuccess &&
+         (e = cudaStreamCreateWithFlags(&s->s_out, cudaStreamNonBlocking)) == cudaSuccess &&
+         (e = cudaEventCreateWithFlags(&s->ev_start, cudaEventDisableTiming)) == cudaSuccess;
+    if (!ok) {
+      s->free_stage();
+      return e == cudaErrorMemoryAllocation ? fail(VSR_ERR_OOM, "staging allocation")
+                                            : cuda_fail(e, "staging allocation");
+    }
     s->stage_cap = chunk;
+    s->stage_counts = cnt;
   }
   cudaStream_t user = reinterpret_cast<cudaStream_t>(stream);
   if ((e = cudaEventRecord(s->ev_start, user)) != cudaSuccess) return cuda_fail(e, "event");
-  for (int k = 0; k < vsr_scene::kSlots; ++k)
-    if ((e = cudaStreamWaitEvent(s->streams[k], s->ev_start, 0)) != cudaSuccess)
+  for (cudaStream_t ss : {s->s_in, s->s_run, s->s_out})
+    if ((e = cudaStreamWaitEvent(ss, s->ev_start, 0)) != cudaSuccess)
       return cuda_fail(e, "stream wait");
   const char* src = reinterpret_cast<const char*>(h_rays);
   char* dst = reinterpret_cast<char*>(h_hits);
@@ -358,30 +368,38 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
   for (uint64_t b = 0; b < n; b += chunk, ++c) {
     const int k = (int)(c % vsr_scene::kSlots);
     const uint64_t m = std::min(chunk, n - b);
-    cudaStream_t ss = s->streams[k];
-    if ((e = cudaMemcpyAsync(s->d_in[k], src + b * 32, m * 32, cudaMemcpyHostToDevice, ss)) !=
-        cudaSuccess)
+    if (c >= (uint64_t)vsr_scene::kSlots &&   // the slot's previous hits are out
+        (e = cudaStreamWaitEvent(s->s_in, s->ev_out[k], 0)) != cudaSuccess)
+      return cuda_fail(e, "stream wait");
+    if ((e = cudaMemcpyAsync(s->d_in[k], src + b * 32, m * 32, cudaMemcpyHostToDevice,
+                             s->s_in)) != cudaSuccess)
       return cuda_fail(e, "H2D rays");
+    if ((e = cudaEventRecord(s->ev_in[k], s->s_in)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s->s_run, s->ev_in[k], 0)) != cudaSuccess)
+      return cuda_fail(e, "event");
     p.rays = s->d_in[k];
     p.hits = s->d_out[k];
     p.counts = s->d_cnt[k];
     p.n = m;
     p.counter = next_counter(s);
-    if ((e = launch_with_scratch(s->scratch, query, isect, p, ss)) != cudaSuccess)
+    if ((e = launch_with_scratch(s->scratch, query, isect, p, s->s_run)) != cudaSuccess)
       return cuda_fail(e, "trace launch");
-    if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost, ss)) !=
-        cudaSuccess)
+    if ((e = cudaEventRecord(s->ev_run[k], s->s_run)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(s->s_out, s->ev_run[k], 0)) != cudaSuccess)
+      return cuda_fail(e, "event");
+    if ((e = cudaMemcpyAsync(dst + b * 16, s->d_out[k], m * 16, cudaMemcpyDeviceToHost,
+                             s->s_out)) != cudaSuccess)
       return cuda_fail(e, "D2H hits");
     if (cnt && (e = cudaMemcpyAsync(cdst + b * 16, s->d_cnt[k], m * 16, cudaMemcpyDeviceToHost,
-                                    ss)) != cudaSuccess)
+                                    s->s_out)) != cudaSuccess)
       return cuda_fail(e, "D2H counts");
-  }
-  for (int k = 0; k < vsr_scene::kSlots; ++k) {
-    if ((e = cudaEventRecord(s->ev_done[k], s->streams[k])) != cudaSuccess)
+    if ((e = cudaEventRecord(s->ev_out[k], s->s_out)) != cudaSuccess)
       return cuda_fail(e, "event");
-    if ((e = cudaStreamWaitEvent(user, s->ev_done[k], 0)) != cudaSuccess)
-      return cuda_fail(e, "stream wait");
   }
+  // s_out's last copy follows every trace and every H2D (event chains)
+  if ((e = cudaEventRecord(s->ev_start, s->s_out)) != cudaSuccess ||
+      (e = cudaStreamWaitEvent(user, s->ev_start, 0)) != cudaSuccess)
+    return cuda_fail(e, "stream wait");
   if ((e = cudaStreamSynchronize(user)) != cudaSuccess) return cuda_fail(e, "trace (host)");
   return VSR_OK;
 }
