@@ -111,8 +111,56 @@ bool valid_isect(int k) {
   }
 }
 
+// The scene's 1-bit alpha plane for a_min (alpha_keep_bits), built on first
+// use; nullptr when the textures are not 32-aligned, the cache is full or the
+// build fails (the A8 path then runs: same results). VSR_ALPHA_BITS=0 disables.
+const uint32_t* alpha_plane(vsr_scene* s, uint32_t a_min) {
+  const char* eb = std::getenv("VSR_ALPHA_BITS");
+  if ((eb && std::strcmp(eb, "0") == 0) || !s->built || s->dev.num_textures == 0) return nullptr;
+  std::lock_guard<std::mutex> lk(s->bits_mu);
+  const uint32_t nt = s->dev.num_textures;
+  for (int i = 0; i < s->num_planes; ++i)
+    if (s->plane_amin[i] == a_min) return s->d_planes[i];
+  if (s->bits_ok < 0) {   // once per device state: are all textures 32-aligned?
+    std::vector<TexDesc> descs(nt);
+    if (cudaMemcpy(descs.data(), s->d_texdescs, nt * sizeof(TexDesc), cudaMemcpyDeviceToHost) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    bool ok = s->num_texels % 32 == 0;
+    uint64_t max_words = 0;
+    for (const TexDesc& d : descs) {
+      ok = ok && d.w % 32 == 0 && d.h % 32 == 0 && d.offset % 1024 == 0;
+      max_words = std::max<uint64_t>(max_words, (uint64_t)d.w * d.h / 32);
+    }
+    s->bits_ok = ok ? 1 : 0;
+    s->bits_max_words = max_words;
+  }
+  if (s->bits_ok != 1) return nullptr;
+  const uint64_t max_words = s->bits_max_words;
+  if (s->num_planes == vsr_scene::kMaxPlanes) return nullptr;
+  DeviceGuard g(s->device);
+  uint32_t* d = nullptr;
+  cudaStream_t st = nullptr;
+  bool ok = cudaMalloc(&d, s->num_texels / 8) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
+            build_alpha_bits(s->d_texdescs, nt, s->d_texels, a_min, d, max_words, st) ==
+                cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess;
+  if (st) cudaStreamDestroy(st);
+  if (!ok) {
+    cudaGetLastError();
+    cudaFree(d);
+    return nullptr;
+  }
+  s->plane_amin[s->num_planes] = a_min;
+  s->d_planes[s->num_planes++] = d;
+  return d;
+}
+
 vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
-                       const vsr_isect_params* params, TraceParams& p) {
+                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits) {
   if (query != VSR_QUERY_CLOSEST && query != VSR_QUERY_ANY)
     return fail(VSR_ERR_INVALID_ARG, "invalid query");
   if (!valid_isect(isect)) return fail(VSR_ERR_INVALID_ARG, "invalid intersector kind");
@@ -129,6 +177,7 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.data.a_min = alpha_min_a8(ip.alpha_threshold);
   p.data.fm = (float)ip.checker_freq;
   p.data.thr = ip.alpha_threshold;
+  if (alpha_bits && isect == VSR_ISECT_ALPHA_TEXTURE) p.data.bits = alpha_plane(s, p.data.a_min);
   int kind = 0;
   if (isect >= 200) kind = isect - 200;
   else if (isect >= 100) kind = isect - 100;

@@ -90,7 +90,7 @@ vsr_status group_trace(vsr_group* g, const vsr_ray* d_rays, uint64_t n, int quer
     return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
   TraceParams p;
   vsr_status st = make_params(g->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
-                              isect, params, p);
+                              isect, params, p, false);
   if (st != VSR_OK) return st;
   if (n == 0) return VSR_OK;
   if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
@@ -367,7 +367,7 @@ vsr_status instances_trace(vsr_instances* I, const vsr_ray* d_rays, uint64_t n, 
     return fail(VSR_ERR_INVALID_ARG, "max_hits must be in [1, 16]");
   TraceParams p;
   vsr_status st = make_params(I->scenes[0], query == 2 ? VSR_QUERY_CLOSEST : (vsr_query)query,
-                              isect, params, p);
+                              isect, params, p, false);
   if (st != VSR_OK) return st;
   if (d_num_hits && (reinterpret_cast<uintptr_t>(d_num_hits) & 3u))
     return fail(VSR_ERR_INVALID_ARG, "num_hits buffer must be 4-byte aligned");

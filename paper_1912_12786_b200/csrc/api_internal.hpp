@@ -126,6 +126,15 @@ struct vsr_scene {
   void* fn_cache[4] = {};
   bool fn_cached[4] = {};
   vsr_api::ScratchSet scratch;   // per-stream scratch of the longest-first order pass
+  // 1-bit alpha planes, one per threshold seen (cache; built on first use, kept until
+  // the device state is freed; at most kMaxPlanes, then the A8 path is used)
+  static constexpr int kMaxPlanes = 8;
+  std::mutex bits_mu;
+  int bits_ok = -1;   // -1 unknown, 0 textures not 32-aligned, 1 eligible
+  uint64_t bits_max_words = 0;   // largest texture's W*H/32
+  uint32_t plane_amin[kMaxPlanes] = {};
+  uint32_t* d_planes[kMaxPlanes] = {};
+  int num_planes = 0;
 
   void free_device() {
     cudaFree(d_nodes);
@@ -145,6 +154,9 @@ struct vsr_scene {
     d_texdescs = nullptr;
     d_texels = nullptr;
     d_counters = nullptr;
+    for (int i = 0; i < num_planes; ++i) cudaFree(d_planes[i]);
+    num_planes = 0;
+    bits_ok = -1;
     built = false;
   }
   void free_stage() {
@@ -203,8 +215,10 @@ bool valid_isect(int k);
 inline bool needs_counts(int k) {
   return k == VSR_ISECT_COUNT || k == VSR_ISECT_COUNT_ALPHA_TEXTURE;
 }
+// alpha_bits: look up (or build) the scene's 1-bit alpha plane for ALPHA_TEXTURE
+// (plain per-scene traces; compounds keep the A8 path)
 vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
-                       const vsr_isect_params* params, TraceParams& p);
+                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits = true);
 
 // Launch with the owner's scratch for stream `st` (see the definition).
 cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TraceParams& p,

@@ -328,6 +328,29 @@ __device__ __forceinline__ bool alpha_keep(const IsectData& d, uint32_t k, float
                     u, v);
 }
 
+// The same decision read from the 1-bit plane (a8 >= a_min) of the call's
+// threshold (SURVEY.md §8(f) NEXT-4 "1-bit alpha plane"): texel (i, j) of a
+// texture whose A8 texels start at offset O is bit (i & 31) of word
+// O/32 + ((j/32)·(W/32) + i/32)·32 + (j & 31) — 32×32-texel tiles of 32 words,
+// one 128-B line each, so rays landing near each other on a billboard share
+// lines in both directions. Same (i, j) as alpha_keep, same comparison made
+// once per texel on the host's behalf: identical results. Only used when every
+// texture's W and H are multiples of 32 (O is then a multiple of 1024).
+__device__ __forceinline__ bool alpha_keep_bits(const IsectData& d, uint32_t k, float u, float v) {
+  const float4 s0 = ldg4(d.sides + k);
+  const float4 s1 = ldg4(reinterpret_cast<const float4*>(d.sides + k) + 1);
+  const float w = (1.0f - u) - v;
+  const float s = (w * s0.x + u * s0.z) + v * s1.x;
+  const float t = (w * s0.y + u * s0.w) + v * s1.y;
+  const uint32_t dims = __float_as_uint(s1.w);
+  const uint32_t tw = (dims & 0xFFFFu) + 1u, th = (dims >> 16) + 1u;
+  const uint32_t i = wrap_texel(s, tw);
+  const uint32_t j = wrap_texel(t, th);
+  const uint32_t word = (__float_as_uint(s1.z) >> 5) +
+                        ((((j >> 5) * (tw >> 5) + (i >> 5)) << 5) | (j & 31u));
+  return (__ldg(d.bits + word) >> (i & 31u)) & 1u;
+}
+
 // NEXT-4 variant (reading A28): bilinear tex2D of the A8 plane, texel centres at
 // (i+.5)/W, wrap; the filtered alpha is compared with the threshold itself.
 // |texcoord| <= 1024 and W <= 65536 keep every index within int32
@@ -396,6 +419,22 @@ struct alpha_texture_intersector : basic_intersector<alpha_texture_intersector> 
   }
   __device__ __forceinline__ void reset() { n_lookups = 0; }
   __device__ __forceinline__ uint32_t lookups() const { return n_lookups; }
+};
+
+// ALPHA_TEXTURE through the 1-bit plane (alpha_keep_bits): chosen by the host
+// for VSR_ISECT_ALPHA_TEXTURE when the scene's plane for the call's threshold
+// exists; otherwise alpha_texture_intersector reads the A8 plane.
+struct alpha_bits_intersector : alpha_texture_intersector {
+  using alpha_texture_intersector::operator();
+  __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
+                                                   float tmax_cur) {
+    hit_record hr = intersect(r, t, k, tmax_cur);
+    if (hr.hit) {
+      ++n_lookups;
+      hr.hit &= alpha_keep_bits(d, hr.k, hr.u, hr.v);
+    }
+    return hr;
+  }
 };
 
 // ALPHA_PROCEDURAL.

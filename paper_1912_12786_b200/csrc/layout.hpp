@@ -90,6 +90,8 @@ struct IsectData {
   uint32_t a_min;   // smallest a8 with (float)a8/255.0f >= threshold (exact, host-derived)
   float fm;         // checker frequency M as float
   float thr;        // the alpha threshold itself (bilinear variant compares filtered alpha)
+  const uint32_t* bits;   // 1-bit plane of (a8 >= a_min) for this a_min, or null (see
+                          // alpha_keep_bits; built per threshold by the host, a cache)
 };
 
 // Pinhole camera for rays generated inside the trace kernel (vsr.h vsr_pinhole;

@@ -25,6 +25,7 @@
 // Build: -gencode arch=compute_100a,code=sm_100a -fmad=false (IEEE fp32
 // contract).
 
+#include <algorithm>
 #include <cstdio>
 #include <string>
 
@@ -333,7 +334,9 @@ cudaError_t dispatch_isect(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
     case VSR_ISECT_NONE: return launch<Q, no_intersector>(p, st);
     case VSR_ISECT_DEFAULT: return launch<Q, default_intersector>(p, st);
-    case VSR_ISECT_ALPHA_TEXTURE: return launch<Q, alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE:
+      return p.data.bits ? launch<Q, alpha_bits_intersector>(p, st)
+                         : launch<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch<Q, alpha_procedural_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch<Q, alpha_bilinear_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch<Q, alpha_procedural_uv_intersector>(p, st);
@@ -433,6 +436,33 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     if (e == cudaSuccess) e = f;
   }
   return e;
+}
+
+// 1-bit alpha plane of threshold a_min (see alpha_keep_bits): one thread per
+// output word = one 32-texel row segment of a 32x32 tile; blockIdx.y = texture.
+__global__ void __launch_bounds__(256) alpha_bits_kernel(const TexDesc* descs, const uint8_t* texels,
+                                                         uint32_t a_min, uint32_t* bits) {
+  const TexDesc td = descs[blockIdx.y];
+  const uint64_t words = (uint64_t)td.w * td.h / 32;
+  const uint32_t tiles_x = td.w / 32;
+  for (uint64_t w = blockIdx.x * 256ull + threadIdx.x; w < words; w += gridDim.x * 256ull) {
+    const uint64_t tile = w >> 5;
+    const uint64_t y = (tile / tiles_x) * 32 + (w & 31u), x0 = (tile % tiles_x) * 32;
+    const uint8_t* row = texels + td.offset + y * td.w + x0;
+    uint32_t m = 0;
+    for (int c = 0; c < 32; ++c) m |= (uint32_t)(row[c] >= a_min) << c;
+    bits[(td.offset >> 5) + w] = m;
+  }
+}
+
+cudaError_t build_alpha_bits(const TexDesc* d_descs, uint32_t num_textures, const uint8_t* texels,
+                             uint32_t a_min, uint32_t* d_bits, uint64_t max_words,
+                             cudaStream_t st) {
+  if (num_textures == 0) return cudaSuccess;
+  const unsigned gx = (unsigned)std::min<uint64_t>(4096, (max_words + 255) / 256);
+  alpha_bits_kernel<<<dim3(gx ? gx : 1, num_textures), 256, 0, st>>>(d_descs, texels, a_min, d_bits);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
 }
 
 std::atomic<uint64_t>& launch_counter() {

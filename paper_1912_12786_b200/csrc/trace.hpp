@@ -43,6 +43,11 @@ struct TraceParams {
 };
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);
+// 1-bit alpha plane of threshold a_min into d_bits (texel_count / 32 words; every
+// texture's W, H multiples of 32); max_words = the largest texture's W*H/32.
+cudaError_t build_alpha_bits(const TexDesc* d_descs, uint32_t num_textures, const uint8_t* texels,
+                             uint32_t a_min, uint32_t* d_bits, uint64_t max_words,
+                             cudaStream_t st);
 size_t order_scratch_bytes(uint64_t n);
 void set_kernel_events(void* start, void* stop);
 cudaError_t filter_fn_pointer(int kind, void** out);
