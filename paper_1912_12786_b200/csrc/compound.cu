@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const Trac
   if (id >= p.n) return;
   I isect = make_isect<I>(p);
   Trav T;
-  float2 stack[kMaxStack];
+  StackEntry<Q> stack[kMaxStack];   // any-hit: refs only (traverse.cuh pop)
   start_ray(p, T, isect, id);   // loads the ray; p.scene is element 0 (root test redone below)
   isect.reset();
   const unsigned live = __activemask();
@@ -70,9 +70,9 @@ __device__ __forceinline__ void to_object(const float4 r0, const float4 r1, cons
 
 // Instance k of the current top-level leaf.  Returns true when the query is
 // finished (any-hit accepted a primitive).
-template <int Q, class I>
+template <int Q, class I, class SE>
 __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& isect,
-                                              float2* stack, uint32_t k, uint32_t& hit_in) {
+                                              SE* stack, uint32_t k, uint32_t& hit_in) {
   const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
   const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
   const uint32_t b = __float_as_uint(ex.x);
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_kernel(const
   if (id >= p.n) return;
   I isect = make_isect<I>(p);
   Trav T;
-  float2 stack[kInstStack];   // top level below, the current instance's entries above
+  StackEntry<Q> stack[kInstStack];   // top level below, the current instance's entries above
   uint32_t hit_in = 0xFFFFFFFFu;
   if (start_ray(p, T, isect, id)) {   // world ray; counted test of the top-level root box
     const int woct = warp_octant(T.r);
