@@ -273,7 +273,7 @@ vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   if ((int)isect >= 100 && valid_isect(isect))
     return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for the multi-hit query");
   TraceParams p;
-  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p, false);
+  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");

@@ -318,7 +318,9 @@ cudaError_t dispatch_multi(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
     case VSR_ISECT_NONE: return launch_multi<no_intersector>(p, st);
     case VSR_ISECT_DEFAULT: return launch_multi<default_intersector>(p, st);
-    case VSR_ISECT_ALPHA_TEXTURE: return launch_multi<alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE:
+      return p.data.bits ? launch_multi<alpha_bits_intersector>(p, st)
+                         : launch_multi<alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_multi<alpha_procedural_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_multi<alpha_bilinear_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_multi<alpha_procedural_uv_intersector>(p, st);

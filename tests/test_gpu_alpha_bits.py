@@ -73,3 +73,21 @@ def test_bits_plane_on_the_forest(V, oracle_lib, monkeypatch):
             assert hb.tobytes() == ha.tobytes()
             wh, _ = o.walk(b, rays.data, oq, o.ALPHA_TEX, alpha_threshold=thr)
             assert np.array_equal(hb.view(np.uint32), wh.view(np.uint32)), (thr, q)
+
+
+@pytest.mark.parametrize("k", [4, 16])
+def test_bits_plane_multi_hit(V, oracle_lib, monkeypatch, k):
+    """vsr_trace_multi reads the plane too: same bytes as the A8 path (which test_gpu_multi.py
+    checks against walker C)."""
+    o = oracle_lib
+    sc = soup_with([(64, 96), (32, 160), (128, 128)], seed=95)
+    rays = W.random_rays(8011, seed=96).data
+    s = V.Scene.from_workload(sc).build()
+    r = torch.from_numpy(np.ascontiguousarray(rays, np.float32)).cuda()
+    out = {}
+    for bits in (True, False):
+        monkeypatch.setenv("VSR_ALPHA_BITS", "1" if bits else "0")
+        h, nh, _ = s.trace_multi(r, k, V.ALPHA_TEXTURE, alpha_threshold=0.5)
+        torch.cuda.synchronize()
+        out[bits] = (h.cpu().numpy().tobytes(), nh.cpu().numpy().tobytes())
+    assert out[True] == out[False]
