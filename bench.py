@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--query", default="any", choices=["closest", "any"])
     ap.add_argument("--isect", default="alpha_texture")
     ap.add_argument("--no-variants", action="store_true", help="skip the C3 intersector sweep")
+    ap.add_argument("--graph", type=int, default=0,
+                    help="1: replay the headline trace call from a CUDA graph each step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--max-leaf", type=int, default=2, help="BVH build: max triangles per leaf")
@@ -251,6 +253,7 @@ def run_own(args):
     multi_hits = None
 
     def trace(kind, query=q):
+        sh = torch.cuda.current_stream().cuda_stream   # the capture stream under a CUDA graph
         if query == "multi":   # multi-hit query, k = 4
             scene.trace_multi(d_rays, multi_k, kind, hits=multi_hits, num_hits=multi_n,
                               counts=counts, stream=sh)
@@ -264,11 +267,20 @@ def run_own(args):
             src = hits if backend == "nccl" else hits.cpu()
             shard.gather_hits(src, rays.n, tile_rays, dist, out=gathered, reorder=False)
 
-    def timed(kind, steps, warmup, query=q, sampler=None, kernel_ms=None):
+    def timed(kind, steps, warmup, query=q, sampler=None, kernel_ms=None, graph=False):
         for _ in range(warmup):
             flush_l2()
             trace(kind, query)
         torch.cuda.synchronize()
+        g = None
+        per_call = 0
+        if graph:   # one trace call (order pass + trace kernel) captured once, replayed per step
+            g = torch.cuda.CUDAGraph()
+            c0 = vsr.launch_count()
+            with torch.cuda.graph(g):
+                trace(kind, query)
+            per_call = vsr.launch_count() - c0
+            torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(steps)]
         kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -287,11 +299,14 @@ def run_own(args):
                 if kev:   # events around the trace kernel alone (after the order pass)
                     vsr.set_kernel_events(*kev[i])
                 a.record(stream)
-                trace(kind, query)
+                if g is not None:
+                    g.replay()
+                else:
+                    trace(kind, query)
                 b.record(stream)
             torch.cuda.synchronize()
         vsr.set_kernel_events(None, None)
-        launches = vsr.launch_count() - l0
+        launches = vsr.launch_count() - l0 + per_call * (steps if g is not None else 0)
         if world > 1:
             dist.barrier()
         ms = [a.elapsed_time(b) for a, b in evs]
@@ -301,7 +316,8 @@ def run_own(args):
 
     # ---- headline ----
     sampler = ClockSampler(local)
-    ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler)
+    use_graph = args.graph and not tiles
+    ms, launches = timed(isect, args.steps, args.warmup, sampler=sampler, graph=use_graph)
     torch.cuda.synchronize()
     head_hits = vsr.hits_to_numpy(hits).copy() if not tiles else None   # for the parity summary
     # the trace kernel alone (roofline denominator), in a second pass: events
@@ -513,6 +529,8 @@ def run_own(args):
                        "bvh": f"binned SAH, {args.sah_bins} bins, max_leaf {args.max_leaf}",
                        "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
                        "l2": "flushed before every timed step (read of a 256 MiB buffer, outside the events)",
+                       "launch": ("one CUDA-graph replay of the trace call per step" if use_graph
+                                  else "eager vsr_trace call per step"),
                        "parallelism": (f"one frame's 8x8 tiles dealt round-robin over {world} rank(s), "
                                        + ("each trace kernel stores its hits into rank 0's frame "
                                           "(CUDA IPC, NVLink peer stores; vsr_trace_tiles)" if fused

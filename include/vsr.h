@@ -195,7 +195,13 @@ vsr_status vsr_bvh_build_ploc(vsr_scene* scene, uint32_t max_leaf_size, uint32_t
  * d_rays / d_hits / d_counts are caller-owned DEVICE buffers on the scene's device,
  * 16-B aligned.  d_counts is required iff isect is COUNT or COUNT_ALPHA_TEXTURE.
  * Asynchronous: results are valid once the stream is synchronised.  n = 0 is a
- * no-op.  Errors: INVALID_ARG, NOT_BUILT, CUDA (launch failure). */
+ * no-op.  Errors: INVALID_ARG, NOT_BUILT, CUDA (launch failure).
+ * CUDA graphs: the call may be captured (stream capture) and the graph replayed; a captured
+ * call takes its order-pass scratch as graph memory nodes (stream-ordered allocation), and
+ * ALPHA_TEXTURE uses the scene's 1-bit alpha plane only if one call with the same threshold ran
+ * before capture (otherwise the A8 path is captured; same results).  The same holds for
+ * vsr_trace_multi, vsr_trace_pinhole, vsr_trace_tiles and the list / instance traces;
+ * vsr_trace_host synchronises and cannot be captured. */
 vsr_status vsr_trace(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_query query,
                      vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
                      vsr_counts* d_counts, void* stream);

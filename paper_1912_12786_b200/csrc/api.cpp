@@ -114,13 +114,20 @@ bool valid_isect(int k) {
 // The scene's 1-bit alpha plane for a_min (alpha_keep_bits), built on first
 // use; nullptr when the textures are not 32-aligned, the cache is full or the
 // build fails (the A8 path then runs: same results). VSR_ALPHA_BITS=0 disables.
-const uint32_t* alpha_plane(vsr_scene* s, uint32_t a_min) {
+const uint32_t* alpha_plane(vsr_scene* s, uint32_t a_min, void* stream) {
   const char* eb = std::getenv("VSR_ALPHA_BITS");
   if ((eb && std::strcmp(eb, "0") == 0) || !s->built || s->dev.num_textures == 0) return nullptr;
   std::lock_guard<std::mutex> lk(s->bits_mu);
   const uint32_t nt = s->dev.num_textures;
   for (int i = 0; i < s->num_planes; ++i)
     if (s->plane_amin[i] == a_min) return s->d_planes[i];
+  // no synchronous build while the call's stream is being captured into a graph
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(stream), &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (cs != cudaStreamCaptureStatusNone) return nullptr;
   if (s->bits_ok < 0) {   // once per device state: are all textures 32-aligned?
     std::vector<TexDesc> descs(nt);
     if (cudaMemcpy(descs.data(), s->d_texdescs, nt * sizeof(TexDesc), cudaMemcpyDeviceToHost) !=
@@ -160,7 +167,8 @@ const uint32_t* alpha_plane(vsr_scene* s, uint32_t a_min) {
 }
 
 vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
-                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits) {
+                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits,
+                       void* stream) {
   if (query != VSR_QUERY_CLOSEST && query != VSR_QUERY_ANY)
     return fail(VSR_ERR_INVALID_ARG, "invalid query");
   if (!valid_isect(isect)) return fail(VSR_ERR_INVALID_ARG, "invalid intersector kind");
@@ -177,7 +185,8 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.data.a_min = alpha_min_a8(ip.alpha_threshold);
   p.data.fm = (float)ip.checker_freq;
   p.data.thr = ip.alpha_threshold;
-  if (alpha_bits && isect == VSR_ISECT_ALPHA_TEXTURE) p.data.bits = alpha_plane(s, p.data.a_min);
+  if (alpha_bits && isect == VSR_ISECT_ALPHA_TEXTURE)
+    p.data.bits = alpha_plane(s, p.data.a_min, stream);
   int kind = 0;
   if (isect >= 200) kind = isect - 200;
   else if (isect >= 100) kind = isect - 100;
@@ -210,6 +219,16 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
 // Caller holds no lock; n must be the launch's ray count.
 cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TraceParams& p,
                                 cudaStream_t st) {
+  // Under stream capture (CUDA graphs) the owner's event-guarded scratch is not
+  // used: launch_trace takes a stream-ordered allocation instead, which the
+  // graph records as its own memory nodes, so every replay has private scratch.
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) cudaGetLastError();
+  if (cs != cudaStreamCaptureStatusNone) {
+    p.order_scratch = nullptr;
+    p.order_scratch_bytes = 0;
+    return launch_trace(query, isect, p, st);
+  }
   std::lock_guard<std::mutex> lk(set.mu);
   const size_t bytes = order_scratch_bytes(p.n);
   ScratchSet::OrderScratch* o = nullptr;

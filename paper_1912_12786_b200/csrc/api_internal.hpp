@@ -217,8 +217,10 @@ inline bool needs_counts(int k) {
 }
 // alpha_bits: look up (or build) the scene's 1-bit alpha plane for ALPHA_TEXTURE
 // (plain per-scene traces; compounds keep the A8 path)
+// (stream: the call's stream — no plane is built while it is being captured)
 vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
-                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits = true);
+                       const vsr_isect_params* params, TraceParams& p, bool alpha_bits = true,
+                       void* stream = nullptr);
 
 // Launch with the owner's scratch for stream `st` (see the definition).
 cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TraceParams& p,

@@ -14,7 +14,7 @@ vsr_status vsr_trace_tiles(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   g_err.clear();
   if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
   TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
+  vsr_status st = make_params(s, query, isect, params, p, true, stream);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
@@ -182,7 +182,7 @@ vsr_status vsr_trace_pinhole(vsr_scene* s, const vsr_pinhole* cam, vsr_query que
   if ((int)isect >= 100 && valid_isect(isect))
     return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided with in-kernel ray generation");
   TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
+  vsr_status st = make_params(s, query, isect, params, p, true, stream);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
@@ -240,7 +240,7 @@ vsr_status vsr_trace(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_query 
   g_err.clear();
   if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
   TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
+  vsr_status st = make_params(s, query, isect, params, p, true, stream);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
@@ -273,7 +273,7 @@ vsr_status vsr_trace_multi(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, uint
   if ((int)isect >= 100 && valid_isect(isect))
     return fail(VSR_ERR_UNSUPPORTED, "run-time controls are not provided for the multi-hit query");
   TraceParams p;
-  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p);
+  vsr_status st = make_params(s, VSR_QUERY_CLOSEST, isect, params, p, true, stream);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
@@ -311,7 +311,7 @@ vsr_status vsr_trace_host(vsr_scene* s, const vsr_ray* h_rays, uint64_t n, vsr_q
   g_err.clear();
   if (!s) return fail(VSR_ERR_INVALID_ARG, "NULL scene");
   TraceParams p;
-  vsr_status st = make_params(s, query, isect, params, p);
+  vsr_status st = make_params(s, query, isect, params, p, true, stream);
   if (st != VSR_OK) return st;
   if (s->device < 0) return fail(VSR_ERR_UNSUPPORTED, "host-only scene (device -1) cannot be traced");
   if (!s->built) return fail(VSR_ERR_NOT_BUILT, "scene has no BVH: call vsr_bvh_build first");
