@@ -59,3 +59,41 @@ def test_many_streams_and_threads(V):
     for t in ts:
         t.join()
     assert not errors, errors
+
+
+def test_threads_building_alpha_planes(V, monkeypatch):
+    """Several threads, each with its own alpha threshold, trace concurrently while the scene
+    builds a 1-bit plane per new threshold (under its lock) — every result equals the A8 path's."""
+    sc, rays = W.config("C2", 480, 272)
+    scene = V.Scene.from_workload(sc).build()
+    d = torch.from_numpy(rays.data).cuda()
+    thrs = [0.05, 0.2, 0.4, 0.6, 0.8, 0.95]
+    monkeypatch.setenv("VSR_ALPHA_BITS", "0")
+    ref = {}
+    for t in thrs:
+        h, _ = scene.trace(d, V.ANY, V.ALPHA_TEXTURE, alpha_threshold=t)
+        torch.cuda.synchronize()
+        ref[t] = h.clone()
+    monkeypatch.setenv("VSR_ALPHA_BITS", "1")
+    errors = []
+
+    def worker(t):
+        try:
+            st = torch.cuda.Stream()
+            outs = []
+            for _ in range(6):
+                h = torch.empty((rays.n, 4), dtype=torch.float32, device="cuda")
+                scene.trace(d, V.ANY, V.ALPHA_TEXTURE, hits=h, stream=st, alpha_threshold=t)
+                outs.append(h)
+            st.synchronize()
+            if any(not torch.equal(h.view(torch.int32), ref[t].view(torch.int32)) for h in outs):
+                errors.append(f"threshold {t}: mismatch")
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(f"threshold {t}: {e!r}")
+
+    ts = [threading.Thread(target=worker, args=(t,)) for t in thrs]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
