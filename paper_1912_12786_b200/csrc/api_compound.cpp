@@ -3,9 +3,64 @@
 // (vsr_instances_*, vsr_trace_instances[_multi]; reading A27).
 #include "api_internal.hpp"
 
+namespace {
+
+// Per-element mask data carrying each element scene's 1-bit alpha plane for a
+// threshold (alpha_keep_bits), one device array per threshold seen (≤ 8).
+struct PlaneData {
+  std::mutex mu;
+  uint32_t a_min[vsr_scene::kMaxPlanes] = {};
+  IsectData* d[vsr_scene::kMaxPlanes] = {};
+  int n = 0;
+  void release() {
+    for (int i = 0; i < n; ++i) cudaFree(d[i]);
+    n = 0;
+  }
+};
+
+// All-or-nothing: the array for a_min when every element scene has (or can now
+// build) its plane, else nullptr (the A8 path runs). Nothing is allocated while
+// `stream` is being captured.
+const IsectData* compound_planes(PlaneData& pd, const std::vector<vsr_scene*>& scenes,
+                                 uint32_t a_min, void* stream) {
+  const char* eb = std::getenv("VSR_ALPHA_BITS");
+  if (eb && std::strcmp(eb, "0") == 0) return nullptr;
+  std::lock_guard<std::mutex> lk(pd.mu);
+  for (int i = 0; i < pd.n; ++i)
+    if (pd.a_min[i] == a_min) return pd.d[i];
+  if (pd.n == vsr_scene::kMaxPlanes) return nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(reinterpret_cast<cudaStream_t>(stream), &cs) != cudaSuccess ||
+      cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  std::vector<IsectData> data(scenes.size());
+  for (size_t k = 0; k < scenes.size(); ++k) {
+    const uint32_t* b = alpha_plane(scenes[k], a_min, stream);
+    if (!b) return nullptr;
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f,
+                        0.0f, b};
+  }
+  IsectData* d = nullptr;
+  if (cudaMalloc(&d, sizeof(IsectData) * data.size()) != cudaSuccess ||
+      cudaMemcpy(d, data.data(), sizeof(IsectData) * data.size(), cudaMemcpyHostToDevice) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(d);
+    return nullptr;
+  }
+  pd.a_min[pd.n] = a_min;
+  pd.d[pd.n++] = d;
+  return d;
+}
+
+}  // namespace
+
 struct vsr_group {
   int device = 0;
   ScratchSet scratch;
+  PlaneData planes;   // per-threshold mask data with the elements' 1-bit alpha planes
   std::vector<vsr_scene*> scenes;
   DevScene* d_list = nullptr;
   IsectData* d_data = nullptr;
@@ -67,6 +122,7 @@ vsr_status vsr_group_destroy(vsr_group* g) {
   {
     DeviceGuard dg(g->device);
     g->scratch.release();
+    g->planes.release();
     cudaFree(g->d_list);
     cudaFree(g->d_data);
   }
@@ -116,6 +172,11 @@ vsr_status group_trace(vsr_group* g, const vsr_ray* d_rays, uint64_t n, int quer
   p.n = n;
   p.list = g->d_list;
   p.list_data = g->d_data;
+  if (isect == VSR_ISECT_ALPHA_TEXTURE)
+    if (const IsectData* bd = compound_planes(g->planes, g->scenes, p.data.a_min, stream)) {
+      p.list_data = bd;
+      p.data.bits = alpha_plane(g->scenes[0], p.data.a_min, stream);   // cached: selects the kernel
+    }
   p.list_count = (uint32_t)g->scenes.size();
   p.which = d_which;
   DeviceGuard dg(g->device);
@@ -156,6 +217,7 @@ vsr_status vsr_trace_group_multi(vsr_group* g, const vsr_ray* d_rays, uint64_t n
 struct vsr_instances {
   int device = 0;
   ScratchSet scratch;
+  PlaneData planes;   // per-threshold mask data with the elements' 1-bit alpha planes
   std::vector<vsr_scene*> scenes;
   HostBvh top;                       // host copy of the top-level nodes (export)
   std::vector<Instance> records;     // leaf order (export)
@@ -220,6 +282,7 @@ void free_instances(vsr_instances* I) {
   if (I->device < 0) return;
   DeviceGuard dg(I->device);
   I->scratch.release();
+  I->planes.release();
   cudaFree(I->d_nodes);
   cudaFree(I->d_records);
   cudaFree(I->d_list);
@@ -391,6 +454,11 @@ vsr_status instances_trace(vsr_instances* I, const vsr_ray* d_rays, uint64_t n, 
   p.n = n;
   p.list = I->d_list;
   p.list_data = I->d_data;
+  if (isect == VSR_ISECT_ALPHA_TEXTURE)
+    if (const IsectData* bd = compound_planes(I->planes, I->scenes, p.data.a_min, stream)) {
+      p.list_data = bd;
+      p.data.bits = alpha_plane(I->scenes[0], p.data.a_min, stream);   // cached: selects the kernel
+    }
   p.list_count = (uint32_t)I->scenes.size();
   p.instances = I->d_records;
   p.which = d_inst;

@@ -226,6 +226,10 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
 cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TraceParams& p,
                                 cudaStream_t st);
 
+// The scene's 1-bit alpha plane for threshold a_min (built on first use, cached), or
+// nullptr (textures not 32-aligned, cache full, disabled, or `stream` capturing).
+const uint32_t* alpha_plane(vsr_scene* s, uint32_t a_min, void* stream);
+
 // A fresh work-counter slot per launch (self-reset by the launch's last warp).
 unsigned long long* next_counter(vsr_scene* s);
 

@@ -251,7 +251,9 @@ cudaError_t dispatch_compound_multi(int isect, const TraceParams& p, cudaStream_
   switch (isect) {
     case VSR_ISECT_NONE: return launch_compound_multi<no_intersector>(p, st);
     case VSR_ISECT_DEFAULT: return launch_compound_multi<default_intersector>(p, st);
-    case VSR_ISECT_ALPHA_TEXTURE: return launch_compound_multi<alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE:
+      return p.data.bits ? launch_compound_multi<alpha_bits_intersector>(p, st)
+                         : launch_compound_multi<alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_compound_multi<alpha_procedural_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_compound_multi<alpha_bilinear_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_compound_multi<alpha_procedural_uv_intersector>(p, st);
@@ -277,7 +279,9 @@ cudaError_t dispatch_inst(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
     case VSR_ISECT_NONE: return launch_inst<Q, no_intersector>(p, st);
     case VSR_ISECT_DEFAULT: return launch_inst<Q, default_intersector>(p, st);
-    case VSR_ISECT_ALPHA_TEXTURE: return launch_inst<Q, alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE:
+      return p.data.bits ? launch_inst<Q, alpha_bits_intersector>(p, st)
+                         : launch_inst<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_inst<Q, alpha_procedural_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_inst<Q, alpha_bilinear_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_inst<Q, alpha_procedural_uv_intersector>(p, st);
@@ -293,7 +297,9 @@ cudaError_t dispatch_list(int isect, const TraceParams& p, cudaStream_t st) {
   switch (isect) {
     case VSR_ISECT_NONE: return launch_list<Q, no_intersector>(p, st);
     case VSR_ISECT_DEFAULT: return launch_list<Q, default_intersector>(p, st);
-    case VSR_ISECT_ALPHA_TEXTURE: return launch_list<Q, alpha_texture_intersector>(p, st);
+    case VSR_ISECT_ALPHA_TEXTURE:
+      return p.data.bits ? launch_list<Q, alpha_bits_intersector>(p, st)
+                         : launch_list<Q, alpha_texture_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL: return launch_list<Q, alpha_procedural_intersector>(p, st);
     case VSR_ISECT_ALPHA_TEXTURE_BILINEAR: return launch_list<Q, alpha_bilinear_intersector>(p, st);
     case VSR_ISECT_ALPHA_PROCEDURAL_UV: return launch_list<Q, alpha_procedural_uv_intersector>(p, st);

@@ -401,6 +401,7 @@ __device__ __forceinline__ void bind_scene_data(I& isect, const IsectData& d) {
     isect.d.sides = d.sides;   // threshold / checker frequency stay the call's
     isect.d.descs = d.descs;
     isect.d.texels = d.texels;
+    isect.d.bits = d.bits;     // the element's 1-bit plane (alpha_bits_intersector)
   } else {
     (void)d;
   }

@@ -91,3 +91,40 @@ def test_bits_plane_multi_hit(V, oracle_lib, monkeypatch, k):
         torch.cuda.synchronize()
         out[bits] = (h.cpu().numpy().tobytes(), nh.cpu().numpy().tobytes())
     assert out[True] == out[False]
+
+
+def test_bits_plane_in_lists_and_instances(V, monkeypatch):
+    """Lists and instances read every element's plane (all elements 32-aligned), or all fall back
+    to A8 when one is not; bytes equal to the A8 path in both cases, any / closest / multi-hit."""
+    aligned = [soup_with([(64, 96), (32, 160)], seed=97), soup_with([(128, 64)], seed=98)]
+    mixed = aligned[:1] + [soup_with([(24, 40)], seed=99)]
+    models, ibvh, imat = W.instanced_forest(n_instances=400, n_models=2, cards=16)
+    rays = W.random_rays(6007, seed=100).data
+    r = torch.from_numpy(np.ascontiguousarray(rays, np.float32)).cuda()
+    _, frame = W.config("C2", 240, 136)
+    fr = torch.from_numpy(frame.data).cuda()
+    for elems in (aligned, mixed):
+        scenes = [V.Scene.from_workload(e).build() for e in elems]
+        grp = V.Group(scenes)
+        out = {}
+        for bits in (True, False):
+            monkeypatch.setenv("VSR_ALPHA_BITS", "1" if bits else "0")
+            res = []
+            for q in (V.ANY, V.CLOSEST):
+                h, w, _ = grp.trace(r, q, V.ALPHA_TEXTURE, alpha_threshold=0.4)
+                res += [h.cpu().numpy().tobytes(), w.cpu().numpy().tobytes()]
+            mh, mn, mw, _ = grp.trace_multi(r, 4, V.ALPHA_TEXTURE, alpha_threshold=0.4)
+            res += [mh.cpu().numpy().tobytes(), mn.cpu().numpy().tobytes()]
+            out[bits] = res
+        assert out[True] == out[False]
+    mscenes = [V.Scene.from_workload(m).build() for m in models]
+    inst = V.Instances(mscenes, ibvh, imat)
+    out = {}
+    for bits in (True, False):
+        monkeypatch.setenv("VSR_ALPHA_BITS", "1" if bits else "0")
+        res = []
+        for q in (V.ANY, V.CLOSEST):
+            h, w, _ = inst.trace(fr, q, V.ALPHA_TEXTURE, alpha_threshold=0.3)
+            res += [h.cpu().numpy().tobytes(), w.cpu().numpy().tobytes()]
+        out[bits] = res
+    assert out[True] == out[False]
