@@ -162,13 +162,14 @@ def make_workload(name, rank=0):
     return W.scene(name), W.rays_for(name, shift_x=2.0 * rank)
 
 
-def algorithmic_bytes(counts_np, isect_has_alpha):
-    """B(r) = 32 + 16 + 64*I + 48*T + 36*A, I = (boxes-1)/2."""
+def algorithmic_bytes(counts_np, isect_has_alpha, counts_out=False):
+    """B(r) = 32 + 16 [+ counts] + 64*I + 48*T + 36*A, I = (boxes-1)/2; the
+    counting intersectors write a 16-B counts record per ray (the layout's, vsr.h vsr_counts)."""
     boxes = counts_np["boxes"].astype(np.int64)
     tris = counts_np["tris"].astype(np.int64)
     alpha = counts_np["alpha"].astype(np.int64) if isect_has_alpha else 0
     inner = (boxes - 1) // 2
-    per_ray = 48 + 64 * inner + 48 * tris + 36 * alpha
+    per_ray = 48 + (16 if counts_out else 0) + 64 * inner + 48 * tris + 36 * alpha
     return int(per_ray.sum()), {"inner_per_ray": float(inner.mean()), "tris_per_ray": float(tris.mean()),
                                 "alpha_per_ray": float(np.mean(alpha)) if isect_has_alpha else 0.0}
 
@@ -335,13 +336,14 @@ def run_own(args):
     value = world * n / (ms_step_max * 1e-3) / 1e6
 
     # ---- algorithmic bytes from the counting intersector (untimed) ----
-    has_alpha = args.isect in ("alpha_texture", "runtime_switch_alpha_texture",
-                               "runtime_fnptr_alpha_texture")
+    has_alpha = args.isect in ("alpha_texture", "count_alpha_texture",
+                               "runtime_switch_alpha_texture", "runtime_fnptr_alpha_texture")
     cnt_kind = vsr.COUNT_ALPHA_TEXTURE if has_alpha else vsr.COUNT
     trace(cnt_kind)
     torch.cuda.synchronize()
     cnp = vsr.counts_to_numpy(counts)
-    bytes_launch, work = algorithmic_bytes(cnp, has_alpha)
+    bytes_launch, work = algorithmic_bytes(cnp, has_alpha,
+                                           counts_out=args.isect in ("count", "count_alpha_texture"))
     peak, peak_src = load_peaks()
     achieved = bytes_launch / (ms_kernel * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
