@@ -257,14 +257,16 @@ def test_c2_trace_host_equals_device(V, c2):
             assert ch.tobytes() == cd.tobytes()
 
 
-@pytest.mark.parametrize("chunk", ["4096", "65536", "300000"])
-def test_trace_host_ring_reuse(V, c2, monkeypatch, chunk):
+@pytest.mark.parametrize("chunk,pin", [("4096", True), ("65536", True), ("300000", True),
+                                       ("4096", False)])
+def test_trace_host_ring_reuse(V, c2, monkeypatch, chunk, pin):
     """The host pipeline's ring of 8 chunk slots: more chunks than slots (slot reuse behind
-    the D2H event), a ragged last chunk, counts and hits both staged; equal to the device path."""
+    the D2H event), a ragged last chunk, counts and hits both staged, pinned or pageable rays
+    (hits: pageable numpy); equal to the device path."""
     sc, rays, s = c2
     sub = np.ascontiguousarray(rays.data[: 8 * 4096 * 3 + 777])   # 99,081 rays
     monkeypatch.setenv("VSR_HOST_CHUNK", chunk)
-    pinned = torch.from_numpy(sub).pin_memory()
+    pinned = torch.from_numpy(sub).pin_memory() if pin else sub
     for q, k in ((V.ANY, V.ALPHA_TEXTURE), (V.CLOSEST, V.COUNT_ALPHA_TEXTURE), (V.ANY, V.COUNT)):
         hd, cd = gpu_trace(V, s, sub, q, k)
         hh, ch = s.trace_host(pinned, q, k)
