@@ -155,6 +155,27 @@ def test_persistent_schedule(V, oracle_lib, monkeypatch, refill):
     assert V.hits_to_numpy(hits).tobytes() == ref[(V.CLOSEST, V.ALPHA_TEXTURE)][0].tobytes()
 
 
+@pytest.mark.parametrize("knobs", [{"VSR_ORDER": "0"}, {"VSR_PDL": "0"},
+                                   {"VSR_ORDER": "0", "VSR_ALPHA_BITS": "0"}])
+def test_scheduling_knobs_change_no_result(V, c2, monkeypatch, knobs):
+    """README's runtime knobs: tile order instead of longest-first, plain launches instead of
+    the PDL chain, A8 instead of the 1-bit plane — the same bytes as the defaults (C2 frame,
+    large enough for the order pass to run)."""
+    sc, rays, s = c2
+    ref = {}
+    for q in (V.CLOSEST, V.ANY):
+        for k in (V.ALPHA_TEXTURE, V.COUNT_ALPHA_TEXTURE):
+            ref[(q, k)] = gpu_trace(V, s, rays.data, q, k)
+    for name, val in knobs.items():
+        monkeypatch.setenv(name, val)
+    for q in (V.CLOSEST, V.ANY):
+        for k in (V.ALPHA_TEXTURE, V.COUNT_ALPHA_TEXTURE):
+            h, c = gpu_trace(V, s, rays.data, q, k)
+            assert h.tobytes() == ref[(q, k)][0].tobytes(), (knobs, q, k)
+            if c is not None:
+                assert c.tobytes() == ref[(q, k)][1].tobytes()
+
+
 def test_imported_oracle_bvh_counts(V, oracle_lib):
     """Counts bit-exact on a tree the product did NOT build (oracle median BVH)."""
     o = oracle_lib
