@@ -131,13 +131,25 @@ __device__ __forceinline__ void gen_ray(const Pinhole& c, uint64_t id, float4& a
                   __double2float_rn((c.w[2] + A * c.u[2]) + B * c.v[2]), c.tmax);
 }
 
+#ifndef VSR_RAY_NA
+#define VSR_RAY_NA 1   // measured +1 % (profiles/r01_tuning.md); 0 = plain __ldg
+#endif
 template <bool GEN>
 __device__ __forceinline__ void fetch_ray(const TraceParams& p, uint64_t id, float4& a, float4& b) {
   if constexpr (GEN) {
     gen_ray(p.cam, id, a, b);
   } else {
+#if VSR_RAY_NA
+    // rays are read once: no L1 allocation, so they do not evict node lines
+    const float4* rp = p.rays + 2 * id;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(rp));
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(rp + 1));
+#else
     a = __ldg(p.rays + 2 * id);
     b = __ldg(p.rays + 2 * id + 1);
+#endif
   }
 }
 
