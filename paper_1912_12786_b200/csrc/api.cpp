@@ -211,6 +211,19 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
   p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
+  // closest-hit occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)
+  const char* eo2 = std::getenv("VSR_OCC");
+  if (eo2) {
+    p.occ = std::strcmp(eo2, "0") != 0;
+  } else {
+    int l2 = 0;
+    if (s->device >= 0 &&
+        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, s->device) != cudaSuccess) {
+      cudaGetLastError();
+      l2 = 0;
+    }
+    p.occ = l2 > 0 && s->stats.device_bytes > (uint64_t)l2;
+  }
   return VSR_OK;
 }
 

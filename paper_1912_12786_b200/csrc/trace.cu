@@ -115,8 +115,12 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
-template <int Q, class I, bool GEN = false>
-__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_kernel(const TraceParams p) {
+// OCC: occupancy variant, 12 CTAs (48 warps) per SM: the closest-hit kernels
+// otherwise run 10 (45 registers). Chosen by the host for scenes larger than L2,
+// where more warps hide DRAM latency (C4 +3 %, C5 +4 %); L2-resident scenes lose
+// ~1 % to its spills (profiles/r01_tuning.md).
+template <int Q, class I, bool GEN = false, bool OCC = false>
+__global__ void __launch_bounds__(kBlock, OCC ? 12 : VSR_MINB) trace_kernel(const TraceParams p) {
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
 #endif
@@ -291,8 +295,12 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
       if constexpr (std::is_same<I, runtime_switch_intersector>::value ||
                     std::is_same<I, runtime_fnptr_intersector>::value)
         return cudaErrorInvalidValue;
+      else if (Q == kClosest && p.occ)
+        e = launch_k(trace_kernel<Q, I, true, true>, need, kBlock, p.perm && p.pdl, st, p);
       else
         e = launch_k(trace_kernel<Q, I, true>, need, kBlock, p.perm && p.pdl, st, p);
+    } else if (Q == kClosest && p.occ) {
+      e = launch_k(trace_kernel<Q, I, false, true>, need, kBlock, p.perm && p.pdl, st, p);
     } else {
       e = launch_k(trace_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);
     }

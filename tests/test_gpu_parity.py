@@ -156,11 +156,11 @@ def test_persistent_schedule(V, oracle_lib, monkeypatch, refill):
 
 
 @pytest.mark.parametrize("knobs", [{"VSR_ORDER": "0"}, {"VSR_PDL": "0"},
-                                   {"VSR_ORDER": "0", "VSR_ALPHA_BITS": "0"}])
+                                   {"VSR_ORDER": "0", "VSR_ALPHA_BITS": "0"}, {"VSR_OCC": "1"}])
 def test_scheduling_knobs_change_no_result(V, c2, monkeypatch, knobs):
     """README's runtime knobs: tile order instead of longest-first, plain launches instead of
-    the PDL chain, A8 instead of the 1-bit plane — the same bytes as the defaults (C2 frame,
-    large enough for the order pass to run)."""
+    the PDL chain, A8 instead of the 1-bit plane, the closest-hit occupancy variant — the same
+    bytes as the defaults (C2 frame, large enough for the order pass to run)."""
     sc, rays, s = c2
     ref = {}
     for q in (V.CLOSEST, V.ANY):

@@ -35,9 +35,8 @@ def sass():
 def _find(funcs, q, tag, gen=False):
     """The trace kernel for query q and intersector `tag`; gen: the fused ray-generation
     instantiation (template flag GEN, mangled Lb1)."""
-    flag = "ELb1E" if gen else "ELb0E"
-    names = [n for n in funcs if f"trace_kernelILi{q}E" in n and tag in n and "cost_" not in n
-             and flag in n]
+    flag = f"{tag}ELb{int(gen)}ELb0E"   # GEN, then OCC = false (the default-occupancy kernel)
+    names = [n for n in funcs if f"trace_kernelILi{q}E" in n and "cost_" not in n and flag in n]
     assert len(names) == 1, names
     return funcs[names[0]]
 
