@@ -211,7 +211,7 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
   p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
-  // closest-hit occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)
+  // 12-CTA occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)
   const char* eo2 = std::getenv("VSR_OCC");
   if (eo2) {
     p.occ = std::strcmp(eo2, "0") != 0;

@@ -115,12 +115,14 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
-// OCC: occupancy variant, 12 CTAs (48 warps) per SM: the closest-hit kernels
-// otherwise run 10 (45 registers). Chosen by the host for scenes larger than L2,
-// where more warps hide DRAM latency (C4 +3 %, C5 +4 %); L2-resident scenes lose
-// ~1 % to its spills (profiles/r01_tuning.md).
+// OCC: occupancy variant, 12 CTAs (48 warps) per SM at <= 40 registers with a
+// few spills, chosen by the host for scenes larger than L2, where more warps hide
+// DRAM latency (closest: C4 +3 %, C5 +4 %; any: C5 +3 %). Otherwise 10 CTAs
+// (43-45 registers, no spills), which L2-resident scenes prefer (C2 any +0.6 %,
+// closest +1.5 %; profiles/r01_tuning.md).
 template <int Q, class I, bool GEN = false, bool OCC = false>
-__global__ void __launch_bounds__(kBlock, OCC ? 12 : VSR_MINB) trace_kernel(const TraceParams p) {
+__global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB))
+    trace_kernel(const TraceParams p) {
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
 #endif
@@ -295,11 +297,11 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
       if constexpr (std::is_same<I, runtime_switch_intersector>::value ||
                     std::is_same<I, runtime_fnptr_intersector>::value)
         return cudaErrorInvalidValue;
-      else if (Q == kClosest && p.occ)
+      else if (p.occ)
         e = launch_k(trace_kernel<Q, I, true, true>, need, kBlock, p.perm && p.pdl, st, p);
       else
         e = launch_k(trace_kernel<Q, I, true>, need, kBlock, p.perm && p.pdl, st, p);
-    } else if (Q == kClosest && p.occ) {
+    } else if (p.occ) {
       e = launch_k(trace_kernel<Q, I, false, true>, need, kBlock, p.perm && p.pdl, st, p);
     } else {
       e = launch_k(trace_kernel<Q, I>, need, kBlock, p.perm && p.pdl, st, p);

@@ -26,7 +26,7 @@ struct TraceParams {
   const uint32_t* perm;          // longest-first block permutation (set by launch_trace)
   uint32_t* hist_reset;          // order histogram the trace kernel re-zeroes (set by launch_trace)
   int pdl;                       // launch the order pass + trace kernel as PDL dependents
-  int occ;                       // closest-hit: the 12-CTA/SM variant (scenes larger than L2)
+  int occ;                       // the 12-CTA/SM trace-kernel variant (scenes larger than L2)
   void* order_scratch;           // optional stream-ordered scratch for the order pass
   size_t order_scratch_bytes;
   int max_hits;                  // multi-hit query: hits kept per ray (1..16)
