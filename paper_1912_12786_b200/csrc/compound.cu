@@ -102,7 +102,7 @@ __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& 
 }
 
 template <int Q, class I>
-__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_kernel(const TraceParams p) {
+__global__ void __launch_bounds__(kBlock, VSR_INST_MINB) trace_instances_kernel(const TraceParams p) {
   const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
   if (id >= p.n) return;

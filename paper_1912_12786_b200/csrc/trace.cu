@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
 // Multi-hit query: same traversal, the leaf accepts into a K-entry sorted
 // buffer (runtime max_hits <= K).  Output ray-major: hits[id*max_hits + j].
 template <class I, int K>
-__global__ void __launch_bounds__(kBlock, VSR_MINB) trace_multi_kernel(const TraceParams p) {
+__global__ void __launch_bounds__(kBlock, VSR_MULTI_MINB) trace_multi_kernel(const TraceParams p) {
   const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
   if (id >= p.n) return;
