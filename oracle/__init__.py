@@ -83,6 +83,8 @@ def lib():
                                    C.c_int]
         L.oracle_eval_pair.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_uint32, C.c_int,
                                        C.c_float, C.c_uint32, C.POINTER(_Hit)]
+        L.oracle_eval_pairs.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_void_p, C.c_uint64,
+                                        C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p]
         L.oracle_mt.argtypes = [C.c_void_p] * 4 + [C.c_float] + [C.POINTER(C.c_float)] * 3
         L.oracle_tex_alpha.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_float, C.c_float]
         L.oracle_tex_alpha.restype = C.c_float
@@ -209,6 +211,21 @@ def eval_pair(scene, ray, prim, isect=DEFAULT, alpha_threshold=0.01, checker_fre
     acc = lib().oracle_eval_pair(C.byref(sc.c), _ptr(r), int(prim), isect, alpha_threshold,
                                  checker_freq, C.byref(h))
     return bool(acc), h.t, h.u, h.v
+
+
+def eval_pairs(scene, rays, prims, isect=DEFAULT, alpha_threshold=0.01, checker_freq=8):
+    """eval_pair over arrays: (accepted bool[n], hits HIT_DTYPE[n]) of ray i against
+    caller-indexed triangle prims[i]."""
+    sc = _as_scene(scene)
+    r = _rays(rays)
+    p = np.ascontiguousarray(prims, dtype=np.uint32).reshape(-1)
+    assert p.shape[0] == r.shape[0]
+    acc = np.zeros(r.shape[0], np.uint8)
+    hits = np.empty(r.shape[0], dtype=HIT_DTYPE)
+    if lib().oracle_eval_pairs(C.byref(sc.c), _ptr(r), _ptr(p), r.shape[0], isect,
+                               alpha_threshold, checker_freq, _ptr(acc), _ptr(hits)) != 0:
+        raise ValueError("oracle_eval_pairs: prim out of range")
+    return acc.astype(bool), hits
 
 
 def mt(ray, v0, v1, v2, tmax=None):

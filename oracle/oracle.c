@@ -113,6 +113,9 @@ float oracle_tex_alpha_bilinear(uint32_t w, uint32_t h, const uint8_t* rgba, flo
   return ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;
 }
 
+static double W_of(const or_scene* s, uint32_t k) { return (double)s->tex_w[k]; }
+static double H_of(const or_scene* s, uint32_t k) { return (double)s->tex_h[k]; }
+
 /* bilinear alpha in double (flags only) */
 static double bilinear_double(uint32_t w, uint32_t h, const uint8_t* rgba, double s, double t) {
   double x = s * w - 0.5, y = t * h - 0.5;
@@ -189,6 +192,17 @@ int oracle_eval_pair(const or_scene* s, const float* ray, uint32_t prim, int ise
   if (degenerate(vt)) hit = 0;
   out->t = t; out->u = u; out->v = v; out->prim = prim;
   return hit && filter(s, prim, isect, u, v, thr, M);
+}
+
+/* oracle_eval_pair over n (ray, prim) pairs: acc[i] = accepted, out[i] = (t, u, v, prim). */
+int oracle_eval_pairs(const or_scene* s, const float* rays, const uint32_t* prims, uint64_t n,
+                      int isect, float thr, uint32_t M, uint8_t* acc, or_hit* out) {
+  if (!s || !rays || !prims || !acc || !out) return -1;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (prims[i] >= s->num_tris) return -1;
+    acc[i] = (uint8_t)oracle_eval_pair(s, rays + i * 8, prims[i], isect, thr, M, out + i);
+  }
+  return 0;
 }
 
 /* ---------------- double shadow (ambiguity flags only) ------------------- */
@@ -361,7 +375,23 @@ static void trace_one(const job_t* jb, uint64_t r) {
       } else {
         uint32_t k = tri_texture(s, i);
         double a = bilinear_double(s->tex_w[k], s->tex_h[k], s->tex_rgba[k], ss, tt);
-        if (fabs(a - (double)jb->thr) < 1e-4) f |= OR_X5_ALPHA_NEAR;
+        /* X5 band (reading A28): north_star's 1e-6, which also covers
+         * the fp32 bilinear formula's own rounding (7 ops on values in [0, 1]:
+         * <= 7 * 2^-24 = 4.2e-7), plus the first-order propagation of the fp32
+         * texcoords' deviation from the double ones: alpha is piecewise bilinear
+         * with |d alpha / d s| <= W and |d alpha / d t| <= H (texel alphas in
+         * [0, 1]), so |alpha32 - alpha64| <~ W |s32 - s64| + H |t32 - t64|;
+         * doubled for second-order terms.  With no fp32 hit there is no fp32
+         * decision to be wrong and the band is the floor. */
+        double band = 1e-6;
+        float t32, u32, v32;
+        if (oracle_mt(ray, vt, vt + 3, vt + 6, ray[7], &t32, &u32, &v32)) {
+          float st32[2];
+          oracle_lerp2(tc, tc + 2, tc + 4, u32, v32, st32);
+          band += 2.0 * (W_of(s, k) * fabs((double)st32[0] - ss) +
+                         H_of(s, k) * fabs((double)st32[1] - tt));
+        }
+        if (fabs(a - (double)jb->thr) < band) f |= OR_X5_ALPHA_NEAR;
       }
     }
   }

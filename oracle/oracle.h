@@ -81,6 +81,10 @@ int oracle_trace_multi(const or_scene* s, const float* rays, uint64_t n, uint32_
  * with the geometric t,u,v. */
 int oracle_eval_pair(const or_scene* s, const float* ray, uint32_t prim, int isect,
                      float alpha_threshold, uint32_t checker_freq, or_hit* out);
+/* Batch form: accepted flags and (t, u, v, prim) of n (ray, caller-indexed prim)
+ * pairs; -1 on a NULL argument or a prim out of range. */
+int oracle_eval_pairs(const or_scene* s, const float* rays, const uint32_t* prims, uint64_t n,
+                      int isect, float thr, uint32_t M, uint8_t* acc, or_hit* out);
 
 /* Individual textbook pieces, exposed for the closed-form pins. */
 int oracle_mt(const float* ray, const float* v0, const float* v1, const float* v2,

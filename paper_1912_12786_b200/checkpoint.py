@@ -26,6 +26,10 @@ def load_scene(path: str, device: int = 0) -> "vsr.Scene":
     with np.load(path, allow_pickle=False) as z:
         if str(z["format"]) != FORMAT:
             raise ValueError(f"{path}: not a {FORMAT} file")
+        if "abi" not in z or int(z["abi"]) != int(vsr.lib().vsr_abi_version()):
+            # the export layout (nodes, sidecars) is versioned by the ABI number
+            raise ValueError(f"{path}: written by ABI {int(z['abi']) if 'abi' in z else '?'}, "
+                             f"this library is ABI {int(vsr.lib().vsr_abi_version())}")
         arrs = {k: z[k] for k in ("nodes", "tris", "sides", "texdescs", "texels", "root_lo",
                                   "root_hi")}
         arrs["root_ref"] = int(z["root_ref"])

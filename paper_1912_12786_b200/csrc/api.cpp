@@ -55,6 +55,9 @@ vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const f
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s->d_counters), cbytes);
     if (e != cudaSuccess) return cuda_fail(e, "counters");
     if ((e = cudaMemset(s->d_counters, 0, cbytes)) != cudaSuccess) return cuda_fail(e, "counters");
+    // cudaMemset may return before the zeroes land; the build is synchronous, so
+    // wait here rather than rely on legacy-stream ordering against later streams
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "counters");
   }
   s->num_texels = num_texels;
   DevScene& d = s->dev;
@@ -264,8 +267,14 @@ cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TracePara
       o->cap = 0;
       if ((e = cudaMalloc(&o->ptr, bytes)) != cudaSuccess) return e;
       // the order histogram must be zero at each launch's entry (launch_trace
-      // keeps it so: the trace kernel re-zeroes it)
-      if ((e = cudaMemset(o->ptr, 0, bytes)) != cudaSuccess) return e;
+      // keeps it so: the trace kernel re-zeroes it).  Zeroed on the launch
+      // stream itself: a legacy-stream memset is not ordered before kernels on
+      // a non-blocking stream, and the event wait below is a no-op on first use.
+      if ((e = cudaMemsetAsync(o->ptr, 0, bytes, st)) != cudaSuccess) {
+        cudaFree(o->ptr);
+        o->ptr = nullptr;
+        return e;
+      }
       o->cap = bytes;
     }
     if ((e = cudaStreamWaitEvent(st, o->ev, 0)) != cudaSuccess) return e;
@@ -273,7 +282,12 @@ cudaError_t launch_with_scratch(ScratchSet& set, int query, int isect, TracePara
     p.order_scratch_bytes = o->cap;
   }
   e = launch_trace(query, isect, p, st);
-  if (e == cudaSuccess && o) e = cudaEventRecord(o->ev, st);
+  // recorded even when the launch failed part-way: kernels touching the
+  // scratch may already be queued, and the next user must wait for them
+  if (o) {
+    const cudaError_t r = cudaEventRecord(o->ev, st);
+    if (e == cudaSuccess) e = r;
+  }
   return e;
 }
 
@@ -642,10 +656,22 @@ vsr_status vsr_scene_import(const vsr_bvh_view* v, int device, vsr_scene** out) 
         t.offset + (uint64_t)t.w * t.h > v->num_texels)
       return fail(VSR_ERR_INVALID_ARG, "texture descriptor " + std::to_string(k) + " out of range");
   }
-  for (uint32_t k = 0; k < v->num_tris; ++k)
+  // Every sidecar must name one of the descriptors exactly (offset and dims): the
+  // 1-bit-plane eligibility is decided on the descriptors, and alpha_keep_bits
+  // indexes the plane with the sidecar's own (offset, dims).
+  std::vector<uint64_t> keys(v->num_textures);
+  for (uint32_t k = 0; k < v->num_textures; ++k)
+    keys[k] = descs[k].offset << 32 | (uint64_t)((descs[k].w - 1u) | (descs[k].h - 1u) << 16);
+  std::sort(keys.begin(), keys.end());
+  for (uint32_t k = 0; k < v->num_tris; ++k) {
     if ((uint64_t)sides[k].texel_offset + (uint64_t)((sides[k].dims & 0xFFFFu) + 1u) *
                                               ((sides[k].dims >> 16) + 1u) > v->num_texels)
       return fail(VSR_ERR_INVALID_ARG, "sidecar " + std::to_string(k) + " texture out of range");
+    const uint64_t key = (uint64_t)sides[k].texel_offset << 32 | sides[k].dims;
+    if (!std::binary_search(keys.begin(), keys.end(), key))
+      return fail(VSR_ERR_INVALID_ARG,
+                  "sidecar " + std::to_string(k) + " does not match any texture descriptor");
+  }
   // Structure: reachable refs in range, every triangle in exactly one leaf, depth <= 64.
   std::vector<uint8_t> seen_tri(v->num_tris, 0), seen_node(v->num_nodes, 0);
   struct Item { uint32_t ref; uint32_t depth; };

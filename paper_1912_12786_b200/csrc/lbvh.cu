@@ -509,7 +509,7 @@ vsr_status build_bvh_gpu(const float* d_vertices, const float* d_texcoords,
   const int init[6] = {0x7FFFFFFF, 0x7FFFFFFF, 0x7FFFFFFF, (int)0x80000000, (int)0x80000000,
                        (int)0x80000000};
   VSR_TRY(cudaMemcpy(cb, init, sizeof init, cudaMemcpyHostToDevice));
-  VSR_TRY(cudaMemset(counters, 0, 3 * sizeof(uint32_t)));
+  VSR_TRY(cudaMemsetAsync(counters, 0, 3 * sizeof(uint32_t), st));   // ordered before prep_kernel
   prep_kernel<<<g, kT, 0, st>>>(d_vertices, n, box, cen, valid, cb, counters);
   VSR_TRY(cudaGetLastError());
   uint32_t m32 = 0;

@@ -399,6 +399,15 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
   const uint64_t nblocks = (p.n + kBlock - 1) / kBlock;
   void* scratch = nullptr;
   bool owned = false;
+  // every exit after a stream-ordered allocation frees it on the stream (after
+  // whatever was queued), so an error part-way through leaks nothing
+  auto done = [&](cudaError_t e) {
+    if (owned) {
+      const cudaError_t f = cudaFreeAsync(scratch, st);
+      if (e == cudaSuccess) e = f;
+    }
+    return e;
+  };
   if (p.order && p.sched == kSchedDirect && nblocks >= 2ull * sm_count() && nblocks < (1u << 24)) {
     // the owner's per-stream scratch (api.cpp ScratchSet); a stream-ordered
     // allocation only past 16 streams per owner
@@ -416,23 +425,29 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     const bool zeroed = !owned;   // caller scratch: zero at entry, kept so by the trace kernel
     if (!zeroed &&
         (e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess)
-      return e;
+      return done(e);
     if (p.gen)
       order_cost_kernel<true><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
           p, (uint32_t)nblocks, hist, slot);
     else
       order_cost_kernel<false><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
           p, (uint32_t)nblocks, hist, slot);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
+      return done(e);
+    }
     if ((e = launch_k(order_scatter_kernel, (nblocks + 255) / 256, 256, p.pdl != 0, st,
                       (uint32_t)nblocks, (const uint32_t*)hist, (const uint32_t*)slot, perm)) !=
         cudaSuccess) {
       if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
-      return e;
+      return done(e);
     }
     launch_counter().fetch_add(2, std::memory_order_relaxed);
     if (!owned) p.hist_reset = hist;   // the trace kernel re-zeroes it for the next launch
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
+      return done(e);
+    }
     p.perm = perm;
   }
   if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
@@ -443,11 +458,7 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
   if (g_kernel_events[1]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[1]), st);
   if (e != cudaSuccess && p.hist_reset)   // the trace kernel did not run: restore the invariant
     cudaMemsetAsync(p.hist_reset, 0, sizeof(uint32_t) * kOrderBuckets, st);
-  if (owned) {
-    cudaError_t f = cudaFreeAsync(scratch, st);
-    if (e == cudaSuccess) e = f;
-  }
-  return e;
+  return done(e);
 }
 
 // 1-bit alpha plane of threshold a_min (see alpha_keep_bits): one thread per

@@ -240,13 +240,68 @@ def _ptr(a):
     return a.ctypes.data
 
 
-def _stream_handle(stream):
+def _stream_handle(stream, device=None):
+    """Raw cudaStream_t: the given stream, else the current stream of `device`
+    (the scene's device, not whichever device happens to be current)."""
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def _check_dev(t, name, dtype, rows, tail, device, optional=False):
+    """Argument check before a device pointer crosses the C ABI (the C side only
+    sees NULL and alignment): a contiguous CUDA tensor on the scene's device with
+    the expected dtype, at least `rows` rows and trailing shape `tail`.  Raises
+    ValueError on a mismatch instead of letting a kernel read or write out of bounds."""
+    import torch
+    if t is None:
+        if optional:
+            return
+        raise ValueError(f"{name}: a CUDA tensor is required")
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name}: expected a torch CUDA tensor, got {type(t).__name__}")
+    if not t.is_cuda or (device is not None and t.device.index != device):
+        raise ValueError(f"{name}: must live on cuda:{device}, got {t.device}")
+    if t.dtype not in dtype:
+        raise ValueError(f"{name}: dtype {t.dtype} not in {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+    if t.dim() != 1 + len(tail) or tuple(t.shape[1:]) != tuple(tail) or t.shape[0] < rows:
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, need [>= {rows}, "
+                         f"{', '.join(map(str, tail))}]")
+
+
+def _f32():
+    import torch
+    return (torch.float32,)
+
+
+def _i32():
+    import torch
+    return (torch.int32, torch.uint32) if hasattr(torch, "uint32") else (torch.int32,)
+
+
+def _check_rays(rays, n, device):
+    _check_dev(rays, "rays", _f32(), n, (8,), device)
+    if n > rays.shape[0]:
+        raise ValueError(f"n={n} exceeds rays.shape[0]={rays.shape[0]}")
+
+
+def _check_host(a, name, rows, row_bytes):
+    """Host buffer for vsr_trace_host: C-contiguous, >= rows x row_bytes bytes."""
+    if hasattr(a, "is_cuda"):
+        if a.is_cuda or not a.is_contiguous():
+            raise ValueError(f"{name}: expected a contiguous host tensor")
+        nbytes = a.numel() * a.element_size()
+    else:
+        if not isinstance(a, np.ndarray) or not a.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"{name}: expected a C-contiguous numpy array")
+        nbytes = a.nbytes
+    if nbytes < rows * row_bytes:
+        raise ValueError(f"{name}: {nbytes} bytes, need {rows * row_bytes}")
 
 
 class Scene:
@@ -329,13 +384,16 @@ class Scene:
         counts: [n, 4] int32 for COUNT kinds (allocated if None)."""
         import torch
         n = rays.shape[0] if n is None else n
+        _check_rays(rays, n, self.device)
         if hits is None:
             hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        _check_dev(hits, "hits", _f32(), n, (4,), self.device)
+        _check_dev(counts, "counts", _i32(), n, (4,), self.device, optional=True)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace(self._h, _ptr(rays), n, query, isect, C.byref(prm), _ptr(hits),
-                               _ptr(counts), _stream_handle(stream)))
+                               _ptr(counts), _stream_handle(stream, self.device)))
         return hits, counts
 
     def trace_pinhole(self, camera, query=CLOSEST, isect=DEFAULT, hits=None, counts=None,
@@ -348,9 +406,12 @@ class Scene:
             hits = torch.empty((n, 4), dtype=torch.float32, device=f"cuda:{self.device}")
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = torch.empty((n, 4), dtype=torch.int32, device=hits.device)
+        _check_dev(hits, "hits", _f32(), n, (4,), self.device)
+        _check_dev(counts, "counts", _i32(), n, (4,), self.device, optional=True)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_pinhole(self._h, C.byref(camera), query, isect, C.byref(prm),
-                                       _ptr(hits), _ptr(counts), _stream_handle(stream)))
+                                       _ptr(hits), _ptr(counts),
+                                       _stream_handle(stream, self.device)))
         return hits, counts
 
     def trace_tiles(self, rays, tile_rays, rank, world, frame_hits_ptr, query=CLOSEST,
@@ -358,22 +419,25 @@ class Scene:
                     checker_freq=8):
         """vsr_trace_tiles: trace this rank's tile shard `rays` and store each hit at its frame
         position in the buffer at `frame_hits_ptr` (e.g. rank 0's frame via ipc_open)."""
+        _check_rays(rays, rays.shape[0], self.device)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_tiles(self._h, _ptr(rays), rays.shape[0], tile_rays, rank, world,
                                      query, isect, C.byref(prm), frame_hits_ptr,
-                                     frame_counts_ptr, _stream_handle(stream)))
+                                     frame_counts_ptr, _stream_handle(stream, self.device)))
 
     def trace_primitives(self, rays, query=CLOSEST, isect=DEFAULT, stream=None,
                          alpha_threshold=0.01, checker_freq=8):
         """vsr_trace_primitives: the query on the triangles as a plain list (no BVH)."""
         import torch
         n = rays.shape[0]
+        _check_rays(rays, n, self.device)
         hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
         counts = (torch.empty((n, 4), dtype=torch.int32, device=rays.device)
                   if isect in (COUNT, COUNT_ALPHA_TEXTURE) else None)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_primitives(self._h, _ptr(rays), n, query, isect, C.byref(prm),
-                                          _ptr(hits), _ptr(counts), _stream_handle(stream)))
+                                          _ptr(hits), _ptr(counts),
+                                          _stream_handle(stream, self.device)))
         return hits, counts
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, hits=None, num_hits=None, counts=None,
@@ -383,16 +447,20 @@ class Scene:
         Returns (hits [n, max_hits, 4] float32, num_hits [n] int32, counts or None)."""
         import torch
         n = rays.shape[0]
+        _check_rays(rays, n, self.device)
         if hits is None:
             hits = torch.empty((n, max_hits, 4), dtype=torch.float32, device=rays.device)
         if num_hits is None:
             num_hits = torch.empty((n,), dtype=torch.int32, device=rays.device)
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        _check_dev(hits, "hits", _f32(), n, (max_hits, 4), self.device)
+        _check_dev(num_hits, "num_hits", _i32(), n, (), self.device)
+        _check_dev(counts, "counts", _i32(), n, (4,), self.device, optional=True)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_multi(self._h, _ptr(rays), n, max_hits, isect, C.byref(prm),
                                      _ptr(hits), _ptr(num_hits), _ptr(counts),
-                                     _stream_handle(stream)))
+                                     _stream_handle(stream, self.device)))
         return hits, num_hits, counts
 
     def trace_raw(self, rays_ptr, n, query, isect, hits_ptr, counts_ptr=None, stream=0,
@@ -409,6 +477,10 @@ class Scene:
             hits = np.empty(n, dtype=HIT_DTYPE)
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = np.empty(n, dtype=COUNTS_DTYPE)
+        _check_host(rays, "rays", n, 32)
+        _check_host(hits, "hits", n, 16)
+        if counts is not None:
+            _check_host(counts, "counts", n, 16)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_host(self._h, _ptr(rays), n, query, isect, C.byref(prm),
                                     _ptr(hits), _ptr(counts),
@@ -483,28 +555,36 @@ class Group:
         """Returns (hits [n, 4], which [n] int32 list index, counts or None)."""
         import torch
         n = rays.shape[0]
+        dev = self.scenes[0].device if self.scenes else None
+        _check_rays(rays, n, dev)
         if hits is None:
             hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
         if which is None:
             which = torch.empty((n,), dtype=torch.int32, device=rays.device)
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        _check_dev(hits, "hits", _f32(), n, (4,), dev)
+        _check_dev(which, "which", _i32(), n, (), dev)
+        _check_dev(counts, "counts", _i32(), n, (4,), dev, optional=True)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_group(self._h, _ptr(rays), n, query, isect, C.byref(prm),
                                      _ptr(hits), _ptr(which), _ptr(counts),
-                                     _stream_handle(stream)))
+                                     _stream_handle(stream, dev)))
         return hits, which, counts
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, stream=None, alpha_threshold=0.01,
                     checker_freq=8):
         """vsr_trace_group_multi: (hits [n, k, 4], num_hits [n], which [n, k], counts or None)."""
         return _compound_multi(lib().vsr_trace_group_multi, self._h, rays, max_hits, isect,
-                               stream, alpha_threshold, checker_freq)
+                               stream, alpha_threshold, checker_freq,
+                               self.scenes[0].device if self.scenes else None)
 
 
-def _compound_multi(fn, handle, rays, max_hits, isect, stream, alpha_threshold, checker_freq):
+def _compound_multi(fn, handle, rays, max_hits, isect, stream, alpha_threshold, checker_freq,
+                    device=None):
     import torch
     n = rays.shape[0]
+    _check_rays(rays, n, device)
     hits = torch.empty((n, max_hits, 4), dtype=torch.float32, device=rays.device)
     num = torch.empty((n,), dtype=torch.int32, device=rays.device)
     which = torch.empty((n, max_hits), dtype=torch.int32, device=rays.device)
@@ -512,7 +592,7 @@ def _compound_multi(fn, handle, rays, max_hits, isect, stream, alpha_threshold, 
               if isect in (COUNT, COUNT_ALPHA_TEXTURE) else None)
     prm = IsectParams(alpha_threshold, checker_freq)
     _check(fn(handle, _ptr(rays), n, max_hits, isect, C.byref(prm), _ptr(hits), _ptr(num),
-              _ptr(which), _ptr(counts), _stream_handle(stream)))
+              _ptr(which), _ptr(counts), _stream_handle(stream, device)))
     return hits, num, which, counts
 
 
@@ -552,23 +632,29 @@ class Instances:
         """Returns (hits [n, 4], inst [n] int32 caller instance index, counts or None)."""
         import torch
         n = rays.shape[0]
+        dev = self.scenes[0].device if self.scenes else None
+        _check_rays(rays, n, dev)
         if hits is None:
             hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
         if inst is None:
             inst = torch.empty((n,), dtype=torch.int32, device=rays.device)
         if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
             counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        _check_dev(hits, "hits", _f32(), n, (4,), dev)
+        _check_dev(inst, "inst", _i32(), n, (), dev)
+        _check_dev(counts, "counts", _i32(), n, (4,), dev, optional=True)
         prm = IsectParams(alpha_threshold, checker_freq)
         _check(lib().vsr_trace_instances(self._h, _ptr(rays), n, query, isect, C.byref(prm),
                                          _ptr(hits), _ptr(inst), _ptr(counts),
-                                         _stream_handle(stream)))
+                                         _stream_handle(stream, dev)))
         return hits, inst, counts
 
     def trace_multi(self, rays, max_hits, isect=DEFAULT, stream=None, alpha_threshold=0.01,
                     checker_freq=8):
         """vsr_trace_instances_multi: (hits [n, k, 4], num_hits [n], inst [n, k], counts)."""
         return _compound_multi(lib().vsr_trace_instances_multi, self._h, rays, max_hits, isect,
-                               stream, alpha_threshold, checker_freq)
+                               stream, alpha_threshold, checker_freq,
+                               self.scenes[0].device if self.scenes else None)
 
     def export(self) -> dict:
         """Host copies of the top level: nodes [num_nodes, 16] uint32 (pair nodes) and

@@ -25,30 +25,31 @@ def compare(oracle, scene, rays, query, isect, gpu, ref, ntie=None, exact=True,
     if query == oracle.CLOSEST:
         same = gpu["prim"] == ref["prim"]
         diff = np.nonzero(~same)[0]
-        for r in diff:
+        if diff.size:
             # only legitimate reason: an exact tie in t among accepted candidates
-            assert ntie is not None and ntie[r] > 1, _report("prim", [r], gpu, ref, max_report)
-            acc, t, u, v = oracle.eval_pair(scene, rays[r], int(gpu["prim"][r]), isect,
-                                            alpha_threshold, checker_freq)
-            assert acc and t == ref["t"][r] and t == gpu["t"][r], f"invalid tie winner ray {r}"
-            assert u == gpu["u"][r] and v == gpu["v"][r]
-            n_ties += 1
+            assert ntie is not None and np.all(ntie[diff] > 1), _report(
+                "prim", diff[ntie[diff] <= 1] if ntie is not None else diff, gpu, ref, max_report)
+            acc, e = oracle.eval_pairs(scene, rays[diff], gpu["prim"][diff], isect,
+                                       alpha_threshold, checker_freq)
+            ok = acc & (e["t"] == ref["t"][diff]) & (e["t"] == gpu["t"][diff]) & \
+                (e["u"] == gpu["u"][diff]) & (e["v"] == gpu["v"][diff])
+            assert np.all(ok), f"invalid tie winner rays {diff[~ok][:max_report]}"
+            n_ties = int(diff.size)
         s = same & g_hit
         _check_tuv(gpu, ref, s, exact)
     else:
+        # every returned any-hit: the prim must be in the accepted set A, with the oracle's
+        # (t, u, v) for that prim (several answers are correct)
         idx = np.nonzero(g_hit)[0]
-        for r in idx:
-            acc, t, u, v = oracle.eval_pair(scene, rays[r], int(gpu["prim"][r]), isect,
-                                            alpha_threshold, checker_freq)
-            if not acc:
-                bad.append(r)
-                continue
-            if exact:
-                if not (t == gpu["t"][r] and u == gpu["u"][r] and v == gpu["v"][r]):
-                    bad.append(r)
-            elif not (abs(t - gpu["t"][r]) <= 1e-5 * abs(t) and abs(u - gpu["u"][r]) <= 1e-5
-                      and abs(v - gpu["v"][r]) <= 1e-5):
-                bad.append(r)
+        acc, e = oracle.eval_pairs(scene, rays[idx], gpu["prim"][idx], isect, alpha_threshold,
+                                   checker_freq)
+        g = gpu[idx]
+        if exact:
+            ok = acc & (e["t"] == g["t"]) & (e["u"] == g["u"]) & (e["v"] == g["v"])
+        else:
+            ok = acc & (np.abs(e["t"] - g["t"]) <= 1e-5 * np.abs(e["t"])) & \
+                (np.abs(e["u"] - g["u"]) <= 1e-5) & (np.abs(e["v"] - g["v"]) <= 1e-5)
+        bad = list(idx[~ok])
         assert not bad, _report("any-hit prim not in accepted set", bad, gpu, ref, max_report)
     miss = ~g_hit
     assert np.all(gpu["t"][miss] == np.inf) and np.all(gpu["u"][miss] == 0) \

@@ -16,7 +16,7 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE = os.path.join(ROOT, "oracle")
 PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py",
-        "tests/test_instances_cpu.py", "tests/test_oracle_variants.py"]
+        "tests/test_instances_cpu.py", "tests/test_oracle_variants.py", "tests/test_oracle_flags.py"]
 
 MUTANTS = [
     # (file, original, mutated, description)
@@ -91,6 +91,30 @@ MUTANTS = [
      "instance multi-hit: instance index not moved with its hit"),
     ("walker.c", "            if (S->nk == S->K) S->best_t = S->mb[S->K - 1].t;\n", "",
      "instance multi-hit: a full buffer does not shrink tmax"),
+    # ---- ambiguity flags X1-X5 (round 2: tests/test_oracle_flags.py) ----
+    ("oracle.c", "(double)second_t - (double)best.t < 1e-5 * fabs((double)best.t))",
+     "(double)second_t - (double)best.t < 1e-7 * fabs((double)best.t))", "X1: tie band 100x too narrow"),
+    ("oracle.c", "      if (t < second_t) second_t = t;\n", "",
+     "X1: a later, farther candidate never becomes the runner-up"),
+    ("oracle.c", "second_t = have ? best.t : second_t;", "second_t = second_t;",
+     "X1: the displaced best is not kept as the runner-up"),
+    ("oracle.c", "if (fabs(m) < 1e-6) f |= OR_X2_EDGE_GRAZE;", "if (m >= 0 && m < 1e-6) f |= OR_X2_EDGE_GRAZE;",
+     "X2: only grazes from inside flagged"),
+    ("oracle.c", "    m = m < w ? m : w;\n    if (fabs(m)", "    if (fabs(m)",
+     "X2: third barycentric (1-u-v) dropped from the margin"),
+    ("oracle.c", "if (d0 != d1 || d0 != d2 || d0 != d3) f |= OR_X3_TEXEL_EDGE;", "f |= OR_X3_TEXEL_EDGE;",
+     "X3: no straddle check (every texel line flagged)"),
+    ("oracle.c", "if (dist_to_int(ss * W) < 1e-5 || dist_to_int(tt * H) < 1e-5) {",
+     "if (dist_to_int(ss * W) < 1e-5) {", "X3: row lines (t*H) not checked"),
+    ("oracle.c", "if (dist_to_int(u * M) < 1e-6 * M || dist_to_int(v * M) < 1e-6 * M) f |= OR_X4_CHECKER_EDGE;",
+     "if (dist_to_int(u * M) < 1e-6 * M) f |= OR_X4_CHECKER_EDGE;", "X4: v cell edges not checked"),
+    ("oracle.c", "      double M = (double)jb->M;\n      if (dist_to_int(u * M)",
+     "      double M = 8.0;\n      if (dist_to_int(u * M)", "X4: fixed M = 8 instead of the call's frequency"),
+    ("oracle.c", "        double band = 1e-6;", "        double band = 1e-8;", "X5: floor below north_star's 1e-6"),
+    ("oracle.c", "        double band = 1e-6;", "        double band = 1e-4;", "X5: round-1 blanket 1e-4 band"),
+    ("oracle.c", "          band += 2.0 * (W_of(s, k) * fabs((double)st32[0] - ss) +\n"
+                 "                         H_of(s, k) * fabs((double)st32[1] - tt));\n", "",
+     "X5: fp32 texcoord error not propagated into the band"),
 ]
 
 
@@ -130,7 +154,7 @@ def run():
 
 if __name__ == "__main__":
     rows = run()
-    print("# r01 — oracle mutation check (CPU pins only)\n")
+    print("# r02 — oracle mutation check (CPU pins only)\n")
     print("Each row patches one plausible mistake into a copy of `oracle/*.c`, builds it, and runs")
     print("`" + " ".join(PINS) + "` against it. A pin suite is adequate if every mutant is killed.\n")
     print("| mutant | result | first failing pin |")

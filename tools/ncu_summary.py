@@ -14,7 +14,8 @@ KEYS = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
         'sass__inst_executed_local_stores', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
         'l1tex__throughput.avg.pct_of_peak_sustained_active',
         'lts__throughput.avg.pct_of_peak_sustained_elapsed',
-        'dram__throughput.avg.pct_of_peak_sustained_elapsed']
+        'dram__throughput.avg.pct_of_peak_sustained_elapsed', 'l1tex__t_bytes.sum',
+        'lts__t_bytes.sum', 'smsp__thread_inst_executed.sum']
 
 
 def raw(rep):

@@ -1,5 +1,7 @@
-"""Record ncu DRAM traffic (and instruction counts) of a trace kernel capture in
-profiles/ncu_traffic.json, keyed "<config>:<query>:<isect>", for bench.py's roofline.traffic.
+"""Record ncu DRAM traffic, L1/L2 bytes and instruction counts of a trace kernel capture in
+profiles/ncu_traffic.json, keyed "<config>:<query>:<isect>" — bench.py's roofline fallback
+when its live ncu probe cannot run; used only while `source_sha` equals the current
+kernel sources' hash (bench.source_hash), so a kernel change never reuses stale counters.
 
     python tools/update_traffic.py <report.ncu-rep> <key> <profile summary path>"""
 import json
@@ -8,6 +10,9 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import raw  # noqa: E402
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from bench import source_hash  # noqa: E402
 
 rep, key, src = sys.argv[1], sys.argv[2], sys.argv[3]
 d = raw(rep)[0]
@@ -24,6 +29,10 @@ db[key] = {
     "simt_threads_per_inst": float(d["smsp__thread_inst_executed_per_inst_executed.ratio"][0]),
     "kernel": d["kernel"],
     "source": src,
+    "source_sha": source_hash(),
 }
+for k in ("l1tex__t_bytes.sum", "lts__t_bytes.sum"):
+    if k in d:
+        db[key][k] = int(mb(k))
 json.dump(db, open(path, "w"), indent=2)
 print(key, db[key])

@@ -18,6 +18,7 @@ from .gen import (  # noqa: F401
     quad_pair_scene,
     quad_pair_rays,
     tree_textures,
+    stress_textures,
     forest_scene,
     heightfield_scene,
     c4_scene,

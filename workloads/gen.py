@@ -200,6 +200,26 @@ def tree_textures(k: int = 16, size: int = 1024, seed: int = 2, discs: int = 48)
     return out
 
 
+def stress_textures(k: int = 1024, size: int = 1024, seed: int = 2, base: int = 64) -> list:
+    """SURVEY.md §8(c) A25 stress variant: K distinct RGBA8 tree masks (K = 1024 at 1024²
+    is 4 GiB), so texel reads of C2 reach HBM.  `base` masks come from the C2 recipe; mask i
+    is base i mod `base`, rolled sideways by a seeded offset and mirrored when (i // base)
+    is odd — the canopy/trunk/rim statistics of C2, every mask distinct."""
+    bases = tree_textures(base, size, seed)
+    rng = np.random.default_rng(seed + 1000)
+    per = -(-k // base)   # variants per base mask, each with its own distinct shift
+    shifts = np.stack([rng.permutation(np.arange(1, size))[:per] for _ in range(base)])
+    out = []
+    for i in range(k):
+        t = bases[i % base]
+        if i >= base:
+            t = np.roll(t, int(shifts[i % base, i // base]), axis=1)
+            if (i // base) % 2:
+                t = t[:, ::-1]
+        out.append(np.ascontiguousarray(t))
+    return out
+
+
 def white_texture() -> np.ndarray:
     return np.full((1, 1, 4), 255, dtype=np.uint8)
 
@@ -422,6 +442,8 @@ CONFIGS = {
     "C3": "C2 scene, procedural vs default vs no intersector (zero-cost check)",
     "C4": "1M-triangle terrain + 20k billboards, 1920×1080, counting intersector",
     "C5": "10M-triangle terrain + 100k billboards, 3840×2160×4 spp",
+    "C2K": "C2 with K = 1024 distinct 1024×1024 RGBA alpha textures (4 GiB; SURVEY A25 HBM-stress "
+           "variant), 1920×1080 primary rays",
 }
 
 
@@ -517,6 +539,7 @@ CAMERAS = {
     "C3": ((0.0, 4.0, -280.0), (0.0, 4.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
     "C4": ((0.0, 40.0, -300.0), (0.0, 0.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
     "C5": ((0.0, 60.0, -1100.0), (0.0, 10.0, 0.0), (0.0, 1.0, 0.0), 45.0, 3840, 2160, 4),
+    "C2K": ((0.0, 4.0, -280.0), (0.0, 4.0, 0.0), (0.0, 1.0, 0.0), 45.0, 1920, 1080, 1),
 }
 
 
@@ -525,6 +548,8 @@ def scene(name: str, textures=None) -> Scene:
         return quad_pair_scene()
     if name in ("C2", "C3"):
         return forest_scene(textures=textures)
+    if name == "C2K":
+        return forest_scene(textures=textures if textures is not None else stress_textures())
     if name == "C4":
         return c4_scene(textures=textures)
     if name == "C5":
