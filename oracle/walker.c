@@ -245,15 +245,40 @@ void oracle_bvh_free(or_bvh* b) {
 
 /* ====================== contract walker C ================================== */
 
-/* Slab test of App. A.2 (no FMA: -ffp-contract=off).  Box hook default. */
+/* Slab test of App. A.2, contract r02 (DESIGN.md §3 A.2): each plane crossing is
+ * ONE explicit fused multiply-add t = fmaf(plane, inv, noi) with noi = -(o*inv)
+ * (rounded once, clamped to +-FLT_MAX); tf is widened by (1 + 2 gamma_3) and by
+ * pad = 4 max_k |e_k|, e_k = fmaf(o_k, inv_k, noi_k) being noi_k's exact rounding
+ * error (the fma form's absolute error allowance), and tn is compared against
+ * best_t + pad.  No implicit contraction (-ffp-contract=off): every fma here is
+ * written out.  Box hook default. */
+static float clamp_noi(float x) { return fminf(fmaxf(x, -3.40282347e38f), 3.40282347e38f); }
+
+static void slab_consts(const float* o, const float* inv, float* noi, float* pad) {
+  float e[3];
+  for (int a = 0; a < 3; ++a) noi[a] = clamp_noi(-(o[a] * inv[a]));
+  for (int a = 0; a < 3; ++a) e[a] = fmaf(o[a], inv[a], noi[a]);
+  *pad = fmaxf(fmaxf(fabsf(e[0]), fabsf(e[1])), fabsf(e[2])) * 4.0f;
+}
+
+/* the culling bound of the box test and of the pop skip: best_t + pad */
+static float cull_bound(const float* o, const float* inv, float best_t) {
+  float noi[3], pad;
+  slab_consts(o, inv, noi, &pad);
+  return best_t + pad;
+}
+
 static int slab(const float* lo, const float* hi, const float* o, const float* inv, float tmin,
                 float best_t, float* tn_out) {
-  float t0x = (lo[0] - o[0]) * inv[0], t1x = (hi[0] - o[0]) * inv[0];
-  float t0y = (lo[1] - o[1]) * inv[1], t1y = (hi[1] - o[1]) * inv[1];
-  float t0z = (lo[2] - o[2]) * inv[2], t1z = (hi[2] - o[2]) * inv[2];
+  float noi[3], pad;
+  slab_consts(o, inv, noi, &pad);
+  float t0x = fmaf(lo[0], inv[0], noi[0]), t1x = fmaf(hi[0], inv[0], noi[0]);
+  float t0y = fmaf(lo[1], inv[1], noi[1]), t1y = fmaf(hi[1], inv[1], noi[1]);
+  float t0z = fmaf(lo[2], inv[2], noi[2]), t1z = fmaf(hi[2], inv[2], noi[2]);
   float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), tmin));
-  float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
-  tf = fminf(tf, best_t);
+  float tf = fmaf(fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)), 1.0000003576f,
+                  pad);
+  tf = fminf(tf, best_t + pad);
   *tn_out = tn;
   return tn <= tf;
 }
@@ -267,10 +292,12 @@ int walker_slab(const float* lo, const float* hi, const float* ray, float best_t
     float dk = ray[4 + a];
     inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
   }
-  float t0x = (lo[0] - ray[0]) * inv[0], t1x = (hi[0] - ray[0]) * inv[0];
-  float t0y = (lo[1] - ray[1]) * inv[1], t1y = (hi[1] - ray[1]) * inv[1];
-  float t0z = (lo[2] - ray[2]) * inv[2], t1z = (hi[2] - ray[2]) * inv[2];
-  *tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)) * 1.0000003576f;
+  float noi[3], pad;
+  slab_consts(ray, inv, noi, &pad);
+  float t0x = fmaf(lo[0], inv[0], noi[0]), t1x = fmaf(hi[0], inv[0], noi[0]);
+  float t0y = fmaf(lo[1], inv[1], noi[1]), t1y = fmaf(hi[1], inv[1], noi[1]);
+  float t0z = fmaf(lo[2], inv[2], noi[2]), t1z = fmaf(hi[2], inv[2], noi[2]);
+  *tf = fmaf(fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fmaxf(t0z, t1z)), 1.0000003576f, pad);
   return slab(lo, hi, ray, inv, ray[3], best_t, tn);
 }
 
@@ -472,7 +499,7 @@ static int walk_one(const wjob_t* jb, uint64_t r) {
     for (;;) {
       if (sp == 0) goto next_bvh;
       sp--;
-      if (st_tn[sp] > best_t) continue;
+      if (st_tn[sp] > cull_bound(o, inv, best_t)) continue;
       cur = st_ref[sp];
       break;
     }
@@ -706,7 +733,7 @@ static int walk_bottom(const ijob_t* jb, const or_bvh* b, const float* ray, ista
     for (;;) {
       if (sp == 0) return 0;
       sp--;
-      if (st_tn[sp] > S->best_t) continue;
+      if (st_tn[sp] > cull_bound(o, inv, S->best_t)) continue;
       cur = st_ref[sp];
       break;
     }
@@ -784,7 +811,7 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
     for (;;) {
       if (sp == 0) goto done;
       sp--;
-      if (st_tn[sp] > S.best_t) continue;
+      if (st_tn[sp] > cull_bound(o, inv, S.best_t)) continue;
       cur = st_ref[sp];
       break;
     }

@@ -51,12 +51,34 @@ __device__ __forceinline__ f2_t mul2(f2_t a, f2_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
+// a * b + c with ONE rounding per lane (FFMA2): the slab contract's explicit fma
+__device__ __forceinline__ f2_t fma2(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
 
 struct RayCtx {
   float ox, oy, oz, tmin;
   float dx, dy, dz;
   float ix, iy, iz;          // guarded reciprocal direction (reading A20)
+  float nx, ny, nz;          // noi = -(o * inv), clamped to +-FLT_MAX (slab contract r02)
+  float pad;                 // 4 max_k |o_k inv_k + noi_k|: the fma-form slab's allowance
 };
+
+// Slab contract r02 (DESIGN.md §3 A.2): a box plane's crossing is ONE fused
+// multiply-add, t = fma(plane, inv, noi) with noi = -(o * inv) rounded once per
+// ray, instead of (plane - o) * inv.  Error: with e_k = o_k inv_k + noi_k the
+// EXACT rounding error of noi_k (fma(o, inv, noi) computes it exactly),
+// t = (t*(1+d0) + e)(1+d2): <= 2u relative (covered by the tf widening
+// 1 + 2 gamma_3, as before) plus the absolute e, covered by `pad` = 4 max_k |e_k|
+// added to tf and to the best_t bound.  Axes with a power-of-two inv (axis-
+// parallel rays' guarded 2^80, unit directions) have e = 0.  The clamp keeps every
+// value finite (no NaN for any finite input); an overflowing origin term makes
+// e, hence pad, infinite: the test then never culls (conservative).
+__device__ __forceinline__ float clamp_noi(float x) {
+  return fminf(fmaxf(x, -3.40282347e38f), 3.40282347e38f);
+}
 
 __device__ __forceinline__ void make_ray(RayCtx& r, float4 a, float4 b) {
   r.ox = a.x; r.oy = a.y; r.oz = a.z; r.tmin = a.w;
@@ -64,6 +86,12 @@ __device__ __forceinline__ void make_ray(RayCtx& r, float4 a, float4 b) {
   r.ix = 1.0f / (fabsf(b.x) > 0x1p-80f ? b.x : copysignf(0x1p-80f, b.x));
   r.iy = 1.0f / (fabsf(b.y) > 0x1p-80f ? b.y : copysignf(0x1p-80f, b.y));
   r.iz = 1.0f / (fabsf(b.z) > 0x1p-80f ? b.z : copysignf(0x1p-80f, b.z));
+  r.nx = clamp_noi(-(a.x * r.ix));
+  r.ny = clamp_noi(-(a.y * r.iy));
+  r.nz = clamp_noi(-(a.z * r.iz));
+  const float ex = __fmaf_rn(a.x, r.ix, r.nx), ey = __fmaf_rn(a.y, r.iy, r.ny),
+              ez = __fmaf_rn(a.z, r.iz, r.nz);
+  r.pad = fmaxf(fmaxf(fabsf(ex), fabsf(ey)), fabsf(ez)) * 4.0f;
 }
 
 // Three-input min/max (sm_100 FMNMX3).  min/max are exact and, NaN operands
@@ -115,44 +143,53 @@ __device__ __forceinline__ float4 ldg4(const void* p) {
 // Default primitive tests (the `intersect` customization points).
 // ---------------------------------------------------------------------------
 
+// The culling bound a box test compares tn against: best_t plus the slab's
+// absolute error allowance (contract r02), so a box holding a hit at t <= best_t
+// is never culled.  Loop-invariant in the inner-node loop (best_t only changes
+// in the leaf loop), so it is computed once per descent.
+__device__ __forceinline__ float cull_t(const RayCtx& r, float best_t) { return best_t + r.pad; }
+
 // Ray/AABB slab test with the caller-supplied inverse direction (the "special
 // interface" of PAPER.md:371-376), clipped to [tmin, best_t]; tf widened by
-// (1 + 2*gamma_3) (reading A23).  min/max are exact, so their order is free.
+// (1 + 2*gamma_3) (reading A23) plus `pad` (contract r02).  min/max are exact,
+// so their order is free.
 __device__ __forceinline__ bool intersect(const RayCtx& r, const Aabb& b, float best_t,
                                           float& tn) {
-  const float t0x = (b.lx - r.ox) * r.ix, t1x = (b.hx - r.ox) * r.ix;
-  const float t0y = (b.ly - r.oy) * r.iy, t1y = (b.hy - r.oy) * r.iy;
-  const float t0z = (b.lz - r.oz) * r.iz, t1z = (b.hz - r.oz) * r.iz;
+  const float t0x = __fmaf_rn(b.lx, r.ix, r.nx), t1x = __fmaf_rn(b.hx, r.ix, r.nx);
+  const float t0y = __fmaf_rn(b.ly, r.iy, r.ny), t1y = __fmaf_rn(b.hy, r.iy, r.ny);
+  const float t0z = __fmaf_rn(b.lz, r.iz, r.nz), t1z = __fmaf_rn(b.hz, r.iz, r.nz);
   const float n = fmax3(fminf(t0x, t1x), fminf(t0y, t1y), fmaxf(fminf(t0z, t1z), r.tmin));
-  float f = fmin3(fmaxf(t0x, t1x), fmaxf(t0y, t1y), fmaxf(t0z, t1z)) * 1.0000003576f;
-  f = fminf(f, best_t);
+  float f = __fmaf_rn(fmin3(fmaxf(t0x, t1x), fmaxf(t0y, t1y), fmaxf(t0z, t1z)), 1.0000003576f,
+                      r.pad);
+  f = fminf(f, cull_t(r, best_t));
   tn = n;
   return n <= f;
 }
 
-// The same test on both children of a pair node at once: every sub/mul is the
-// scalar contract's operation, done two at a time (FADD2/FMUL2).
+// The same test on both children of a pair node at once: every fma is the
+// scalar contract's operation, done two at a time (FFMA2).
 __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair& b,
                                                 float best_t) {
   float t0x0, t0x1, t1x0, t1x1, t0y0, t0y1, t1y0, t1y1, t0z0, t0z1, t1z0, t1z1;
-  // (o.k, o.k) and (inv.k, inv.k) are broadcast operands (SASS ".F32" form)
-  const f2_t ox2 = pk(r.ox, r.ox), oy2 = pk(r.oy, r.oy), oz2 = pk(r.oz, r.oz);
+  // (noi.k, noi.k) and (inv.k, inv.k) are broadcast operands (SASS ".F32" form)
+  const f2_t nx2 = pk(r.nx, r.nx), ny2 = pk(r.ny, r.ny), nz2 = pk(r.nz, r.nz);
   const f2_t ix2 = pk(r.ix, r.ix), iy2 = pk(r.iy, r.iy), iz2 = pk(r.iz, r.iz);
-  upk(mul2(sub2(pk(b.x.x, b.x.y), ox2), ix2), t0x0, t0x1);
-  upk(mul2(sub2(pk(b.x.z, b.x.w), ox2), ix2), t1x0, t1x1);
-  upk(mul2(sub2(pk(b.y.x, b.y.y), oy2), iy2), t0y0, t0y1);
-  upk(mul2(sub2(pk(b.y.z, b.y.w), oy2), iy2), t1y0, t1y1);
-  upk(mul2(sub2(pk(b.z.x, b.z.y), oz2), iz2), t0z0, t0z1);
-  upk(mul2(sub2(pk(b.z.z, b.z.w), oz2), iz2), t1z0, t1z1);
+  upk(fma2(pk(b.x.x, b.x.y), ix2, nx2), t0x0, t0x1);
+  upk(fma2(pk(b.x.z, b.x.w), ix2, nx2), t1x0, t1x1);
+  upk(fma2(pk(b.y.x, b.y.y), iy2, ny2), t0y0, t0y1);
+  upk(fma2(pk(b.y.z, b.y.w), iy2, ny2), t1y0, t1y1);
+  upk(fma2(pk(b.z.x, b.z.y), iz2, nz2), t0z0, t0z1);
+  upk(fma2(pk(b.z.z, b.z.w), iz2, nz2), t1z0, t1z1);
   BoxPairHit h;
   h.tn0 = fmax3(fminf(t0x0, t1x0), fminf(t0y0, t1y0), fmaxf(fminf(t0z0, t1z0), r.tmin));
   h.tn1 = fmax3(fminf(t0x1, t1x1), fminf(t0y1, t1y1), fmaxf(fminf(t0z1, t1z1), r.tmin));
   const float f0 = fmin3(fmaxf(t0x0, t1x0), fmaxf(t0y0, t1y0), fmaxf(t0z0, t1z0));
   const float f1 = fmin3(fmaxf(t0x1, t1x1), fmaxf(t0y1, t1y1), fmaxf(t0z1, t1z1));
   float g0, g1;
-  upk(mul2(pk(f0, f1), pk(1.0000003576f, 1.0000003576f)), g0, g1);
-  h.h0 = h.tn0 <= fminf(g0, best_t);
-  h.h1 = h.tn1 <= fminf(g1, best_t);
+  upk(fma2(pk(f0, f1), pk(1.0000003576f, 1.0000003576f), pk(r.pad, r.pad)), g0, g1);
+  const float bt = cull_t(r, best_t);
+  h.h0 = h.tn0 <= fminf(g0, bt);
+  h.h1 = h.tn1 <= fminf(g1, bt);
   return h;
 }
 
@@ -163,35 +200,37 @@ template <int OCT>
 struct octant {};
 
 // Octant-specialised pair slab test.  With lo <= hi (validated on import) and
-// inv never 0 or NaN (guarded reciprocal), IEEE rounding is monotone, so
-// min((lo-o)*inv, (hi-o)*inv) is exactly the near-plane term and max the far
-// one: selecting the planes at compile time gives bit-identical tn/tf to the
-// generic test above without its 12 per-axis min/max.
+// inv never 0 or NaN (guarded reciprocal), the exact products lo*inv and hi*inv
+// are ordered, the addend noi is shared and rounding is monotone, so
+// min(fma(lo,inv,noi), fma(hi,inv,noi)) is exactly the near-plane term and max
+// the far one: selecting the planes at compile time gives bit-identical tn/tf to
+// the generic test above without its 12 per-axis min/max.
 template <int OCT>
 __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair& b, float best_t,
                                                 octant<OCT>) {
   constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
-  const f2_t ox2 = pk(r.ox, r.ox), oy2 = pk(r.oy, r.oy), oz2 = pk(r.oz, r.oz);
+  const f2_t nx2 = pk(r.nx, r.nx), ny2 = pk(r.ny, r.ny), nz2 = pk(r.nz, r.nz);
   const f2_t ix2 = pk(r.ix, r.ix), iy2 = pk(r.iy, r.iy), iz2 = pk(r.iz, r.iz);
   const f2_t lox = pk(b.x.x, b.x.y), hix = pk(b.x.z, b.x.w);
   const f2_t loy = pk(b.y.x, b.y.y), hiy = pk(b.y.z, b.y.w);
   const f2_t loz = pk(b.z.x, b.z.y), hiz = pk(b.z.z, b.z.w);
   float nx0, nx1, fx0, fx1, ny0, ny1, fy0, fy1, nz0, nz1, fz0, fz1;
-  upk(mul2(sub2(sx ? hix : lox, ox2), ix2), nx0, nx1);
-  upk(mul2(sub2(sx ? lox : hix, ox2), ix2), fx0, fx1);
-  upk(mul2(sub2(sy ? hiy : loy, oy2), iy2), ny0, ny1);
-  upk(mul2(sub2(sy ? loy : hiy, oy2), iy2), fy0, fy1);
-  upk(mul2(sub2(sz ? hiz : loz, oz2), iz2), nz0, nz1);
-  upk(mul2(sub2(sz ? loz : hiz, oz2), iz2), fz0, fz1);
+  upk(fma2(sx ? hix : lox, ix2, nx2), nx0, nx1);
+  upk(fma2(sx ? lox : hix, ix2, nx2), fx0, fx1);
+  upk(fma2(sy ? hiy : loy, iy2, ny2), ny0, ny1);
+  upk(fma2(sy ? loy : hiy, iy2, ny2), fy0, fy1);
+  upk(fma2(sz ? hiz : loz, iz2, nz2), nz0, nz1);
+  upk(fma2(sz ? loz : hiz, iz2, nz2), fz0, fz1);
   BoxPairHit h;
   h.tn0 = fmax3(nx0, ny0, fmaxf(nz0, r.tmin));
   h.tn1 = fmax3(nx1, ny1, fmaxf(nz1, r.tmin));
   float g0, g1;
-  upk(mul2(pk(fmin3(fx0, fy0, fz0), fmin3(fx1, fy1, fz1)),
-           pk(1.0000003576f, 1.0000003576f)),
+  upk(fma2(pk(fmin3(fx0, fy0, fz0), fmin3(fx1, fy1, fz1)),
+           pk(1.0000003576f, 1.0000003576f), pk(r.pad, r.pad)),
       g0, g1);
-  h.h0 = h.tn0 <= fminf(g0, best_t);
-  h.h1 = h.tn1 <= fminf(g1, best_t);
+  const float bt = cull_t(r, best_t);
+  h.h0 = h.tn0 <= fminf(g0, bt);
+  h.h1 = h.tn1 <= fminf(g1, bt);
   return h;
 }
 

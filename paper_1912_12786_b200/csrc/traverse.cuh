@@ -56,12 +56,14 @@ struct Trav {
   int sp;
 };
 
-// Pop the next entry not farther than the current best (reading A14).
+// Pop the next entry not farther than the current best (reading A14), with the
+// same culling bound as the box test (best_t + pad, contract r02).
 __device__ __forceinline__ bool pop(Trav& T, const float2* stack) {
+  const float bt = cull_t(T.r, T.best_t);
   while (T.sp > 0) {
     --T.sp;
     const float2 e = stack[T.sp];
-    if (e.y <= T.best_t) {
+    if (e.y <= bt) {
       T.cur = __float_as_uint(e.x);
       return true;
     }

@@ -69,12 +69,43 @@ def test_intersector_code_only_where_used(sass, q):
     assert any(indirect.match(i) for i in fnptr)
 
 
-def test_no_packed_fma_contraction(sass):
-    """The arithmetic contract forbids FMA contraction.  ptxas fuses a packed
-    f32x2 multiply feeding a packed add into FFMA2 even under --fmad=false, so the kernels only
-    use packed products whose consumers are not packed adds (slab: sub then mul; MT: FMUL2 then
-    scalar sums).  Any FFMA2 in the library would break bit-exact parity."""
-    bad = [name for name, ins in sass.items() if any(i.split()[0].lstrip("@!P0123456789 ")
-                                                     .startswith("FFMA2") or " FFMA2 " in f" {i} "
-                                                     for i in ins)]
+@pytest.fixture(scope="module")
+def trace_ptx(tmp_path_factory):
+    """PTX of trace.cu (the library embeds SASS only), built with the library's flags."""
+    import os
+    from paper_1912_12786_b200 import _build
+    out = str(tmp_path_factory.mktemp("ptx") / "trace.ptx")
+    cmd = [_build.nvcc(), "-O3", "-std=c++17", *_build.ARCH, "-fmad=false", "-prec-div=true",
+           "-prec-sqrt=true", "-ftz=false", "-I", os.path.join(_build.ROOT, "include"), "-ptx",
+           "-o", out, os.path.join(_build.CSRC, "trace.cu")]
+    subprocess.run(cmd, check=True, capture_output=True)
+    return open(out).read()
+
+
+def test_no_packed_fma_contraction(trace_ptx):
+    """The arithmetic contract forbids IMPLICIT FMA contraction.  The slab
+    test's fused multiply-adds are explicit (contract r02: t = fma(plane, inv, noi) and
+    tf = fma(tf, 1 + 2 gamma_3, pad), `fma.rn.f32x2` in the PTX).  ptxas fuses a packed
+    f32x2 multiply whose result feeds a packed add/sub into FFMA2 even under --fmad=false,
+    so no `mul.rn.f32x2` result may be an operand of an `add`/`sub.rn.f32x2` (MT's packed
+    products feed scalar sums); that dataflow is checked on the PTX of every kernel."""
+    prods, bad = set(), []
+    for line in trace_ptx.splitlines():
+        t = line.strip()
+        if ".entry " in t or ".func " in t:
+            prods = set()
+        m = re.match(r"mul\.rn\.f32x2\s+(%rd\d+)", t)
+        if m:
+            prods.add(m.group(1))
+            continue
+        m = re.match(r"(add|sub)\.rn\.f32x2\s+%rd\d+,\s*(%rd\d+),\s*(%rd\d+)", t)
+        if m and (m.group(2) in prods or m.group(3) in prods):
+            bad.append(t)
+    assert "fma.rn.f32x2" in trace_ptx
     assert not bad, bad[:3]
+
+
+def test_slab_uses_explicit_fma(sass):
+    """Contract r02: the pair-node slab is FFMA2 (one rounding per plane), not FADD2+FMUL2."""
+    body = _find(sass, 1, "19default_intersector")
+    assert sum(1 for i in body if "FFMA2" in i) >= 7

@@ -16,7 +16,8 @@ import tempfile
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ORACLE = os.path.join(ROOT, "oracle")
 PINS = ["tests/test_oracle_pins.py", "tests/test_oracle_multi.py", "tests/test_oracle_list.py",
-        "tests/test_instances_cpu.py", "tests/test_oracle_variants.py", "tests/test_oracle_flags.py"]
+        "tests/test_instances_cpu.py", "tests/test_oracle_variants.py", "tests/test_oracle_flags.py",
+        "tests/test_oracle_slab_r02.py"]
 
 MUTANTS = [
     # (file, original, mutated, description)
@@ -57,7 +58,7 @@ MUTANTS = [
     ("walker.c", "if (tn1 < tn0) { nearr = nd->ref[1]; farr = nd->ref[0]; ftn = tn0; }",
      "if (tn1 > tn0) { nearr = nd->ref[1]; farr = nd->ref[0]; ftn = tn0; }", "walker: far child first"),
     ("walker.c", "      c.boxes += 2;", "      c.boxes += 1;", "walker: one box count per inner node"),
-    ("walker.c", "      if (st_tn[sp] > best_t) continue;", "", "walker: popped entries never culled"),
+    ("walker.c", "      if (st_tn[sp] > cull_bound(o, inv, best_t)) continue;", "", "walker: popped entries never culled"),
     ("walker.c", "  c.boxes++;\n  if (!slab(b->root_lo", "  if (!slab(b->root_lo", "walker: root test not counted"),
     ("walker.c", "        if (jb->isect == OR_ALPHA_TEX) c.alpha++;", "", "walker: alpha lookups not counted"),
     ("walker.c", "ax[a][c] = lo[a];\n    ax[a][2 + c] = hi[a];", "ax[a][2 + c] = lo[a];\n    ax[a][c] = hi[a];",
@@ -91,6 +92,17 @@ MUTANTS = [
      "instance multi-hit: instance index not moved with its hit"),
     ("walker.c", "            if (S->nk == S->K) S->best_t = S->mb[S->K - 1].t;\n", "",
      "instance multi-hit: a full buffer does not shrink tmax"),
+    # ---- slab contract r02 (round 2: tests/test_oracle_slab_r02.py) ----
+    ("walker.c", "  *pad = fmaxf(fmaxf(fabsf(e[0]), fabsf(e[1])), fabsf(e[2])) * 4.0f;", "  *pad = 0.0f;",
+     "slab r02: no allowance for the fma form's absolute error"),
+    ("walker.c", "  tf = fminf(tf, best_t + pad);", "  tf = fminf(tf, best_t);",
+     "slab r02: best_t bound without the allowance"),
+    ("walker.c", "  float t0x = fmaf(lo[0], inv[0], noi[0]), t1x = fmaf(hi[0], inv[0], noi[0]);",
+     "  float t0x = (lo[0] - o[0]) * inv[0], t1x = (hi[0] - o[0]) * inv[0];",
+     "slab r02: x planes in the round-1 sub-mul form"),
+    ("walker.c", "  for (int a = 0; a < 3; ++a) e[a] = fmaf(o[a], inv[a], noi[a]);",
+     "  for (int a = 0; a < 3; ++a) e[a] = o[a] * inv[a] + noi[a];",
+     "slab r02: rounding error of noi taken from an unfused sum (always 0)"),
     # ---- ambiguity flags X1-X5 (round 2: tests/test_oracle_flags.py) ----
     ("oracle.c", "(double)second_t - (double)best.t < 1e-5 * fabs((double)best.t))",
      "(double)second_t - (double)best.t < 1e-7 * fabs((double)best.t))", "X1: tie band 100x too narrow"),
