@@ -136,7 +136,9 @@ __device__ __forceinline__ void write_multi(const TraceParams& p, uint64_t id,
                                             const MultiBuf<K, true>& mb, const I& isect) {
   float4* out = p.hits + id * (uint64_t)p.max_hits;
   uint32_t* wout = p.which ? p.which + id * (uint64_t)p.max_hits : nullptr;
-  for (int j = 0; j < mb.maxk; ++j) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) {   // static indices: the buffer stays in registers
+    if (j >= mb.maxk) break;
     const bool kept = j < mb.n;
     out[j] = kept ? make_float4(mb.t[j], mb.u[j], mb.v[j], __uint_as_float(mb.prim[j]))
                   : make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f, __uint_as_float(kMissPrim));

@@ -26,6 +26,10 @@
 
 #include "layout.hpp"
 
+#ifndef VSR_LDG256
+#define VSR_LDG256 1   // 0: 128-bit loads only (A/B builds)
+#endif
+
 namespace vsr {
 
 // ---------------------------------------------------------------------------
@@ -137,6 +141,33 @@ struct hit_record {
 
 __device__ __forceinline__ float4 ldg4(const void* p) {
   return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// 256-bit read-only load (sm_100 LDG.E.ENL2.256): 32 B per lane in ONE load
+// instruction — a 64-B pair node is two loads instead of four, halving the
+// L1 data-pipe wavefronts of a divergent warp's node fetch.  `p` 32-B aligned.
+__device__ __forceinline__ void ldg8(const void* p, float4& a, float4& b) {
+#if VSR_LDG256
+  asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+#else
+  a = __ldg(reinterpret_cast<const float4*>(p));
+  b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+#endif
+}
+// the same without L1 allocation (streamed data read once: rays)
+__device__ __forceinline__ void ldg8_na(const void* p, float4& a, float4& b) {
+#if VSR_LDG256
+  asm("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+      : "l"(p));
+#else
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(p));
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(reinterpret_cast<const float4*>(p) + 1));
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -33,6 +33,50 @@
 
 namespace vsr {
 
+#ifndef VSR_INST_COST
+#define VSR_INST_COST 1   // 0: instanced queries keep the flat-scene length proxy (A/B builds)
+#endif
+// Cost proxy of an INSTANCED query (p.instances set, p.scene = the top level):
+// the number of instance world boxes the ray's [tmin, tmax] segment enters,
+// capped at kOrderBuckets - 1.  The length of the segment inside the union of
+// all instances (the flat-scene proxy) barely separates a ray that crosses a
+// dense cluster of instances from one that crosses open ground, so the
+// longest-first order needs the top level itself (measured: the instanced
+// forest's tail).  No best_t pruning: this estimates the work.
+__device__ uint32_t instance_cost(const TraceParams& p, const RayCtx& r, float tmax) {
+  const DevScene& S = p.scene;
+  const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
+  float tn;
+  if (!intersect(r, root, tmax, tn)) return 0u;
+  uint32_t stack[kMaxStack];
+  int sp = 0;
+  uint32_t cur = S.root_ref, cnt = 0;
+  const uint32_t cap = kOrderBuckets - 1;
+  for (;;) {
+    if (cur & kLeafBit) {
+      cnt += ((cur >> kLeafCountShift) & 31u) + 1u;
+      if (cnt >= cap || sp == 0) break;
+      cur = stack[--sp];
+      continue;
+    }
+    const float4* np = reinterpret_cast<const float4*>(S.nodes + cur);
+    const BoxPairHit h = intersect(r, AabbPair{__ldg(np), __ldg(np + 1), __ldg(np + 2)}, tmax);
+    const float4 nr = __ldg(np + 3);
+    const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
+    if (h.h0 && h.h1) {
+      stack[sp++] = r1;
+      cur = r0;
+    } else if (h.h0 || h.h1) {
+      cur = h.h0 ? r0 : r1;
+    } else if (sp > 0) {
+      cur = stack[--sp];
+    } else {
+      break;
+    }
+  }
+  return cnt < cap ? cnt : cap;
+}
+
 template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
@@ -52,7 +96,8 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
       const float t0z = (p.scene.root_lo[2] - r.oz) * r.iz, t1z = (p.scene.root_hi[2] - r.oz) * r.iz;
       const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
       const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
-      if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+      if (VSR_INST_COST && p.instances) len = (float)instance_cost(p, r, d.w);   // bucket index directly
+      else if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
     }
   }
   len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 1));
@@ -70,7 +115,7 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
     const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
     const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
     const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
-    q = diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
+    q = (VSR_INST_COST && p.instances) ? (int)len : diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
     q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
     lpos = atomicAdd(lh + q, 1u);
   }
@@ -175,10 +220,12 @@ __global__ void __launch_bounds__(kBlock, VSR_MULTI_MINB) trace_multi_kernel(con
   const int woct = __match_any_sync(live, oct) == live ? oct : 8;
   if (go) traverse<kMulti>(p.scene, T, isect, stack, woct, mb);
   float4* out = p.hits + id * (uint64_t)p.max_hits;
-  for (int j = 0; j < mb.maxk; ++j) {
-    out[j] = j < mb.n ? make_float4(mb.t[j], mb.u[j], mb.v[j], __uint_as_float(mb.prim[j]))
-                      : make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
-                                    __uint_as_float(kMissPrim));
+#pragma unroll
+  for (int j = 0; j < K; ++j) {   // static indices: the buffer stays in registers
+    if (j < mb.maxk)
+      out[j] = j < mb.n ? make_float4(mb.t[j], mb.u[j], mb.v[j], __uint_as_float(mb.prim[j]))
+                        : make_float4(__int_as_float(0x7f800000), 0.0f, 0.0f,
+                                      __uint_as_float(kMissPrim));
   }
   if (p.num_hits) p.num_hits[id] = (uint32_t)mb.n;
   if constexpr (I::kCounts) {

@@ -143,11 +143,7 @@ __device__ __forceinline__ void fetch_ray(const TraceParams& p, uint64_t id, flo
   } else {
 #if VSR_RAY_NA
     // rays are read once: no L1 allocation, so they do not evict node lines
-    const float4* rp = p.rays + 2 * id;
-    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(rp));
-    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
-        : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(rp + 1));
+    ldg8_na(p.rays + 2 * id, a, b);
 #else
     a = __ldg(p.rays + 2 * id);
     b = __ldg(p.rays + 2 * id + 1);
@@ -195,7 +191,9 @@ template <int OCT, class I, class SE>
 __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, SE* stack) {
   while (!(T.cur & kLeafBit)) {
     const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
-    const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2), nr = __ldg(np + 3);
+    float4 nx, ny, nz, nr;
+    ldg8(np, nx, ny);
+    ldg8(np + 2, nz, nr);
 #if VSR_PREFETCH
     // both children towards L1 while the box tests run (scheduling only)
     prefetch_ref(S, __float_as_uint(nr.x));
@@ -235,6 +233,67 @@ struct MultiBuf {
   int maxk;
 };
 
+// Stable insertion by t into the sorted buffer (equal t keep discovery order); a
+// full buffer drops its worst, then tmax shrinks to the new worst.  For K <= 8
+// every array index is a compile-time constant (the insertion is a carry that
+// walks the K slots: at the first slot holding a larger t it swaps in, every
+// later occupied slot shifts, the first empty slot absorbs the carry), so the
+// buffer lives in registers instead of local memory.
+#ifndef VSR_MULTI_REG
+#define VSR_MULTI_REG 1   // 0: the round-1 dynamic-index insertion (A/B builds)
+#endif
+template <int K, bool SRC>
+__device__ __forceinline__ void multi_insert(MultiBuf<K, SRC>& mb, Trav& T, float t, float u,
+                                             float v, uint32_t prim) {
+  if constexpr (K <= 8 && VSR_MULTI_REG) {
+    float ct = t, cu = u, cv = v;
+    uint32_t cp = prim, cs = mb.cur_src;
+    bool carry = true, shifting = false;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < mb.maxk) {
+        const bool occ = j < mb.n;
+        if (carry && (!occ || shifting || mb.t[j] > ct)) {
+          const float t0 = mb.t[j], u0 = mb.u[j], v0 = mb.v[j];
+          const uint32_t p0 = mb.prim[j];
+          mb.t[j] = ct; mb.u[j] = cu; mb.v[j] = cv; mb.prim[j] = cp;
+          ct = t0; cu = u0; cv = v0; cp = p0;
+          if constexpr (SRC) {
+            const uint32_t s0 = mb.src[j];
+            mb.src[j] = cs;
+            cs = s0;
+          }
+          if (occ) shifting = true;
+          else carry = false;
+        }
+      }
+    }
+    if (mb.n < mb.maxk) ++mb.n;
+    if (mb.n == mb.maxk) {
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (j == mb.maxk - 1) T.best_t = mb.t[j];
+    }
+  } else {
+    int pos = mb.n < mb.maxk ? mb.n : mb.maxk - 1;   // a full buffer drops its worst
+    while (pos > 0 && mb.t[pos - 1] > t) {          // stable insertion by t
+      mb.t[pos] = mb.t[pos - 1];
+      mb.u[pos] = mb.u[pos - 1];
+      mb.v[pos] = mb.v[pos - 1];
+      mb.prim[pos] = mb.prim[pos - 1];
+      if constexpr (SRC) mb.src[pos] = mb.src[pos - 1];
+      --pos;
+    }
+    mb.t[pos] = t;
+    mb.u[pos] = u;
+    mb.v[pos] = v;
+    mb.prim[pos] = prim;
+    if constexpr (SRC) mb.src[pos] = mb.cur_src;
+    if (mb.n < mb.maxk) ++mb.n;
+    if (mb.n == mb.maxk) T.best_t = mb.t[mb.maxk - 1];
+  }
+}
+
 // ---- leaf loop: "while node contains untested primitives" ----
 // Returns true when the query is finished (any-hit accepted a primitive).
 template <int Q, class I, class M>
@@ -246,24 +305,8 @@ __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb
     const TriData td{__ldg(tp), __ldg(tp + 1), __ldg(tp + 2)};
     const hit_record hr = tri_hook(isect, T.r, td, k, T.best_t);
     if constexpr (Q == kMulti) {
-      if (hr.hit && (mb.n < mb.maxk || hr.t < T.best_t)) {
-        int pos = mb.n < mb.maxk ? mb.n : mb.maxk - 1;   // a full buffer drops its worst
-        while (pos > 0 && mb.t[pos - 1] > hr.t) {       // stable insertion by t
-          mb.t[pos] = mb.t[pos - 1];
-          mb.u[pos] = mb.u[pos - 1];
-          mb.v[pos] = mb.v[pos - 1];
-          mb.prim[pos] = mb.prim[pos - 1];
-          if constexpr (M::kSrc) mb.src[pos] = mb.src[pos - 1];
-          --pos;
-        }
-        mb.t[pos] = hr.t;
-        mb.u[pos] = hr.u;
-        mb.v[pos] = hr.v;
-        mb.prim[pos] = __float_as_uint(td.a.w);
-        if constexpr (M::kSrc) mb.src[pos] = mb.cur_src;
-        if (mb.n < mb.maxk) ++mb.n;
-        if (mb.n == mb.maxk) T.best_t = mb.t[mb.maxk - 1];
-      }
+      if (hr.hit && (mb.n < mb.maxk || hr.t < T.best_t))
+        multi_insert(mb, T, hr.t, hr.u, hr.v, __float_as_uint(td.a.w));
     } else if (Q == kAny) {
       if (hr.hit) {   // any-hit: the first accepted hit ends the query
         T.best_t = hr.t;
