@@ -27,7 +27,7 @@
 #include "layout.hpp"
 
 #ifndef VSR_LDG256
-#define VSR_LDG256 1   // 0: 128-bit loads only (A/B builds)
+#define VSR_LDG256 0   // 1: 256-bit node / ray loads — measured 3-4.5 % SLOWER (profiles/r02_tuning.md)
 #endif
 
 namespace vsr {

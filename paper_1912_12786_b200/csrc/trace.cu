@@ -34,7 +34,7 @@
 namespace vsr {
 
 #ifndef VSR_INST_COST
-#define VSR_INST_COST 1   // 0: instanced queries keep the flat-scene length proxy (A/B builds)
+#define VSR_INST_COST 0   // 1: instance-box-count proxy — measured 5-18 % SLOWER (profiles/r02_tuning.md)
 #endif
 // Cost proxy of an INSTANCED query (p.instances set, p.scene = the top level):
 // the number of instance world boxes the ray's [tmin, tmax] segment enters,

@@ -240,7 +240,7 @@ struct MultiBuf {
 // later occupied slot shifts, the first empty slot absorbs the carry), so the
 // buffer lives in registers instead of local memory.
 #ifndef VSR_MULTI_REG
-#define VSR_MULTI_REG 1   // 0: the round-1 dynamic-index insertion (A/B builds)
+#define VSR_MULTI_REG 0   // 1: register-resident K <= 8 insertion — measured 6 % SLOWER (profiles/r02_tuning.md)
 #endif
 template <int K, bool SRC>
 __device__ __forceinline__ void multi_insert(MultiBuf<K, SRC>& mb, Trav& T, float t, float u,
