@@ -73,6 +73,9 @@ def parse():
                     help="1: replay the headline trace call from a CUDA graph each step")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--bvh", default="binary", choices=["binary", "wide"],
+                    help="binary: 64-B pair-node SAH BVH (default); wide: the same tree collapsed "
+                         "into the 8-wide compressed BVH (vsr_bvh8_build / vsr_trace_bvh8)")
     ap.add_argument("--max-leaf", type=int, default=2, help="BVH build: max triangles per leaf")
     ap.add_argument("--sah-bins", type=int, default=16, help="BVH build: SAH bins per axis")
     ap.add_argument("--mode", default="weak", choices=["weak", "tiles", "tiles-nccl"],
@@ -254,10 +257,10 @@ def probe_counters(args, timeout=420):
     if not os.path.exists(ncu):
         return None, "ncu not found"
     cmd = [ncu, "--metrics", ",".join(COUNTER_METRICS), "--print-units", "base", "--csv",
-           "--clock-control", "none", "-k", "regex:trace_kernel", "-s", "2", "-c", "1",
+           "--clock-control", "none", "-k", "regex:trace_(wide_)?kernel", "-s", "2", "-c", "1",
            sys.executable, os.path.abspath(__file__), "--probe", "--config", args.config,
            "--query", args.query, "--isect", args.isect, "--max-leaf", str(args.max_leaf),
-           "--sah-bins", str(args.sah_bins)]
+           "--sah-bins", str(args.sah_bins), "--bvh", args.bvh]
     env = {k: v for k, v in os.environ.items()
            if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
     try:
@@ -370,6 +373,13 @@ def run_own(args):
         scene = vsr.Scene.from_workload(sc, device=local).build(max_leaf_size=args.max_leaf, sah_bins=args.sah_bins)
     setup_s = time.time() - t0
     stats = scene.stats()
+    wide_info = None
+    if args.bvh == "wide":
+        scene.build_wide()
+        we = scene.export_wide()
+        wide_info = {"nodes": int(we["nodes"].shape[0]), "max_depth": we["max_depth"],
+                     "build_ms": round(we["build_ms"], 1), "node_bytes": 80}
+        del we
     tiles = args.mode in ("tiles", "tiles-nccl")
     fused = args.mode == "tiles"
     tile_rays = 64 * rays.spp
@@ -414,6 +424,9 @@ def run_own(args):
             return
         if fused and kind not in (vsr.COUNT, vsr.COUNT_ALPHA_TEXTURE):
             scene.trace_tiles(d_rays, tile_rays, rank, world, frame_ptr, query, kind, stream=sh)
+            return
+        if args.bvh == "wide":
+            scene.trace_wide(d_rays, query, kind, hits=hits, counts=counts, stream=sh)
             return
         scene.trace_raw(d_rays.data_ptr(), n, query, kind, hits.data_ptr(),
                         counts.data_ptr(), sh)
@@ -504,8 +517,10 @@ def run_own(args):
     cnp = vsr.counts_to_numpy(counts)
     bytes_launch, work = algorithmic_bytes(cnp, has_alpha,
                                            counts_out=args.isect in ("count", "count_alpha_texture"))
+    if args.bvh == "wide":   # SURVEY 8(d)'s bytes per ray are defined on the binary tree's visits
+        bytes_launch, work = None, None
     peak, peak_src = load_peaks()
-    touched = bytes_launch / (ms_kernel * 1e-3) / 1e9
+    touched = bytes_launch / (ms_kernel * 1e-3) / 1e9 if bytes_launch else None
     mhz = sampler.summary().get("sm_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(local).multi_processor_count
     ctr, ctr_src = (None, "skipped (--no-counters)")
@@ -519,7 +534,7 @@ def run_own(args):
                 "traffic": levels.get("dram", {}).get("per_launch"),
                 "kernel": (ctr or {}).get("kernel") or f"trace_kernel<{args.query}, {args.isect}>",
                 "kernel_ms": round(ms_kernel, 4), "levels": levels, "counters_source": ctr_src,
-                "algorithmic": {
+                "algorithmic": None if bytes_launch is None else {
                     "bytes_per_launch": bytes_launch, "bytes_per_ray": round(bytes_launch / n, 1),
                     "work_per_ray": work, "touched_gbs": round(touched, 1),
                     "cache_reuse_ratio": round(touched / peak, 4),
@@ -646,6 +661,25 @@ def run_own(args):
                         "value": round(n / (np.mean(mg) * 1e-3) / 1e6, 1),
                         "ms": round(float(np.mean(mg)), 4)}
             del gscene
+        # NEXT-3: the same SAH tree collapsed into the 8-wide compressed BVH (vsr_trace_bvh8)
+        if args.bvh == "binary" and not tiles:
+            scene.build_wide()
+            we = scene.export_wide()
+            args.bvh = "wide"
+            try:
+                mw, _ = timed(isect, max(5, args.steps // 2), 3)
+                mwo, _ = timed(isect, max(5, args.steps // 2), 3,
+                               query=vsr.ANY if q == vsr.CLOSEST else vsr.CLOSEST)
+            finally:
+                args.bvh = "binary"
+            extra["wide_bvh"] = {
+                "api": "vsr_bvh8_build + vsr_trace_bvh8 (80-B nodes, 8 children, 8-bit planes)",
+                "nodes": int(we["nodes"].shape[0]), "max_depth": we["max_depth"],
+                "build_ms": round(we["build_ms"], 1),
+                "value": round(n / (np.mean(mw) * 1e-3) / 1e6, 1), "ms": round(float(np.mean(mw)), 4),
+                "other_query": {"query": "any" if q == vsr.CLOSEST else "closest",
+                                "value": round(n / (np.mean(mwo) * 1e-3) / 1e6, 1)}}
+            del we
         extra["gpu_build"] = {"builders": "vsr_bvh_build_gpu (LBVH, Karras 2012), "
                                           "vsr_bvh_build_ploc (PLOC, radius 16)", **gb}
         extra["zero_cost"] = {"none_ms": round(float(np.median(a_ms)), 4),
@@ -702,7 +736,10 @@ def run_own(args):
             "config": {**config_desc(args.config), "query": args.query, "intersector": args.isect,
                        "rays_per_gpu": n, "resolution": f"{rays.width}x{rays.height}x{rays.spp}spp",
                        "triangles": int(stats["num_tris"]), "bvh_nodes": int(stats["num_nodes"]),
-                       "bvh": f"binned SAH, {args.sah_bins} bins, max_leaf {args.max_leaf}",
+                       "bvh": f"binned SAH, {args.sah_bins} bins, max_leaf {args.max_leaf}"
+                              + (", collapsed to the 8-wide compressed BVH" if args.bvh == "wide"
+                                 else ""),
+                       "wide_bvh": wide_info,
                        "textures": f"{len(sc.textures)}x{sc.textures[0].shape[1]}x{sc.textures[0].shape[0]} RGBA8",
                        "l2": "flushed before every timed step (read of a 256 MiB buffer, outside the events)",
                        "launch": ("one CUDA-graph replay of the trace call per step" if use_graph

@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define VSR_ABI_VERSION 1u
+#define VSR_ABI_VERSION 2u   /* 2: slab contract r02, 8-wide BVH entry points */
 
 typedef enum {
   VSR_OK = 0,
@@ -190,6 +190,42 @@ vsr_status vsr_bvh_build_gpu(vsr_scene* scene, uint32_t max_leaf_size);
  * typical) and mutual pairs merge, round after round — trees close to binned SAH in quality at
  * GPU build speed.  Same layout, rules and errors as vsr_bvh_build_gpu. */
 vsr_status vsr_bvh_build_ploc(vsr_scene* scene, uint32_t max_leaf_size, uint32_t radius);
+
+/* 8-WIDE COMPRESSED BVH (SURVEY.md §8(f) NEXT-3 "wide / compressed BVH (8-wide quantized
+ * nodes)"; Ylitie, Karras & Laine, HPG 2017).  Collapses the scene's built binary BVH (any
+ * builder; leaves of at most 4 triangles) into 80-B nodes of up to 8 children whose boxes are
+ * quantized to 8 bits per plane on a per-node grid: plane(q) = fma(2^23 + q, 2^(e-127), pm),
+ * the codes chosen so every decoded child box contains the binary child box.
+ * Children are visited in slot order s ^ octant(ray); the box hook of a wide node counts one box
+ * test per valid child (COUNT: num_boxes = 1 root + the valid children of every visited node).
+ * The triangles / sidecars are reordered for the wide leaves (prim ids unchanged).  Synchronous,
+ * untimed; kept until the binary BVH is rebuilt or the scene destroyed; works for host-only
+ * scenes (device -1: exportable, not traceable) and imported scenes.  Errors: INVALID_ARG,
+ * NOT_BUILT, UNSUPPORTED (a leaf with > 4 triangles), BVH_TOO_DEEP, CUDA, OOM. */
+vsr_status vsr_bvh8_build(vsr_scene* scene);
+
+/* Host copies of the wide BVH.  Two calls: first with NULL arrays (sizes filled), then with
+ * caller-owned host arrays of num_nodes x 80 B (wide.hpp WideNode: pm[3] f32, e[3] u8, imask
+ * u8, child_base u32, tri_base u32, meta[8] u8, qlo[3][8] u8, qhi[3][8] u8), num_tris x 48 B
+ * triangles and num_tris x 32 B sidecars (the binary export layouts, in the wide leaf order).
+ * Root box = the binary root box (tested once, counted).  Errors: INVALID_ARG, NOT_BUILT. */
+typedef struct {
+  uint32_t num_nodes, num_tris, max_depth, pad;
+  float root_lo[3], root_hi[3];
+  double build_ms;
+  void* nodes;
+  void* tris;
+  void* sides;
+} vsr_bvh8_view;
+vsr_status vsr_bvh8_export(const vsr_scene* scene, vsr_bvh8_view* out);
+
+/* vsr_trace over the wide BVH: same arguments, semantics, asynchrony and results (hits are
+ * those of vsr_trace up to exact-t ties; the BVH only prunes); counts follow the wide
+ * traversal.  Intersectors: every kind except the run-time controls (>= 100: UNSUPPORTED).
+ * Errors: INVALID_ARG, NOT_BUILT (no wide BVH: call vsr_bvh8_build), UNSUPPORTED, CUDA. */
+vsr_status vsr_trace_bvh8(vsr_scene* scene, const vsr_ray* d_rays, uint64_t n, vsr_query query,
+                          vsr_isect isect, const vsr_isect_params* params, vsr_hit* d_hits,
+                          vsr_counts* d_counts, void* stream);
 
 /* Enqueue one trace of n rays on `stream` (a cudaStream_t; NULL = legacy default).
  * d_rays / d_hits / d_counts are caller-owned DEVICE buffers on the scene's device,

@@ -85,6 +85,9 @@ def lib():
                                        C.c_float, C.c_uint32, C.POINTER(_Hit)]
         L.oracle_eval_pairs.argtypes = [C.POINTER(_Scene), C.c_void_p, C.c_void_p, C.c_uint64,
                                         C.c_int, C.c_float, C.c_uint32, C.c_void_p, C.c_void_p]
+        L.walker_trace_wide.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_uint32, C.c_void_p,
+                                        C.c_uint64, C.c_int, C.c_int, C.c_float, C.c_uint32,
+                                        C.c_void_p, C.c_void_p, C.c_int]
         L.oracle_mt.argtypes = [C.c_void_p] * 4 + [C.c_float] + [C.POINTER(C.c_float)] * 3
         L.oracle_tex_alpha.argtypes = [C.c_uint32, C.c_uint32, C.c_void_p, C.c_float, C.c_float]
         L.oracle_tex_alpha.restype = C.c_float
@@ -288,6 +291,25 @@ class BvhArrays:
                     (C.c_float * 3)(*self.root_hi.tolist()), keep[0].shape[0], keep[1].shape[0],
                     keep[3].shape[0], _ptr(keep[0]), _ptr(keep[1]), _ptr(keep[2]), _ptr(keep[3]),
                     _ptr(keep[4]))
+
+
+def walk_wide(bvh: BvhArrays, wnodes, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01,
+              checker_freq=8, nthreads=None):
+    """Walker C over an 8-wide compressed BVH: `wnodes` uint32 [N, 20]
+    (80-B nodes), `bvh` carrying the root box and the WIDE-ordered tris / sides (+ texdescs /
+    texels).  Returns (hits HIT_DTYPE, counts COUNT_DTYPE)."""
+    r = _rays(rays)
+    n = r.shape[0]
+    w = np.ascontiguousarray(wnodes, dtype=np.uint32).reshape(-1, 20)
+    hits = np.empty(n, dtype=HIT_DTYPE)
+    counts = np.empty(n, dtype=COUNT_DTYPE)
+    cb = bvh.c_struct()
+    rc = lib().walker_trace_wide(C.byref(cb), _ptr(w), w.shape[0], _ptr(r), n, query, isect,
+                                 alpha_threshold, checker_freq, _ptr(hits), _ptr(counts),
+                                 nthreads or default_threads())
+    if rc != 0:
+        raise ValueError(f"walker_trace_wide failed ({rc})")
+    return hits, counts
 
 
 def build_bvh(scene, max_leaf: int = 4) -> BvhArrays:

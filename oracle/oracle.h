@@ -165,6 +165,30 @@ int walker_trace_list(const or_bvh* list, uint32_t nlist, const float* rays, uin
 typedef struct {
   float m[12]; uint32_t bvh, index, pad[2];
 } or_instance;
+/* 8-wide compressed BVH, re-declared from the
+ * documented 80-B layout: per axis k a decode origin pm[k] and scale exponent field e[k]
+ * (scale = the float with exponent field e[k], mantissa 0); imask bit s = slot s is an inner
+ * child; inner children of a node are nodes child_base + (rank of s among the inner slots);
+ * meta[s] = 0xFF empty, 0x80 inner, else leaf: triangles tri_base + (meta & 31), count
+ * (meta >> 5) + 1; child box planes plane(q) = fmaf(2^23 + q, scale, pm) of the codes
+ * qlo[k][s], qhi[k][s]. */
+typedef struct {
+  float pm[3]; uint8_t e[3]; uint8_t imask;
+  uint32_t child_base, tri_base;
+  uint8_t meta[8];
+  uint8_t qlo[3][8], qhi[3][8];
+} or_wnode;
+
+/* Walker over the wide BVH: the root box of `b` (tested once, counted), then from node 0:
+ * test every valid child (counted, one box each), the triangles of hit leaf children in key
+ * order (key of slot s = s XOR the ray octant, ascending; octant bit k = sign bit of inv_k),
+ * then descend into the hit inner child of smallest key and keep the rest as a pending group
+ * (no t on the stack: a pending child is visited whatever best_t has become).  b->tris /
+ * b->sides must be the wide leaf order; b->nodes is unused.  Closest / any only. */
+int walker_trace_wide(const or_bvh* b, const or_wnode* nodes, uint32_t num_nodes,
+                      const float* rays, uint64_t n, int query, int isect, float alpha_threshold,
+                      uint32_t checker_freq, or_hit* hits, or_counts* counts, int nthreads);
+
 int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_bvh* bottoms,
                            uint32_t nbottoms, const float* rays, uint64_t n, int query,
                            int isect, float alpha_threshold, uint32_t checker_freq,

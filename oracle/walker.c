@@ -878,3 +878,157 @@ int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
   }
   return jb.err ? -1 : 0;
 }
+
+
+/* ====================== 8-wide compressed BVH walker ======================= */
+/* DESIGN.md §9h.  Written from the documented layout and traversal order; it
+ * shares nothing with the product's wide.cu / bvh8_build.cpp. */
+typedef struct {
+  const or_bvh* b;
+  const or_wnode* nodes;
+  uint32_t num_nodes;
+  const float* rays;
+  uint64_t n;
+  int query, isect;
+  float thr;
+  uint32_t M;
+  or_hit* hits;
+  or_counts* counts;
+  uint64_t next;
+  int err;
+} wwjob_t;
+
+static float wide_plane(uint8_t q, uint8_t e, float pm) {
+  uint32_t bits = (uint32_t)e << 23;
+  float scale;
+  memcpy(&scale, &bits, 4);
+  return fmaf(8388608.0f + (float)q, scale, pm);
+}
+
+static int walk_wide_one(const wwjob_t* jb, uint64_t r) {
+  const or_bvh* b = jb->b;
+  const float* ray = jb->rays + r * 8;
+  const float* o = ray;
+  const float* d = ray + 4;
+  const float tmin = ray[3];
+  float inv[3];
+  for (int a = 0; a < 3; ++a) {
+    float dk = d[a];
+    inv[a] = 1.0f / (fabsf(dk) > 0x1p-80f ? dk : copysignf(0x1p-80f, dk));
+  }
+  const uint32_t oct = (uint32_t)(signbit(inv[0]) != 0) | (uint32_t)(signbit(inv[1]) != 0) << 1 |
+                       (uint32_t)(signbit(inv[2]) != 0) << 2;
+  or_hit best = {INFINITY, 0.0f, 0.0f, 0xFFFFFFFFu};
+  float best_t = ray[7];
+  int have = 0, bad = 0;
+  or_counts c = {0, 0, 0};
+  uint32_t st_base[MAX_STACK], st_imask[MAX_STACK], st_keys[MAX_STACK];
+  int sp = 0;
+  float tn;
+  c.boxes++;
+  if (!slab(b->root_lo, b->root_hi, o, inv, tmin, best_t, &tn)) goto done;
+  uint32_t node = 0;
+  for (;;) {
+    if (node >= jb->num_nodes) { bad = 1; goto done; }
+    const or_wnode* w = &jb->nodes[node];
+    uint32_t valid = 0, hits = 0;
+    for (int s = 0; s < 8; ++s)
+      if (w->meta[s] != 0xFF) valid |= 1u << s;
+    c.boxes += (uint32_t)__builtin_popcount(valid);
+    for (int s = 0; s < 8; ++s) {
+      if (!(valid >> s & 1u)) continue;
+      float lo[3], hi[3];
+      for (int a = 0; a < 3; ++a) {
+        lo[a] = wide_plane(w->qlo[a][s], w->e[a], w->pm[a]);
+        hi[a] = wide_plane(w->qhi[a][s], w->e[a], w->pm[a]);
+      }
+      if (slab(lo, hi, o, inv, tmin, best_t, &tn)) hits |= 1u << s;
+    }
+    /* leaf children, keys ascending */
+    for (uint32_t k = 0; k < 8; ++k) {
+      const uint32_t s = k ^ oct;
+      if (!(hits >> s & 1u) || (w->imask >> s & 1u)) continue;
+      const uint32_t m = w->meta[s];
+      const uint32_t first = w->tri_base + (m & 31u), cnt = (m >> 5) + 1u;
+      if ((uint64_t)first + cnt > b->num_tris) { bad = 1; goto done; }
+      for (uint32_t t_i = first; t_i < first + cnt; ++t_i) {
+        const or_tri* tr = &b->tris[t_i];
+        float t, u, v;
+        c.tris++;
+        if (!mt_tri(tr, o, d, tmin, best_t, &t, &u, &v)) continue;
+        if (jb->isect == OR_ALPHA_TEX) c.alpha++;
+        if (!walk_filter(b, t_i, jb->isect, u, v, jb->thr, jb->M)) continue;
+        if (jb->query == OR_ANY) {
+          best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
+          goto done;
+        }
+        if (!have || t < best_t) {
+          best.t = t; best.u = u; best.v = v; best.prim = tr->prim;
+          best_t = t;
+          have = 1;
+        }
+      }
+    }
+    /* inner children: descend into the smallest key, keep the others */
+    uint32_t keys = 0;
+    for (uint32_t s = 0; s < 8; ++s)
+      if ((hits >> s & 1u) && (w->imask >> s & 1u)) keys |= 1u << (s ^ oct);
+    uint32_t base = w->child_base, imask = w->imask;
+    if (!keys) {
+      if (sp == 0) goto done;
+      base = st_base[sp - 1];
+      imask = st_imask[sp - 1];
+      keys = st_keys[sp - 1];
+      sp--;
+    }
+    const uint32_t k0 = (uint32_t)__builtin_ctz(keys);
+    keys &= keys - 1u;
+    if (keys) {
+      if (sp >= MAX_STACK) { bad = 1; goto done; }
+      st_base[sp] = base; st_imask[sp] = imask; st_keys[sp] = keys;
+      sp++;
+    }
+    const uint32_t s0 = k0 ^ oct;
+    node = base + (uint32_t)__builtin_popcount(imask & ((1u << s0) - 1u));
+  }
+done:
+  jb->hits[r] = best;
+  if (jb->counts) jb->counts[r] = c;
+  return bad;
+}
+
+static void* wwworker(void* arg) {
+  wwjob_t* jb = (wwjob_t*)arg;
+  const uint64_t chunk = 1024;
+  for (;;) {
+    uint64_t s = __atomic_fetch_add(&jb->next, chunk, __ATOMIC_RELAXED);
+    if (s >= jb->n) break;
+    uint64_t e = s + chunk < jb->n ? s + chunk : jb->n;
+    for (uint64_t r = s; r < e; ++r)
+      if (walk_wide_one(jb, r)) __atomic_store_n(&jb->err, 1, __ATOMIC_RELAXED);
+  }
+  return NULL;
+}
+
+int walker_trace_wide(const or_bvh* b, const or_wnode* nodes, uint32_t num_nodes,
+                      const float* rays, uint64_t n, int query, int isect, float thr, uint32_t M,
+                      or_hit* hits, or_counts* counts, int nthreads) {
+  if (!b || !nodes || num_nodes == 0 || !rays || !hits) return -1;
+  if (query != OR_CLOSEST && query != OR_ANY) return -1;
+  if (isect < OR_NONE || isect > OR_ALPHA_PROC_UV) return -1;
+  if ((isect == OR_ALPHA_PROC || isect == OR_ALPHA_PROC_UV) && M == 0) return -1;
+  wwjob_t jb;
+  memset(&jb, 0, sizeof jb);
+  jb.b = b; jb.nodes = nodes; jb.num_nodes = num_nodes; jb.rays = rays; jb.n = n;
+  jb.query = query; jb.isect = isect; jb.thr = thr; jb.M = M; jb.hits = hits; jb.counts = counts;
+  if (nthreads < 1) nthreads = 1;
+  if (nthreads == 1) {
+    wwworker(&jb);
+  } else {
+    pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int k = 0; k < nthreads; ++k) pthread_create(&th[k], NULL, wwworker, &jb);
+    for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+    free(th);
+  }
+  return jb.err ? -2 : 0;
+}

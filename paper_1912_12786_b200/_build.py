@@ -17,8 +17,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvsr.so")
-SOURCES = ["api.cpp", "api_trace.cpp", "api_compound.cpp", "bvh_build.cpp", "trace.cu", "compound.cu", "prims.cu", "lbvh.cu"]
-HEADERS = ["api_internal.hpp", "layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh", "traverse.cuh"]
+SOURCES = ["api.cpp", "api_trace.cpp", "api_compound.cpp", "api_wide.cpp", "bvh_build.cpp",
+           "bvh8_build.cpp", "trace.cu", "compound.cu", "prims.cu", "lbvh.cu", "wide.cu"]
+HEADERS = ["api_internal.hpp", "layout.hpp", "builder.hpp", "trace.hpp", "intersectors.cuh",
+           "traverse.cuh", "wide.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -135,8 +135,29 @@ struct vsr_scene {
   uint32_t plane_amin[kMaxPlanes] = {};
   uint32_t* d_planes[kMaxPlanes] = {};
   int num_planes = 0;
+  // ---- 8-wide compressed BVH (vsr_bvh8_build; NEXT-3) ----
+  bool wide_built = false;
+  HostWide host_wide;   // host-only scenes keep it here; device scenes upload it
+  WideNode* d_wnodes = nullptr;
+  Tri* d_wtris = nullptr;
+  Side* d_wsides = nullptr;
+  uint32_t num_wnodes = 0, wide_depth = 0;
+  double wide_build_ms = 0.0;
+
+  void free_wide() {
+    cudaFree(d_wnodes);
+    cudaFree(d_wtris);
+    cudaFree(d_wsides);
+    d_wnodes = nullptr;
+    d_wtris = nullptr;
+    d_wsides = nullptr;
+    num_wnodes = wide_depth = 0;
+    host_wide = HostWide{};
+    wide_built = false;
+  }
 
   void free_device() {
+    free_wide();
     cudaFree(d_nodes);
     cudaFree(d_tris);
     cudaFree(d_sides);

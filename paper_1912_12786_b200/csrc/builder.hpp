@@ -6,6 +6,7 @@
 
 #include "../../include/vsr.h"
 #include "layout.hpp"
+#include "wide.hpp"
 
 namespace vsr {
 
@@ -28,6 +29,17 @@ struct HostBvh {
 
 vsr_status build_bvh(const BuildInput& in, const vsr_build_params& prm, HostBvh& out,
                      std::string& err);
+
+// 8-wide compressed BVH collapsed from a built binary BVH (bvh8_build.cpp, NEXT-3):
+// nodes breadth-first (root = 0), triangles / sidecars in the wide leaf order.
+struct HostWide {
+  float root_lo[3] = {0, 0, 0}, root_hi[3] = {0, 0, 0};
+  std::vector<WideNode> nodes;
+  std::vector<Tri> tris;
+  std::vector<Side> sides;
+  uint32_t max_depth = 0;
+};
+vsr_status build_wide(const HostBvh& b, HostWide& out, std::string& err);
 
 // GPU linear BVH (lbvh.cu) on the current device from device inputs (9 floats
 // per triangle, optional 6 texcoords, resolved texture index, texture table).

@@ -224,6 +224,78 @@ __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair&
   return h;
 }
 
+// ---------------------------------------------------------------------------
+// The 8 quantized child boxes of a wide node (wide.hpp, SURVEY.md §8(f)
+// NEXT-3), as loaded: h = (pm.x, pm.y, pm.z, e bytes | imask << 24); per axis
+// the lower and upper plane codes of slots 0-3 and 4-7 (one byte each):
+// q0 = (lo.x 0-3, lo.x 4-7, lo.y 0-3, lo.y 4-7), q1 = (lo.z 0-3, lo.z 4-7,
+// hi.x 0-3, hi.x 4-7), q2 = (hi.y 0-3, hi.y 4-7, hi.z 0-3, hi.z 4-7).
+// A box hook on an AabbOct stands for one box-hook call per VALID child.
+// ---------------------------------------------------------------------------
+struct AabbOct {
+  float4 h;
+  uint4 q0, q1, q2;
+};
+
+// 2^23 + byte j of w, as a float (PRMT: the byte becomes the mantissa)
+__device__ __forceinline__ float qbyte(uint32_t w, int j) {
+  return __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7540u | (uint32_t)j));
+}
+
+// t of the 8 slots' planes on one axis: plane = fma(2^23 + q, scale, pm) (the
+// decode, one rounding), then the r02 slab crossing fma(plane, inv, noi).
+__device__ __forceinline__ void oct_axis(uint32_t w03, uint32_t w47, float scale, float pm,
+                                         float inv, float noi, float (&t)[8]) {
+  const f2_t s2 = pk(scale, scale), p2 = pk(pm, pm), i2 = pk(inv, inv), n2 = pk(noi, noi);
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const uint32_t w = j < 4 ? w03 : w47;
+    upk(fma2(fma2(pk(qbyte(w, j & 3), qbyte(w, (j & 3) + 1)), s2, p2), i2, n2), t[j], t[j + 1]);
+  }
+}
+
+__device__ __forceinline__ float oct_scale(uint32_t hw, int a) {
+  return __uint_as_float(((hw >> (8 * a)) & 0xFFu) << 23);
+}
+
+// Slot hit mask of the 8 children (generic: per-axis min/max).  Bits of slots
+// that are not valid children are meaningless (the caller masks them).
+__device__ __forceinline__ uint32_t intersect(const RayCtx& r, const AabbOct& b, float best_t,
+                                              uint32_t /*valid*/) {
+  const uint32_t hw = __float_as_uint(b.h.w);
+  // axis by axis, folded into the running entry / exit so at most 4 arrays live
+  float tn[8], tf[8], a[8], c[8];
+  oct_axis(b.q0.x, b.q0.y, oct_scale(hw, 0), b.h.x, r.ix, r.nx, a);
+  oct_axis(b.q1.z, b.q1.w, oct_scale(hw, 0), b.h.x, r.ix, r.nx, c);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    tn[j] = fmaxf(fminf(a[j], c[j]), r.tmin);
+    tf[j] = fmaxf(a[j], c[j]);
+  }
+  oct_axis(b.q0.z, b.q0.w, oct_scale(hw, 1), b.h.y, r.iy, r.ny, a);
+  oct_axis(b.q2.x, b.q2.y, oct_scale(hw, 1), b.h.y, r.iy, r.ny, c);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    tn[j] = fmaxf(tn[j], fminf(a[j], c[j]));
+    tf[j] = fminf(tf[j], fmaxf(a[j], c[j]));
+  }
+  oct_axis(b.q1.x, b.q1.y, oct_scale(hw, 2), b.h.z, r.iz, r.nz, a);
+  oct_axis(b.q2.z, b.q2.w, oct_scale(hw, 2), b.h.z, r.iz, r.nz, c);
+  const float bt = cull_t(r, best_t);
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float n0 = fmaxf(tn[j], fminf(a[j], c[j])), n1 = fmaxf(tn[j + 1], fminf(a[j + 1], c[j + 1]));
+    float g0, g1;
+    upk(fma2(pk(fminf(tf[j], fmaxf(a[j], c[j])), fminf(tf[j + 1], fmaxf(a[j + 1], c[j + 1]))),
+             pk(1.0000003576f, 1.0000003576f), pk(r.pad, r.pad)),
+        g0, g1);
+    m |= (n0 <= fminf(g0, bt) ? 1u : 0u) << j;
+    m |= (n1 <= fminf(g1, bt) ? 1u : 0u) << (j + 1);
+  }
+  return m;
+}
+
 // Ray octant (sign bits of inv.x, inv.y, inv.z) known at compile time: an
 // extra box-hook argument, forwarded like the paper's inverse direction
 // (PAPER.md:371-376).
@@ -263,6 +335,43 @@ __device__ __forceinline__ BoxPairHit intersect(const RayCtx& r, const AabbPair&
   h.h0 = h.tn0 <= fminf(g0, bt);
   h.h1 = h.tn1 <= fminf(g1, bt);
   return h;
+}
+
+// Octant-specialised slot hit mask: the near / far code words of each axis are
+// chosen at compile time (the same monotonicity argument as the pair test:
+// plane(q) is nondecreasing in q and fma(plane, inv, noi) is monotone in the
+// plane, so for inv > 0 the lower code gives the entry crossing).
+template <int OCT>
+__device__ __forceinline__ uint32_t intersect(const RayCtx& r, const AabbOct& b, float best_t,
+                                              uint32_t /*valid*/, octant<OCT>) {
+  constexpr bool sx = OCT & 1, sy = OCT & 2, sz = OCT & 4;
+  const uint32_t hw = __float_as_uint(b.h.w);
+  // axis by axis, folded into the running entry / exit so at most 4 arrays live
+  float tn[8], tf[8], a[8], c[8];
+  oct_axis(sx ? b.q1.z : b.q0.x, sx ? b.q1.w : b.q0.y, oct_scale(hw, 0), b.h.x, r.ix, r.nx, tn);
+  oct_axis(sx ? b.q0.x : b.q1.z, sx ? b.q0.y : b.q1.w, oct_scale(hw, 0), b.h.x, r.ix, r.nx, tf);
+  oct_axis(sy ? b.q2.x : b.q0.z, sy ? b.q2.y : b.q0.w, oct_scale(hw, 1), b.h.y, r.iy, r.ny, a);
+  oct_axis(sy ? b.q0.z : b.q2.x, sy ? b.q0.w : b.q2.y, oct_scale(hw, 1), b.h.y, r.iy, r.ny, c);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    tn[j] = fmax3(tn[j], a[j], r.tmin);
+    tf[j] = fminf(tf[j], c[j]);
+  }
+  oct_axis(sz ? b.q2.z : b.q1.x, sz ? b.q2.w : b.q1.y, oct_scale(hw, 2), b.h.z, r.iz, r.nz, a);
+  oct_axis(sz ? b.q1.x : b.q2.z, sz ? b.q1.y : b.q2.w, oct_scale(hw, 2), b.h.z, r.iz, r.nz, c);
+  const float bt = cull_t(r, best_t);
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j += 2) {
+    const float n0 = fmaxf(tn[j], a[j]), n1 = fmaxf(tn[j + 1], a[j + 1]);
+    float g0, g1;
+    upk(fma2(pk(fminf(tf[j], c[j]), fminf(tf[j + 1], c[j + 1])),
+             pk(1.0000003576f, 1.0000003576f), pk(r.pad, r.pad)),
+        g0, g1);
+    m |= (n0 <= fminf(g0, bt) ? 1u : 0u) << j;
+    m |= (n1 <= fminf(g1, bt) ? 1u : 0u) << (j + 1);
+  }
+  return m;
 }
 
 __device__ __forceinline__ int ray_octant(const RayCtx& r) {
@@ -348,6 +457,11 @@ struct basic_intersector {
   __device__ __forceinline__ BoxPairHit operator()(const RayCtx& r, const AabbPair& b,
                                                    Args&&... args) {
     return intersect(r, b, static_cast<Args&&>(args)...);
+  }
+  template <class... Args>
+  __device__ __forceinline__ uint32_t operator()(const RayCtx& r, const AabbOct& b, float best_t,
+                                                 uint32_t valid, Args&&... args) {
+    return intersect(r, b, best_t, valid, static_cast<Args&&>(args)...);
   }
   __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
                                                    float tmax_cur) {
@@ -561,6 +675,12 @@ struct cost_intersector : Inner {
                                                    Args&&... args) {
     num_boxes += 2;   // two box tests: one per child
     return Inner::operator()(r, b, static_cast<Args&&>(args)...);
+  }
+  template <class... Args>
+  __device__ __forceinline__ uint32_t operator()(const RayCtx& r, const AabbOct& b, float best_t,
+                                                 uint32_t valid, Args&&... args) {
+    num_boxes += (uint32_t)__popc(valid);   // one box test per valid child of the wide node
+    return Inner::operator()(r, b, best_t, valid, static_cast<Args&&>(args)...);
   }
   __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
                                                    float tmax_cur) {

@@ -498,7 +498,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     p.perm = perm;
   }
   if (g_kernel_events[0]) cudaEventRecord(static_cast<cudaEvent_t>(g_kernel_events[0]), st);
-  cudaError_t e = p.list ? launch_compound(query, isect, p, st)   // lists, instances (compound.cu)
+  cudaError_t e = p.wide ? launch_wide(query, isect, p, st)       // 8-wide BVH (wide.cu)
+                  : p.list ? launch_compound(query, isect, p, st)   // lists, instances (compound.cu)
                   : query == kMulti ? dispatch_multi(isect, p, st)
                   : query == kAny ? dispatch_isect<kAny>(isect, p, st)
                                   : dispatch_isect<kClosest>(isect, p, st);

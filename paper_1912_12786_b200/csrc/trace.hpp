@@ -9,6 +9,8 @@
 
 namespace vsr {
 
+struct WideNode;
+
 enum : int { kSchedDirect = 0, kSchedPersistent = 1 };
 
 // Kernel parameters (passed by value: they live in the constant parameter bank).
@@ -41,6 +43,7 @@ struct TraceParams {
   Pinhole cam;
   int runtime_kind;
   void* filter_fn;
+  const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
 };
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);
@@ -58,5 +61,7 @@ uint64_t launch_count();
 cudaError_t launch_prims(int query, int isect, const TraceParams& p, cudaStream_t st);
 // Lists of BVHs and instances (p.list set; compound.cu), closest / any / multi.
 cudaError_t launch_compound(int query, int isect, const TraceParams& p, cudaStream_t st);
+// The 8-wide compressed BVH (p.wide set; wide.cu), closest / any.
+cudaError_t launch_wide(int query, int isect, const TraceParams& p, cudaStream_t st);
 
 }  // namespace vsr

@@ -55,7 +55,8 @@ EXPORTED_SYMBOLS = ["vsr_scene_create", "vsr_bvh_build", "vsr_trace", "vsr_trace
                     "vsr_trace_instances", "vsr_instances_export", "vsr_bvh_build_gpu",
                     "vsr_trace_pinhole", "vsr_trace_tiles", "vsr_device_alloc", "vsr_device_free",
                     "vsr_ipc_handle", "vsr_ipc_open", "vsr_ipc_close", "vsr_bvh_build_ploc",
-                    "vsr_trace_group_multi", "vsr_trace_instances_multi", "vsr_trace_primitives"]
+                    "vsr_trace_group_multi", "vsr_trace_instances_multi", "vsr_trace_primitives",
+                    "vsr_bvh8_build", "vsr_bvh8_export", "vsr_trace_bvh8"]
 
 
 class VsrError(RuntimeError):
@@ -83,6 +84,13 @@ class BuildParams(C.Structure):
 
 class IsectParams(C.Structure):
     _fields_ = [("alpha_threshold", C.c_float), ("checker_freq", C.c_uint32)]
+
+
+class Bvh8View(C.Structure):
+    _fields_ = [("num_nodes", C.c_uint32), ("num_tris", C.c_uint32), ("max_depth", C.c_uint32),
+                ("pad", C.c_uint32), ("root_lo", C.c_float * 3), ("root_hi", C.c_float * 3),
+                ("build_ms", C.c_double), ("nodes", C.c_void_p), ("tris", C.c_void_p),
+                ("sides", C.c_void_p)]
 
 
 class BvhView(C.Structure):
@@ -173,6 +181,13 @@ def lib():
         L.vsr_bvh_build_gpu.restype = C.c_int
         L.vsr_bvh_build_ploc.argtypes = [P, C.c_uint32, C.c_uint32]
         L.vsr_bvh_build_ploc.restype = C.c_int
+        L.vsr_bvh8_build.argtypes = [P]
+        L.vsr_bvh8_build.restype = C.c_int
+        L.vsr_bvh8_export.argtypes = [P, C.POINTER(Bvh8View)]
+        L.vsr_bvh8_export.restype = C.c_int
+        L.vsr_trace_bvh8.argtypes = [P, P, C.c_uint64, C.c_int, C.c_int, C.POINTER(IsectParams),
+                                     P, P, P]
+        L.vsr_trace_bvh8.restype = C.c_int
         for name in ("vsr_trace_group_multi", "vsr_trace_instances_multi"):
             getattr(L, name).argtypes = [P, P, C.c_uint64, C.c_uint32, C.c_int,
                                          C.POINTER(IsectParams), P, P, P, P, P]
@@ -369,6 +384,42 @@ class Scene:
         """vsr_bvh_build_ploc: GPU build by PLOC clustering (NEXT-3)."""
         _check(lib().vsr_bvh_build_ploc(self._h, max_leaf_size, radius))
         return self
+
+    def build_wide(self):
+        """vsr_bvh8_build: collapse the built binary BVH into the 8-wide compressed BVH."""
+        _check(lib().vsr_bvh8_build(self._h))
+        return self
+
+    def trace_wide(self, rays, query=CLOSEST, isect=DEFAULT, hits=None, counts=None, stream=None,
+                   alpha_threshold=0.01, checker_freq=8):
+        """vsr_trace_bvh8 on device tensors (after build_wide); returns (hits, counts)."""
+        import torch
+        n = rays.shape[0]
+        _check_rays(rays, n, self.device)
+        if hits is None:
+            hits = torch.empty((n, 4), dtype=torch.float32, device=rays.device)
+        if isect in (COUNT, COUNT_ALPHA_TEXTURE) and counts is None:
+            counts = torch.empty((n, 4), dtype=torch.int32, device=rays.device)
+        _check_dev(hits, "hits", _f32(), n, (4,), self.device)
+        _check_dev(counts, "counts", _i32(), n, (4,), self.device, optional=True)
+        prm = IsectParams(alpha_threshold, checker_freq)
+        _check(lib().vsr_trace_bvh8(self._h, _ptr(rays), n, query, isect, C.byref(prm), _ptr(hits),
+                                    _ptr(counts), _stream_handle(stream, self.device)))
+        return hits, counts
+
+    def export_wide(self) -> dict:
+        """Host copies of the 8-wide BVH: nodes [num_nodes, 20] uint32 (80-B WideNode),
+        tris [num_tris, 12] uint32, sides [num_tris, 8] uint32 (wide leaf order)."""
+        v = Bvh8View()
+        _check(lib().vsr_bvh8_export(self._h, C.byref(v)))
+        arrs = {"nodes": np.zeros((v.num_nodes, 20), np.uint32),
+                "tris": np.zeros((v.num_tris, 12), np.uint32),
+                "sides": np.zeros((v.num_tris, 8), np.uint32)}
+        v.nodes, v.tris, v.sides = _ptr(arrs["nodes"]), _ptr(arrs["tris"]), _ptr(arrs["sides"])
+        _check(lib().vsr_bvh8_export(self._h, C.byref(v)))
+        arrs.update(root_lo=np.array(v.root_lo, np.float32), root_hi=np.array(v.root_hi, np.float32),
+                    max_depth=int(v.max_depth), build_ms=float(v.build_ms))
+        return arrs
 
     def stats(self) -> dict:
         s = Stats()

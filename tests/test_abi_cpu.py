@@ -36,7 +36,7 @@ def test_header_symbols_exported(vsr):
     for name in declared:
         assert name in exported, name
         assert hasattr(vsr.lib(), name)
-    assert vsr.lib().vsr_abi_version() == 1
+    assert vsr.lib().vsr_abi_version() == 2
 
 
 def test_library_is_sm100a(vsr):
