@@ -318,8 +318,12 @@ vsr_status vsr_trace_group(vsr_group* group, const vsr_ray* d_rays, uint64_t n, 
  *   o'_i = ((A_i0*o_x + A_i1*o_y) + A_i2*o_z) + b_i,   d'_i = (A_i0*d_x + A_i1*d_y) + A_i2*d_z,
  * tmin and tmax unchanged, so t is the same parameter in both spaces.  A must be finite and
  * invertible (|det A| > 1e-30 in fp64).  Instance world boxes: the scene's padded root box mapped
- * by the fp64 inverse, then padded outward by 2^-10 of (box diagonal + max |coordinate|)
- * (conservative for rays whose origin lies within ~1000 scene diagonals; reading A27).
+ * by the fp64 inverse, then padded outward by 2^-10 of (box diagonal + max |coordinate|).
+ * That pad covers the fp32 ray map's error for ray origins up to a bound r_safe derived per
+ * instance from |A|, |A^-1|, |b| and the box (reading A27; thousands of scene
+ * diagonals for well-conditioned maps); a ray with max_k |o_k| > r_safe skips the top-level
+ * BVH and visits every instance in leaf order (the definition itself: conservative at any
+ * distance, slower only for such rays).  Counts: top root 1, then per instance as below.
  * Scenes: built, one device, alive and unmodified while the object exists; 1..1024 scenes,
  * 1..2^26 instances.  Host-only scenes (device -1) give host-only instances: built and
  * exportable, not traceable.  params: top-level build (NULL = {1, 16, 1, 1}; max_leaf_size
@@ -354,6 +358,7 @@ typedef struct {
   uint32_t root_ref;
   float root_lo[3], root_hi[3];
   uint32_t num_nodes, num_instances, max_depth;
+  float r_safe;   /* rays with max_k |o_k| > r_safe skip the top level (see vsr_trace_instances) */
   void* nodes;
   void* records;
 } vsr_instances_view;

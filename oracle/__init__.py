@@ -113,7 +113,7 @@ def lib():
         L.walker_trace_instances.argtypes = [C.POINTER(_Bvh), C.c_void_p, C.c_void_p, C.c_uint32,
                                              C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_float,
                                              C.c_uint32, C.c_void_p, C.c_void_p, C.c_void_p,
-                                             C.c_int]
+                                             C.c_float, C.c_int]
         L.oracle_ray_to_object.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.walker_trace_list_multi.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint64,
                                               C.c_uint32, C.c_int, C.c_float, C.c_uint32,
@@ -123,7 +123,7 @@ def lib():
                                                    C.c_uint32, C.c_void_p, C.c_uint64, C.c_int,
                                                    C.c_uint32, C.c_int, C.c_float, C.c_uint32,
                                                    C.c_void_p, C.c_void_p, C.c_void_p,
-                                                   C.c_void_p, C.c_int]
+                                                   C.c_void_p, C.c_float, C.c_int]
         _lib = L
     return _lib
 
@@ -464,7 +464,8 @@ def trace_instances(scenes, bvh, mats, rays, query=CLOSEST, isect=DEFAULT, alpha
 def walk_instances(top, records, bottoms, rays, query=CLOSEST, isect=DEFAULT, alpha_threshold=0.01,
                    checker_freq=8, nthreads=None):
     """Contract walker C over a two-level hierarchy.  top: dict with root_ref, root_lo,
-    root_hi, nodes [m, 16] uint32; records [k, 16] uint32 (64 B or_instance, leaf order);
+    root_hi, nodes [m, 16] uint32 and optionally r_safe (the product's far-origin bound,
+    reading A27; absent = infinity); records [k, 16] uint32 (64 B or_instance, leaf order);
     bottoms: list of BvhArrays.  Returns (hits, inst uint32, counts)."""
     r = _rays(rays)
     n = r.shape[0]
@@ -479,7 +480,8 @@ def walk_instances(top, records, bottoms, rays, query=CLOSEST, isect=DEFAULT, al
     counts = np.empty(n, dtype=COUNT_DTYPE)
     rc = lib().walker_trace_instances(C.byref(tb), _ptr(recs), arr, len(bottoms), _ptr(r), n,
                                       query, isect, alpha_threshold, checker_freq, _ptr(hits),
-                                      _ptr(inst), _ptr(counts), nthreads or default_threads())
+                                      _ptr(inst), _ptr(counts), float(top.get("r_safe", np.inf)),
+                                      nthreads or default_threads())
     if rc != 0:
         raise ValueError(f"walker_trace_instances failed ({rc})")
     return hits, inst, counts
@@ -521,6 +523,7 @@ def walk_instances_multi(top, records, bottoms, rays, k, isect=DEFAULT, alpha_th
     rc = lib().walker_trace_instances_multi(C.byref(tb), _ptr(recs), arr, len(bottoms), _ptr(r), n,
                                             CLOSEST, k, isect, alpha_threshold, checker_freq,
                                             _ptr(hits), _ptr(nh), _ptr(inst), _ptr(counts),
+                                            float(top.get("r_safe", np.inf)),
                                             nthreads or default_threads())
     if rc != 0:
         raise ValueError(f"walker_trace_instances_multi failed ({rc})")

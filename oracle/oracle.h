@@ -189,10 +189,15 @@ int walker_trace_wide(const or_bvh* b, const or_wnode* nodes, uint32_t num_nodes
                       const float* rays, uint64_t n, int query, int isect, float alpha_threshold,
                       uint32_t checker_freq, or_hit* hits, or_counts* counts, int nthreads);
 
+/* r_safe (reading A27, round 2): a ray whose origin has max_k |o_k| > r_safe (fp32
+ * compare) tests the top root box (counted) and then visits EVERY instance record in leaf
+ * order instead of walking the top level — the product exports the bound it traces with
+ * (vsr_instances_view.r_safe); INFINITY = always the top level. */
 int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_bvh* bottoms,
                            uint32_t nbottoms, const float* rays, uint64_t n, int query,
                            int isect, float alpha_threshold, uint32_t checker_freq,
-                           or_hit* hits, uint32_t* inst, or_counts* counts, int nthreads);
+                           or_hit* hits, uint32_t* inst, or_counts* counts, float r_safe,
+                           int nthreads);
 
 /* Multi-hit over a list of BVHs / over instances: one K-entry buffer across
  * all elements (walk_one's acceptance rule), which / inst get K entries per ray: the list index /
@@ -205,7 +210,8 @@ int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
                                  const or_bvh* bottoms, uint32_t nbottoms, const float* rays,
                                  uint64_t n, int query, uint32_t K, int isect,
                                  float alpha_threshold, uint32_t checker_freq, or_hit* hits,
-                                 uint32_t* nhits, uint32_t* inst, or_counts* counts, int nthreads);
+                                 uint32_t* nhits, uint32_t* inst, or_counts* counts, float r_safe,
+                                 int nthreads);
 
 /* The ray map of reading A27 on its own (pins): out = 8 floats (o', tmin, d', tmax). */
 void oracle_ray_to_object(const float* m, const float* ray, float* out);

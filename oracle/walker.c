@@ -646,6 +646,7 @@ typedef struct {
   or_counts* counts;
   uint32_t K;        /* multi-hit: hits kept per ray (0 = closest / any) */
   uint32_t* nhits;
+  float r_safe;      /* origins with max |o_k| > r_safe skip the top level (reading A27) */
   uint64_t next;
   int err;
 } ijob_t;
@@ -740,6 +741,22 @@ static int walk_bottom(const ijob_t* jb, const or_bvh* b, const float* ray, ista
   }
 }
 
+/* Instance record k: map the ray (oracle_ray_to_object), walk its bottom BVH with the
+ * running state.  Returns 1 when the query is finished (any-hit accepted). */
+static int inst_visit(ijob_t* jb, const float* ray, uint32_t k, istate_t* S, uint32_t* which) {
+  const or_instance* in = &jb->recs[k];
+  if (in->bvh >= jb->nbottoms) { S->bad = 1; return 1; }
+  float oray[8];
+  oracle_ray_to_object(in->m, ray, oray);
+  const int had = S->have;
+  const float bt = S->best_t;
+  S->src = in->index;
+  const int stop = walk_bottom(jb, &jb->bottoms[in->bvh], oray, S);
+  if (S->bad) return 1;
+  if ((S->have && !had) || S->best_t < bt) *which = in->index;
+  return stop;
+}
+
 static void walk_instances_one(ijob_t* jb, uint64_t r) {
   const float* ray = jb->rays + r * 8;
   const float* o = ray;
@@ -763,7 +780,16 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
   int sp = 0;
   float tn;
   S.c.boxes++;
-  if (!slab(top->root_lo, top->root_hi, o, inv, tmin, S.best_t, &tn)) goto done;
+  {
+    const int root_hit = slab(top->root_lo, top->root_hi, o, inv, tmin, S.best_t, &tn);
+    if (fmaxf(fmaxf(fabsf(o[0]), fabsf(o[1])), fabsf(o[2])) > jb->r_safe) {
+      /* beyond the proven range: every instance in leaf order, the top level unused */
+      for (uint32_t k = 0; k < top->num_tris; ++k)
+        if (inst_visit(jb, ray, k, &S, &which)) goto done;
+      goto done;
+    }
+    if (!root_hit) goto done;
+  }
   uint32_t cur = top->root_ref;
   for (;;) {
     while (!(cur & LEAF_BIT)) {
@@ -793,19 +819,8 @@ static void walk_instances_one(ijob_t* jb, uint64_t r) {
       uint32_t first = cur & 0x03FFFFFFu;
       uint32_t cnt = ((cur >> 26) & 31u) + 1u;
       if ((uint64_t)first + cnt > top->num_tris) { S.bad = 1; goto done; }
-      for (uint32_t k = first; k < first + cnt; ++k) {
-        const or_instance* in = &jb->recs[k];
-        if (in->bvh >= jb->nbottoms) { S.bad = 1; goto done; }
-        float oray[8];
-        oracle_ray_to_object(in->m, ray, oray);
-        const int had = S.have;
-        const float bt = S.best_t;
-        S.src = in->index;
-        const int stop = walk_bottom(jb, &jb->bottoms[in->bvh], oray, &S);
-        if (S.bad) goto done;
-        if ((S.have && !had) || S.best_t < bt) which = in->index;
-        if (stop) goto done;
-      }
+      for (uint32_t k = first; k < first + cnt; ++k)
+        if (inst_visit(jb, ray, k, &S, &which)) goto done;
     }
   pop:
     for (;;) {
@@ -847,16 +862,16 @@ static void* iworker(void* arg) {
 int walker_trace_instances(const or_bvh* top, const or_instance* recs, const or_bvh* bottoms,
                            uint32_t nbottoms, const float* rays, uint64_t n, int query,
                            int isect, float thr, uint32_t M, or_hit* hits, uint32_t* inst,
-                           or_counts* counts, int nthreads) {
+                           or_counts* counts, float r_safe, int nthreads) {
   return walker_trace_instances_multi(top, recs, bottoms, nbottoms, rays, n, query, 0, isect, thr,
-                                      M, hits, NULL, inst, counts, nthreads);
+                                      M, hits, NULL, inst, counts, r_safe, nthreads);
 }
 
 int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
                                  const or_bvh* bottoms, uint32_t nbottoms, const float* rays,
                                  uint64_t n, int query, uint32_t K, int isect, float thr,
                                  uint32_t M, or_hit* hits, uint32_t* nhits, uint32_t* inst,
-                                 or_counts* counts, int nthreads) {
+                                 or_counts* counts, float r_safe, int nthreads) {
   if (!top || !recs || !bottoms || nbottoms < 1 || !rays || !hits) return -1;
   if (query != OR_CLOSEST && query != OR_ANY) return -1;
   if (K > MAX_MULTI) return -1;
@@ -867,6 +882,7 @@ int walker_trace_instances_multi(const or_bvh* top, const or_instance* recs,
   jb.top = top; jb.recs = recs; jb.bottoms = bottoms; jb.nbottoms = nbottoms;
   jb.rays = rays; jb.n = n; jb.query = query; jb.isect = isect; jb.thr = thr; jb.M = M;
   jb.hits = hits; jb.inst = inst; jb.counts = counts; jb.K = K; jb.nhits = nhits;
+  jb.r_safe = r_safe;
   if (nthreads < 1) nthreads = 1;
   if (nthreads == 1) {
     iworker(&jb);

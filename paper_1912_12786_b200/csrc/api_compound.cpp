@@ -221,6 +221,7 @@ struct vsr_instances {
   std::vector<vsr_scene*> scenes;
   HostBvh top;                       // host copy of the top-level nodes (export)
   std::vector<Instance> records;     // leaf order (export)
+  float r_safe = 0.0f;               // rays with |o|_inf above take the linear path (A27)
   DevScene dev{};                    // top level: nodes, root ref / box
   PairNode* d_nodes = nullptr;
   Instance* d_records = nullptr;
@@ -233,7 +234,8 @@ namespace {
 // World box of an instance: the 8 corners of the scene's (padded) root box
 // mapped by the fp64 inverse of [A | b], then padded by 2^-10 (diagonal +
 // max |coordinate|) and rounded outward (reading A27).  False if A is singular.
-bool instance_world_box(const float* m, const float* lo, const float* hi, float* out) {
+bool instance_world_box(const float* m, const float* lo, const float* hi, float* out,
+                        double* pad_out = nullptr) {
   const double a[3][3] = {{m[0], m[1], m[2]}, {m[4], m[5], m[6]}, {m[8], m[9], m[10]}};
   const double bv[3] = {m[3], m[7], m[11]};
   const double det = a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
@@ -266,6 +268,7 @@ bool instance_world_box(const float* m, const float* lo, const float* hi, float*
     mag = std::max(mag, std::max(std::fabs(wlo[i]), std::fabs(whi[i])));
   }
   const double pad = std::ldexp(std::sqrt(diag) + mag, -10);
+  if (pad_out) *pad_out = pad;
   for (int i = 0; i < 3; ++i) {
     const double l = wlo[i] - pad, h = whi[i] + pad;
     float lf = (float)l, hf = (float)h;
@@ -276,6 +279,47 @@ bool instance_world_box(const float* m, const float* lo, const float* hi, float*
     out[3 + i] = hf;
   }
   return true;
+}
+
+// Far-origin bound (reading A27, round 2): the world box above holds the
+// instance for a ray whose origin satisfies |o|_inf <= R, where the fp32 ray map
+// o' = ((A_i0 o_x + A_i1 o_y) + A_i2 o_z) + b_i, d' = (A d) (3 products, 3 sums)
+// errs by |do'| <= g5 (|A||o| + |b|), |dd'| <= g4 |A||d| (componentwise, g_n = n u /
+// (1 - n u)).  A point of the mapped ray that reaches the object box is then within
+// |A^-1| (|do'| + t |dd'|) of the exact world ray, and t |A||d| <= k t |Ad| <=
+// k (mag_obj + |A||o| + |b|) with k = ||A|| ||A^-1|| (inf-norms), so the world-space
+// displacement is at most ||A^-1|| [g5 (1 + k)(||A|| R + |b|) + g4 k mag_obj]; the box
+// pad P (2^-10 (diagonal + max |coord|)) covers it for R up to the value returned
+// (halved for margin; 0 if even R = 0 is not covered).  Rays beyond the minimum of
+// this over all instances take the linear path over every instance instead of the
+// top-level BVH (trace_instances_kernel), which is the definition itself.
+double instance_safe_range(const float* m, const float* obj_lo, const float* obj_hi, double pad) {
+  const double a[3][3] = {{m[0], m[1], m[2]}, {m[4], m[5], m[6]}, {m[8], m[9], m[10]}};
+  const double bv[3] = {m[3], m[7], m[11]};
+  const double det = a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
+                     a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
+                     a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+  double inv[3][3];
+  inv[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) / det;
+  inv[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) / det;
+  inv[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) / det;
+  inv[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) / det;
+  inv[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) / det;
+  inv[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) / det;
+  inv[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) / det;
+  inv[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) / det;
+  inv[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) / det;
+  double nA = 0.0, nI = 0.0, nb = 0.0, mag = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    nA = std::max(nA, std::fabs(a[i][0]) + std::fabs(a[i][1]) + std::fabs(a[i][2]));
+    nI = std::max(nI, std::fabs(inv[i][0]) + std::fabs(inv[i][1]) + std::fabs(inv[i][2]));
+    nb = std::max(nb, std::fabs(bv[i]));
+    mag = std::max(mag, std::max(std::fabs((double)obj_lo[i]), std::fabs((double)obj_hi[i])));
+  }
+  const double u = std::ldexp(1.0, -24), g4 = 4 * u / (1 - 4 * u), g5 = 5 * u / (1 - 5 * u);
+  const double k = nA * nI;
+  const double r = (pad / nI - g4 * k * mag - g5 * (1.0 + k) * nb) / (g5 * (1.0 + k) * nA);
+  return r > 0.0 ? 0.5 * r : 0.0;
 }
 
 void free_instances(vsr_instances* I) {
@@ -317,6 +361,7 @@ vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
       prm.sah_bins > 256 || !(prm.traversal_cost >= 0.0f) || !(prm.intersection_cost > 0.0f))
     return fail(VSR_ERR_INVALID_ARG, "invalid build params");
   std::vector<float> boxes(6 * (size_t)num_instances);
+  double r_safe = INFINITY;
   for (uint32_t i = 0; i < num_instances; ++i) {
     const vsr_instance& in = instances[i];
     if (in.bvh >= num_scenes)
@@ -325,13 +370,21 @@ vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
       if (!std::isfinite(x))
         return fail(VSR_ERR_INVALID_ARG, "instance " + std::to_string(i) + ": non-finite matrix");
     const DevScene& d = scenes[in.bvh]->dev;
-    if (!instance_world_box(in.object_from_world, d.root_lo, d.root_hi, boxes.data() + 6 * (size_t)i))
+    double pad = 0.0;
+    if (!instance_world_box(in.object_from_world, d.root_lo, d.root_hi, boxes.data() + 6 * (size_t)i,
+                            &pad))
       return fail(VSR_ERR_INVALID_ARG, "instance " + std::to_string(i) + ": singular matrix");
+    r_safe = std::min(r_safe, instance_safe_range(in.object_from_world, d.root_lo, d.root_hi, pad));
   }
   vsr_instances* I = new (std::nothrow) vsr_instances();
   if (!I) return fail(VSR_ERR_OOM, "instances allocation");
   I->device = scenes[0]->device;
   I->scenes.assign(scenes, scenes + num_scenes);
+  {   // rounded down to fp32: the kernel and walker compare fp32 |o_k| <= r_safe
+    float rf = (float)r_safe;
+    if ((double)rf > r_safe) rf = std::nextafter(rf, 0.0f);
+    I->r_safe = rf;
+  }
   std::vector<uint32_t> order;
   std::string err;
   vsr_status st = build_top(boxes.data(), num_instances, prm, I->top, order, err);
@@ -409,6 +462,7 @@ vsr_status vsr_instances_export(const vsr_instances* I, vsr_instances_view* v) {
   v->num_nodes = (uint32_t)I->top.nodes.size();
   v->num_instances = (uint32_t)I->records.size();
   v->max_depth = I->top.max_depth;
+  v->r_safe = I->r_safe;
   if (v->nodes && !I->top.nodes.empty())
     std::memcpy(v->nodes, I->top.nodes.data(), I->top.nodes.size() * sizeof(PairNode));
   if (v->records) std::memcpy(v->records, I->records.data(), I->records.size() * sizeof(Instance));
@@ -461,6 +515,8 @@ vsr_status instances_trace(vsr_instances* I, const vsr_ray* d_rays, uint64_t n, 
     }
   p.list_count = (uint32_t)I->scenes.size();
   p.instances = I->d_records;
+  p.num_instances = (uint32_t)I->records.size();
+  p.inst_r_safe = I->r_safe;
   p.which = d_inst;
   DeviceGuard dg(I->device);
   if (dg.err != cudaSuccess) return cuda_fail(dg.err, "cudaSetDevice");

@@ -101,6 +101,11 @@ __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& 
   return Q == kAny && better;
 }
 
+// A ray whose origin lies beyond the instances' proven range (|o|_inf > r_safe).
+__device__ __forceinline__ bool far_origin(const TraceParams& p, const RayCtx& r) {
+  return fmax3(fabsf(r.ox), fabsf(r.oy), fabsf(r.oz)) > p.inst_r_safe;
+}
+
 template <int Q, class I>
 __global__ void __launch_bounds__(kBlock, VSR_INST_MINB) trace_instances_kernel(const TraceParams p) {
   const uint64_t blk = launch_block(p);
@@ -110,7 +115,13 @@ __global__ void __launch_bounds__(kBlock, VSR_INST_MINB) trace_instances_kernel(
   Trav T;
   StackEntry<Q> stack[kInstStack];   // top level below, the current instance's entries above
   uint32_t hit_in = 0xFFFFFFFFu;
-  if (start_ray(p, T, isect, id)) {   // world ray; counted test of the top-level root box
+  const bool go = start_ray(p, T, isect, id);   // world ray; counted test of the top-level root box
+  if (far_origin(p, T.r)) {
+    // beyond r_safe the world boxes are not proven conservative for the fp32 ray map:
+    // every instance in leaf order, whatever the top level says (reading A27)
+    for (uint32_t k = 0; k < p.num_instances; ++k)
+      if (instance_leaf<Q>(p, T, isect, stack, k, hit_in)) break;
+  } else if (go) {
     const int woct = warp_octant(T.r);
     for (;;) {
       if (!descend_oct(p.scene, T, isect, stack, woct)) break;
@@ -178,6 +189,30 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_multi_kernel(cons
   write_multi<I, K>(p, id, mb, isect);
 }
 
+// Instance k of the multi-hit query: the bottom traversal into the shared K-buffer.
+template <class I, int K>
+__device__ __forceinline__ void instance_leaf_multi(const TraceParams& p, Trav& T, I& isect,
+                                                    float2* stack, uint32_t k,
+                                                    MultiBuf<K, true>& mb) {
+  const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
+  const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
+  const uint32_t b = __float_as_uint(ex.x);
+  const DevScene& S = p.list[b];
+  bind_scene_data(isect, p.list_data[b]);
+  Trav B = T;
+  float4 oa, ob;
+  to_object(r0, r1, r2, T.r, oa, ob);
+  make_ray(B.r, oa, ob);
+  B.sp = 0;
+  B.cur = S.root_ref;
+  const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1], S.root_hi[2]};
+  float tn;
+  if (!box_hook(isect, B.r, root, B.best_t, tn)) return;
+  mb.cur_src = __float_as_uint(ex.y);
+  traverse<kMulti>(S, B, isect, stack, warp_octant(B.r), mb);
+  T.best_t = B.best_t;   // a full buffer's worst kept t prunes the rest
+}
+
 template <class I, int K>
 __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_multi_kernel(const TraceParams p) {
   const uint64_t blk = launch_block(p);
@@ -189,32 +224,16 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_instances_multi_kernel
   MultiBuf<K, true> mb;
   mb.n = 0;
   mb.maxk = p.max_hits;
-  if (start_ray(p, T, isect, id)) {   // world ray; counted test of the top-level root box
+  const bool go = start_ray(p, T, isect, id);   // world ray; counted test of the top-level root box
+  if (far_origin(p, T.r)) {   // beyond r_safe: every instance (reading A27)
+    for (uint32_t k = 0; k < p.num_instances; ++k) instance_leaf_multi(p, T, isect, stack, k, mb);
+  } else if (go) {
     const int woct = warp_octant(T.r);
     for (;;) {
       if (!descend_oct(p.scene, T, isect, stack, woct)) break;
       const uint32_t first = T.cur & kLeafFirstMask;
       const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
-      for (uint32_t k = first; k < end; ++k) {
-        const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
-        const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
-        const uint32_t b = __float_as_uint(ex.x);
-        const DevScene& S = p.list[b];
-        bind_scene_data(isect, p.list_data[b]);
-        Trav B = T;
-        float4 oa, ob;
-        to_object(r0, r1, r2, T.r, oa, ob);
-        make_ray(B.r, oa, ob);
-        B.sp = 0;
-        B.cur = S.root_ref;
-        const Aabb root{S.root_lo[0], S.root_lo[1], S.root_lo[2], S.root_hi[0], S.root_hi[1],
-                        S.root_hi[2]};
-        float tn;
-        if (!box_hook(isect, B.r, root, B.best_t, tn)) continue;
-        mb.cur_src = __float_as_uint(ex.y);
-        traverse<kMulti>(S, B, isect, stack + T.sp, warp_octant(B.r), mb);
-        T.best_t = B.best_t;   // a full buffer's worst kept t prunes the rest
-      }
+      for (uint32_t k = first; k < end; ++k) instance_leaf_multi(p, T, isect, stack + T.sp, k, mb);
       if (!pop(T, stack)) break;
     }
   }

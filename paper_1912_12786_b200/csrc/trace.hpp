@@ -38,6 +38,8 @@ struct TraceParams {
   uint32_t list_count;
   uint32_t* which;               // list / instance query: optional per-ray element of the hit
   const Instance* instances;     // instance query: records in top-level leaf order (p.scene = top)
+  uint32_t num_instances;        // instance query: number of records
+  float inst_r_safe;             // instance query: origins beyond take the linear path (A27)
   uint32_t out_tile, out_rank, out_world;   // vsr_trace_tiles output mapping (world 0: identity)
   int gen;                       // 1: rays generated in-kernel from `cam` (rays unused)
   Pinhole cam;

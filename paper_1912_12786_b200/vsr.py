@@ -107,7 +107,8 @@ class Instance(C.Structure):
 class InstancesView(C.Structure):
     _fields_ = [("root_ref", C.c_uint32), ("root_lo", C.c_float * 3), ("root_hi", C.c_float * 3),
                 ("num_nodes", C.c_uint32), ("num_instances", C.c_uint32),
-                ("max_depth", C.c_uint32), ("nodes", C.c_void_p), ("records", C.c_void_p)]
+                ("max_depth", C.c_uint32), ("r_safe", C.c_float), ("nodes", C.c_void_p),
+                ("records", C.c_void_p)]
 
 
 class Pinhole(C.Structure):
@@ -719,7 +720,7 @@ class Instances:
         _check(lib().vsr_instances_export(self._h, C.byref(v)))
         return {"root_ref": int(v.root_ref), "root_lo": np.array(v.root_lo, np.float32),
                 "root_hi": np.array(v.root_hi, np.float32), "nodes": nodes, "records": recs,
-                "max_depth": int(v.max_depth)}
+                "max_depth": int(v.max_depth), "r_safe": float(v.r_safe)}
 
 
 # ---- device buffers shared across processes (CUDA IPC) ----------------------------------

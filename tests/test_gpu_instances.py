@@ -166,3 +166,39 @@ def test_instanced_forest_full_frame_vs_walker(V, oracle_lib):
     assert np.array_equal(h.view(np.uint32), wh.view(np.uint32))
     assert np.array_equal(ii, wi)
     assert (h["prim"] != MISS).mean() > 0.3
+
+
+@pytest.mark.parametrize("dist", [3e2, 1e5])
+def test_instances_far_origins(V, oracle_lib, dist):
+    """Reading A27 (round 2): origins beyond the exported r_safe take the linear path over
+    every instance; at 10^4 model diagonals the GPU equals walker C bit for bit (hits,
+    instance ids, counts, both queries, multi-hit k = 4) and brute force on hit/miss and t."""
+    from tests.test_instances_cpu import _aimed_rays
+    o = oracle_lib
+    models = [W.random_soup(120, seed=s, extent=3.0) for s in (51, 52)]
+    m = random_affine(30, 53, extent=12.0)
+    bvh = np.arange(30) % 2
+    scenes, inst, top, bottoms = setup(V, models, bvh, m, 1)
+    centres = -np.einsum("kij,kj->ki", np.linalg.inv(m.reshape(-1, 3, 4)[:, :, :3].astype(np.float64)),
+                         m.reshape(-1, 3, 4)[:, :, 3].astype(np.float64))
+    rays = _aimed_rays(centres, dist, 3001, int(dist) + 1)
+    assert (np.abs(rays[:, 0:3]).max(axis=1) > top["r_safe"]).all() == (dist > 1e4)
+    for q, oq in ((V.CLOSEST, o.CLOSEST), (V.ANY, o.ANY)):
+        for name in ("DEFAULT", "COUNT", "ALPHA_TEXTURE"):
+            k = getattr(V, name)
+            h, ii, c = run(V, inst, rays, q, k)
+            wh, wi, wc = o.walk_instances(top, top["records"], bottoms, rays, oq, okind(V, o, k))
+            assert h.tobytes() == wh.tobytes() and np.array_equal(ii, wi), (name, q)
+            if c is not None:
+                assert np.array_equal(c["boxes"], wc["boxes"]) and np.array_equal(c["tris"], wc["tris"])
+    ref, _, _, _ = o.trace_instances(models, bvh, m, rays, o.CLOSEST, o.DEFAULT)
+    h, _, _ = run(V, inst, rays, V.CLOSEST, V.DEFAULT)
+    hit = ref["prim"] != MISS
+    assert hit.sum() > 100 and np.array_equal(h["prim"] != MISS, hit)
+    assert np.array_equal(h["t"][hit], ref["t"][hit])
+    r = torch.from_numpy(rays).cuda()
+    mh, mn, mi, _ = inst.trace_multi(r, 4, V.DEFAULT)
+    torch.cuda.synchronize()
+    wh4, wn4, wi4, _ = o.walk_instances_multi(top, top["records"], bottoms, rays, 4, o.DEFAULT)
+    assert V.hits_to_numpy(mh.reshape(-1, 4)).tobytes() == wh4.reshape(-1).tobytes()
+    assert np.array_equal(mn.cpu().numpy().astype(np.uint32), wn4)

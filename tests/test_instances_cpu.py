@@ -321,3 +321,47 @@ def test_instances_multi_walker(vsr, oracle_lib):
             ro = o.rays_to_object(rays.data[i:i + 1], m[q])[0]
             acc, t, u, v = o.eval_pair(models[bvh[q]], ro, int(h["prim"][i, j]), o.ALPHA_TEX)
             assert acc and (t, u, v) == (h["t"][i, j], h["u"][i, j], h["v"][i, j])
+
+
+def _aimed_rays(targets, dist, n, seed):
+    """n rays from origins `dist` away (random directions) through random target points."""
+    rng = np.random.default_rng(seed)
+    p = targets[rng.integers(0, targets.shape[0], n)] + rng.uniform(-2.0, 2.0, (n, 3))
+    u = rng.normal(size=(n, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    o = p + dist * u
+    r = np.zeros((n, 8), np.float32)
+    r[:, 0:3] = o
+    r[:, 3] = 1e-4
+    r[:, 4:7] = (p - o) * rng.uniform(0.5, 2.0, (n, 1))
+    r[:, 7] = np.inf
+    return r
+
+
+@pytest.mark.parametrize("dist", [3e2, 1e5])
+def test_instances_conservative_at_any_distance(vsr, oracle_lib, dist):
+    """Reading A27, round 2: the instance world boxes are proven conservative only for ray
+    origins with max |o_k| <= r_safe (exported); beyond it the walk visits every instance.
+    At 10^4 model diagonals (origin 1e5 away, model diagonal ~10) the walker over the
+    product's top level must equal brute force over all instances, as it does near by."""
+    o = oracle_lib
+    models = [W.random_soup(120, seed=s, extent=3.0) for s in (51, 52)]
+    m = random_affine(30, 53, extent=12.0)
+    bvh = np.arange(30) % 2
+    scenes, inst = _host_instances(vsr, models, bvh, m, 1)
+    top = inst.export()
+    assert 100.0 < top["r_safe"] < 1e5      # non-trivial, and exceeded by the far rays
+    bottoms = [bvh_check.to_oracle(s.export()) for s in scenes]
+    centres = -np.einsum("kij,kj->ki", np.linalg.inv(m.reshape(-1, 3, 4)[:, :, :3].astype(np.float64)),
+                         m.reshape(-1, 3, 4)[:, :, 3].astype(np.float64))
+    rays = _aimed_rays(centres, dist, 1500, int(dist))
+    far = np.abs(rays[:, 0:3]).max(axis=1) > top["r_safe"]
+    assert far.all() if dist > 1e4 else not far.any()
+    ref, rinst, fl, nt = o.trace_instances(models, bvh, m, rays, o.CLOSEST, o.DEFAULT)
+    h, winst, c = o.walk_instances(top, top["records"], bottoms, rays, o.CLOSEST, o.DEFAULT)
+    hit = ref["prim"] != MISS
+    assert hit.sum() > 100
+    assert np.array_equal(h["prim"] != MISS, hit)
+    assert np.array_equal(h["t"][hit], ref["t"][hit])
+    if dist > 1e4:   # the linear path: the top root box (1) + every instance's root box
+        assert np.all(c["boxes"] >= 1 + 30)

@@ -70,10 +70,13 @@ MUTANTS = [
      "instance map: direction by the transposed matrix"),
     ("walker.c", "  S->c.boxes++;\n  if (!slab(b->root_lo", "  if (!slab(b->root_lo",
      "instances: bottom root test not counted"),
-    ("walker.c", "if ((S.have && !had) || S.best_t < bt) which = in->index;",
-     "if ((S.have && !had) || S.best_t < bt) which = k;",
+    ("walker.c", "if ((S->have && !had) || S->best_t < bt) *which = in->index;",
+     "if ((S->have && !had) || S->best_t < bt) *which = k;",
      "instances: leaf position reported instead of the caller's index"),
-    ("walker.c", "        if (stop) goto done;", "", "instances: any-hit keeps walking after a hit"),
+    ("walker.c", "  return stop;\n}\n\nstatic void walk_instances_one", "  return 0;\n}\n\nstatic void walk_instances_one",
+     "instances: any-hit keeps walking after a hit"),
+    ("walker.c", "    if (fmaxf(fmaxf(fabsf(o[0]), fabsf(o[1])), fabsf(o[2])) > jb->r_safe) {",
+     "    if (0) {", "instances: far origins walk the unproven top level (reading A27)"),
     ("oracle.c", "  float x = s * (float)w - 0.5f;\n  float y = t * (float)h - 0.5f;",
      "  float x = s * (float)w;\n  float y = t * (float)h - 0.5f;", "bilinear: texel-centre offset dropped in x"),
     ("oracle.c", "return ((1.0f - fx) * a00 + fx * a10) * (1.0f - fy) + ((1.0f - fx) * a01 + fx * a11) * fy;",
