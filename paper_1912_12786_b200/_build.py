@@ -67,6 +67,20 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     return target
 
 
+CHECKED = os.path.join(ROOT, "variants", "libvsr_checked.so")
+
+
+def build_checked(force: bool = False) -> str:
+    """The bounds-checked variant (-DVSR_CHECKED=1: device-side index checks that trap;
+    tests/test_gpu_checked.py) — the kernels' memory-safety evidence, compute-sanitizer
+    being closed on this GPU pool.  Rebuilt when the main library is newer."""
+    if (not force and os.path.exists(CHECKED) and os.path.exists(LIB)
+            and os.path.getmtime(CHECKED) >= os.path.getmtime(LIB) and not _stale()):
+        return CHECKED
+    os.makedirs(os.path.dirname(CHECKED), exist_ok=True)
+    return build(out=CHECKED, defines=("VSR_CHECKED=1",))
+
+
 if __name__ == "__main__":
     args = [a for a in sys.argv[1:] if not a.startswith("-")]
     defs = tuple(a[2:] for a in sys.argv[1:] if a.startswith("-D"))

@@ -185,6 +185,7 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   p.data.sides = s->d_sides;
   p.data.descs = s->d_texdescs;
   p.data.texels = s->d_texels;
+  p.data.num_texels = s->num_texels;
   p.data.a_min = alpha_min_a8(ip.alpha_threshold);
   p.data.fm = (float)ip.checker_freq;
   p.data.thr = ip.alpha_threshold;

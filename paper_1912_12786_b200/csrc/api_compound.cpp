@@ -40,7 +40,7 @@ const IsectData* compound_planes(PlaneData& pd, const std::vector<vsr_scene*>& s
     const uint32_t* b = alpha_plane(scenes[k], a_min, stream);
     if (!b) return nullptr;
     data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f,
-                        0.0f, b};
+                        0.0f, b, scenes[k]->num_texels};
   }
   IsectData* d = nullptr;
   if (cudaMalloc(&d, sizeof(IsectData) * data.size()) != cudaSuccess ||
@@ -93,7 +93,8 @@ vsr_status vsr_group_create(vsr_scene* const* scenes, uint32_t count, vsr_group*
   }
   for (uint32_t k = 0; k < count; ++k) {
     list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f,
+                        0.0f, nullptr, scenes[k]->num_texels};
     for (int a = 0; a < 3; ++a) {
       g->lo[a] = std::min(g->lo[a], scenes[k]->dev.root_lo[a]);
       g->hi[a] = std::max(g->hi[a], scenes[k]->dev.root_hi[a]);
@@ -418,7 +419,8 @@ vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
   std::vector<IsectData> data(num_scenes);
   for (uint32_t k = 0; k < num_scenes; ++k) {
     list[k] = scenes[k]->dev;
-    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f, 0.0f};
+    data[k] = IsectData{scenes[k]->d_sides, scenes[k]->d_texdescs, scenes[k]->d_texels, 0u, 0.0f,
+                        0.0f, nullptr, scenes[k]->num_texels};
   }
   DeviceGuard dg(I->device);
   cudaError_t e;

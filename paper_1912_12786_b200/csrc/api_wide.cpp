@@ -150,6 +150,7 @@ vsr_status vsr_trace_bvh8(vsr_scene* s, const vsr_ray* d_rays, uint64_t n, vsr_q
   p.n = n;
   p.sched = kSchedDirect;
   p.wide = s->d_wnodes;
+  p.num_wide = s->num_wnodes;
   p.scene.tris = s->d_wtris;     // the wide leaf order
   p.data.sides = s->d_wsides;
   DeviceGuard g(s->device);

@@ -73,9 +73,11 @@ __device__ __forceinline__ void to_object(const float4 r0, const float4 r1, cons
 template <int Q, class I, class SE>
 __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& isect,
                                               SE* stack, uint32_t k, uint32_t& hit_in) {
+  VSR_CHECK(k < p.num_instances);
   const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
   const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
   const uint32_t b = __float_as_uint(ex.x);
+  VSR_CHECK(b < p.list_count);
   const DevScene& S = p.list[b];
   bind_scene_data(isect, p.list_data[b]);
   Trav B = T;   // running best (t, u, v, prim, have, best_t) carried in and out
@@ -194,9 +196,11 @@ template <class I, int K>
 __device__ __forceinline__ void instance_leaf_multi(const TraceParams& p, Trav& T, I& isect,
                                                     float2* stack, uint32_t k,
                                                     MultiBuf<K, true>& mb) {
+  VSR_CHECK(k < p.num_instances);
   const float4* ip = reinterpret_cast<const float4*>(p.instances + k);
   const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
   const uint32_t b = __float_as_uint(ex.x);
+  VSR_CHECK(b < p.list_count);
   const DevScene& S = p.list[b];
   bind_scene_data(isect, p.list_data[b]);
   Trav B = T;

@@ -26,6 +26,21 @@
 
 #include "layout.hpp"
 
+// Bounds-checked builds (-DVSR_CHECKED=1; compute-sanitizer is closed on this GPU pool):
+// every node, triangle, sidecar, texel, bit-plane word and stack index is checked on the
+// device and a violation traps (the launch fails; tests/test_gpu_checked.py).
+#ifndef VSR_CHECKED
+#define VSR_CHECKED 0
+#endif
+#if VSR_CHECKED
+#define VSR_CHECK(c) \
+  do {               \
+    if (!(c)) __trap(); \
+  } while (0)
+#else
+#define VSR_CHECK(c) ((void)0)
+#endif
+
 #ifndef VSR_LDG256
 #define VSR_LDG256 0   // 1: 256-bit node / ray loads — measured 3-4.5 % SLOWER (profiles/r02_tuning.md)
 #endif
@@ -503,6 +518,7 @@ __device__ __forceinline__ bool alpha_keep(const IsectData& d, const float4 s0, 
   const uint32_t tw = (dims & 0xFFFFu) + 1u, th = (dims >> 16) + 1u;
   const uint32_t i = wrap_texel(s, tw);
   const uint32_t j = wrap_texel(t, th);
+  VSR_CHECK((uint64_t)__float_as_uint(s1.z) + (uint64_t)j * tw + i < d.num_texels);
   const uint32_t a8 = __ldg(d.texels + (uint64_t)__float_as_uint(s1.z) + (uint64_t)j * tw + i);
   return a8 >= d.a_min;
 }
@@ -532,6 +548,7 @@ __device__ __forceinline__ bool alpha_keep_bits(const IsectData& d, uint32_t k, 
   const uint32_t j = wrap_texel(t, th);
   const uint32_t word = (__float_as_uint(s1.z) >> 5) +
                         ((((j >> 5) * (tw >> 5) + (i >> 5)) << 5) | (j & 31u));
+  VSR_CHECK(word < d.num_texels / 32);
   return (__ldg(d.bits + word) >> (i & 31u)) & 1u;
 }
 
@@ -559,6 +576,10 @@ __device__ __forceinline__ bool alpha_bilinear_keep(const IsectData& d, uint32_t
   const uint32_t i0 = wrap_i((int)x0, tw), i1 = wrap_i((int)x0 + 1, tw);
   const uint64_t r0 = (uint64_t)wrap_i((int)y0, th) * tw, r1 = (uint64_t)wrap_i((int)y0 + 1, th) * tw;
   const uint8_t* p = d.texels + __float_as_uint(s1.z);
+  VSR_CHECK((uint64_t)__float_as_uint(s1.z) + r0 + i0 < d.num_texels &&
+            (uint64_t)__float_as_uint(s1.z) + r0 + i1 < d.num_texels &&
+            (uint64_t)__float_as_uint(s1.z) + r1 + i0 < d.num_texels &&
+            (uint64_t)__float_as_uint(s1.z) + r1 + i1 < d.num_texels);
   const float a00 = (float)__ldg(p + r0 + i0) / 255.0f;
   const float a10 = (float)__ldg(p + r0 + i1) / 255.0f;
   const float a01 = (float)__ldg(p + r1 + i0) / 255.0f;

@@ -92,6 +92,7 @@ struct IsectData {
   float thr;        // the alpha threshold itself (bilinear variant compares filtered alpha)
   const uint32_t* bits;   // 1-bit plane of (a8 >= a_min) for this a_min, or null (see
                           // alpha_keep_bits; built per threshold by the host, a cache)
+  uint64_t num_texels;    // size of the A8 plane (bounds-checked builds, VSR_CHECKED)
 };
 
 // Pinhole camera for rays generated inside the trace kernel (vsr.h vsr_pinhole;

@@ -46,6 +46,7 @@ struct TraceParams {
   int runtime_kind;
   void* filter_fn;
   const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
+  uint32_t num_wide;             // its node count (bounds-checked builds)
 };
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);

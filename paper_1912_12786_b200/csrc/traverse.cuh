@@ -82,9 +82,11 @@ __device__ __forceinline__ bool pop(Trav& T, const uint32_t* stack) {
 }
 
 __device__ __forceinline__ void push(Trav& T, float2* stack, uint32_t ref, float tn) {
+  VSR_CHECK(T.sp < kMaxStack);
   stack[T.sp++] = make_float2(__uint_as_float(ref), tn);
 }
 __device__ __forceinline__ void push(Trav& T, uint32_t* stack, uint32_t ref, float) {
+  VSR_CHECK(T.sp < kMaxStack);
   stack[T.sp++] = ref;
 }
 
@@ -190,6 +192,7 @@ __device__ __forceinline__ void prefetch_ref(const DevScene& S, uint32_t ref) {
 template <int OCT, class I, class SE>
 __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, SE* stack) {
   while (!(T.cur & kLeafBit)) {
+    VSR_CHECK(T.cur < S.num_nodes);
     const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
     float4 nx, ny, nz, nr;
     ldg8(np, nx, ny);
@@ -216,6 +219,59 @@ __device__ __forceinline__ bool descend(const DevScene& S, Trav& T, I& isect, SE
     }
   }
   return true;
+}
+
+// ---- any-hit inner loop without divergent branches (VSR_ANY_SENTINEL) ----
+// The any-hit stack holds refs only, and its traversal pushes a sentinel ref
+// (leaf bit set) below its entries: the inner loop then never needs an "is the
+// stack empty" exit — "neither child hit" pops unconditionally, and popping the
+// sentinel leaves the loop as a leaf would.  Push, pop and the next-node choice
+// become predicated selects; the node sequence is exactly descend's (same test,
+// same order), so results and counts are unchanged.
+#ifndef VSR_ANY_SENTINEL
+#define VSR_ANY_SENTINEL 1
+#endif
+constexpr uint32_t kSentinel = 0xFFFFFFFFu;
+
+template <int OCT, class I>
+__device__ __forceinline__ void descend_any(const DevScene& S, Trav& T, I& isect, uint32_t* stack) {
+  while (!(T.cur & kLeafBit)) {
+    VSR_CHECK(T.cur < S.num_nodes);
+    const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
+    const float4 nx = __ldg(np), ny = __ldg(np + 1), nz = __ldg(np + 2);
+    const uint2 nr = __ldg(reinterpret_cast<const uint2*>(np + 3));
+    // the top entry, read unconditionally (the floor keeps T.sp >= 1): its load
+    // overlaps the node's, and the pop needs no branch
+    const uint32_t top = stack[T.sp - 1];
+    BoxPairHit h;
+    if constexpr (OCT >= 0) h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t, octant<OCT>{});
+    else h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
+    const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
+    const uint32_t nearr = (h.h0 && !(h.h1 && swap)) ? nr.x : nr.y;
+    if (h.h0 && h.h1) {
+      VSR_CHECK(T.sp < kMaxStack);
+      stack[T.sp++] = swap ? nr.x : nr.y;
+    }
+    const bool any = h.h0 || h.h1;
+    T.cur = any ? nearr : top;
+    T.sp -= any ? 0 : 1;
+  }
+}
+
+template <class I>
+__device__ __forceinline__ void descend_any_oct(const DevScene& S, Trav& T, I& isect,
+                                                uint32_t* stack, int oct) {
+  switch (oct) {
+    case 0: descend_any<0>(S, T, isect, stack); break;
+    case 1: descend_any<1>(S, T, isect, stack); break;
+    case 2: descend_any<2>(S, T, isect, stack); break;
+    case 3: descend_any<3>(S, T, isect, stack); break;
+    case 4: descend_any<4>(S, T, isect, stack); break;
+    case 5: descend_any<5>(S, T, isect, stack); break;
+    case 6: descend_any<6>(S, T, isect, stack); break;
+    case 7: descend_any<7>(S, T, isect, stack); break;
+    default: descend_any<-1>(S, T, isect, stack); break;
+  }
 }
 
 // Multi-hit accumulator ("the first N hit points"; SPEC
@@ -300,6 +356,7 @@ template <int Q, class I, class M>
 __device__ __forceinline__ bool leaf(const DevScene& S, Trav& T, I& isect, M& mb) {
   const uint32_t first = T.cur & kLeafFirstMask;
   const uint32_t end = first + ((T.cur >> kLeafCountShift) & 31u) + 1u;
+  VSR_CHECK(end <= S.num_tris);
   for (uint32_t k = first; k < end; ++k) {
     const float4* tp = reinterpret_cast<const float4*>(S.tris + k);
     const TriData td{__ldg(tp), __ldg(tp + 1), __ldg(tp + 2)};
@@ -358,9 +415,19 @@ __device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect
 template <int Q, class I, class SE, class M = NoMulti>
 __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, SE* stack,
                                          int oct, M& mb) {
-  for (;;) {
-    const bool at_leaf = descend_oct(S, T, isect, stack, oct);
-    if (!at_leaf || leaf<Q>(S, T, isect, mb) || !pop(T, stack)) return;
+  if constexpr (std::is_same<SE, uint32_t>::value && VSR_ANY_SENTINEL) {
+    stack[T.sp++] = kSentinel;   // the stack's floor (see descend_any)
+    for (;;) {
+      descend_any_oct(S, T, isect, stack, oct);
+      if (T.cur == kSentinel) return;                 // popped the floor: done
+      if (leaf<Q>(S, T, isect, mb)) return;           // any-hit accepted a primitive
+      T.cur = stack[--T.sp];                          // next entry (possibly the floor)
+    }
+  } else {
+    for (;;) {
+      const bool at_leaf = descend_oct(S, T, isect, stack, oct);
+      if (!at_leaf || leaf<Q>(S, T, isect, mb) || !pop(T, stack)) return;
+    }
   }
 }
 
@@ -467,6 +534,7 @@ __device__ __forceinline__ void bind_scene_data(I& isect, const IsectData& d) {
     isect.d.descs = d.descs;
     isect.d.texels = d.texels;
     isect.d.bits = d.bits;     // the element's 1-bit plane (alpha_bits_intersector)
+    isect.d.num_texels = d.num_texels;
   } else {
     (void)d;
   }

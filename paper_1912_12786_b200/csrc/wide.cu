@@ -57,6 +57,7 @@ __device__ __forceinline__ void traverse_wide(const TraceParams& p, Trav& T, I& 
   uint32_t node = 0;
   int sp = 0;
   for (;;) {
+    VSR_CHECK(node < p.num_wide);
     const float4* np = reinterpret_cast<const float4*>(W + node);
     AabbOct b;
     b.h = __ldg(np);
@@ -83,6 +84,7 @@ __device__ __forceinline__ void traverse_wide(const TraceParams& p, Trav& T, I& 
     if (ik) {   // descend into the first inner child, keep the rest as a group
       const int s = (__ffs(ik) - 1) ^ (OCT >= 0 ? OCT : oct);
       ik &= ik - 1;
+      VSR_CHECK(sp < kMaxStack);
       if (ik) stack[sp++] = make_uint2(w1.x, imask | ik << 8);
       node = w1.x + __popc(imask & ((1u << s) - 1u));
       continue;

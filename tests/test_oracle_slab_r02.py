@@ -83,3 +83,121 @@ def test_overflowing_origin_term_never_culls():
     hit, tn, tf = oracle.slab([-1, -1, -1], [1, 1, 1],
                               np.array([1e30, 0, -2, 1e-4, 0, 0, 1, np.inf], np.float32))
     assert hit and not np.isnan(tn) and tf == np.inf
+
+
+# ---- conservativeness against exact rational arithmetic (the definition of a hit) ----------
+from fractions import Fraction as Fr  # noqa: E402
+
+
+def _exact_entry(lo, hi, o, d, tmin, tmax):
+    """Exact (rational) intersection of the segment o + t d, t in [tmin, tmax], with the
+    closed box [lo, hi]: the entry t, or None if they do not meet."""
+    a, b = Fr(float(tmin)), (Fr(float(tmax)) if np.isfinite(tmax) else None)
+    for k in range(3):
+        ok, dk = Fr(float(o[k])), Fr(float(d[k]))
+        lk, hk = Fr(float(lo[k])), Fr(float(hi[k]))
+        if dk == 0:
+            if not (lk <= ok <= hk):
+                return None
+            continue
+        t0, t1 = (lk - ok) / dk, (hk - ok) / dk
+        if t0 > t1:
+            t0, t1 = t1, t0
+        a = max(a, t0)
+        b = t1 if b is None else min(b, t1)
+    return a if (b is None or a <= b) else None
+
+
+def _grazing_cases(n, seed, far):
+    """Boxes near the coordinate origin, ray origins `far` away along random directions,
+    aimed at points ON the box boundary (edges and corners): the exact segment touches the
+    box, so the inclusive test must report a hit.  Non-dyadic directions make inv and
+    o * inv inexact."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        c = rng.uniform(-2, 2, 3)
+        h = rng.uniform(1e-3, 1.0, 3)
+        lo, hi = (c - h).astype(np.float32), (c + h).astype(np.float32)
+        p = rng.uniform(lo, hi)
+        snap = rng.integers(1, 4)   # snap 1..3 coordinates to the boundary: faces, edges, corners
+        for k in rng.choice(3, snap, replace=False):
+            p[k] = lo[k] if rng.random() < 0.5 else hi[k]
+        u = rng.normal(size=3)
+        u /= np.linalg.norm(u)
+        o = (p + far * u).astype(np.float32)
+        d = ((p - o) * rng.uniform(0.3, 3.0)).astype(np.float32)
+        out.append((lo, hi, o, d))
+    return out
+
+
+@pytest.mark.parametrize("far", [3.0, 1e3, 1e6])
+def test_slab_conservative_vs_exact(far):
+    """Every box the exact segment meets is reported hit by the fp32 test (tmax = +inf)."""
+    met = 0
+    for lo, hi, o, d in _grazing_cases(600, int(far) + 3, far):
+        if _exact_entry(lo, hi, o, d, np.float32(1e-4), np.inf) is None:
+            continue
+        met += 1
+        hit, _, _ = oracle.slab(lo, hi, np.array([*o, 1e-4, *d, np.inf], np.float32))
+        assert hit, (lo, hi, o, d)
+    assert met > 100
+
+
+@pytest.mark.parametrize("far", [1e3, 1e6])
+def test_slab_best_t_bound_conservative(far):
+    """A box whose exact entry t* is <= best_t must not be culled: best_t = the float just
+    at or above t* (the tightest admissible bound), rays whose origin term o*inv is large
+    against t* (the fma form's absolute error e is then far above u t*)."""
+    met = 0
+    for lo, hi, o, d in _grazing_cases(600, int(far) + 7, far):
+        t_star = _exact_entry(lo, hi, o, d, np.float32(1e-4), np.inf)
+        if t_star is None or t_star <= 0:
+            continue
+        bt = np.float32(float(t_star))
+        if Fr(float(bt)) < t_star:
+            bt = np.nextafter(bt, np.float32(np.inf))
+        met += 1
+        hit, _, _ = oracle.slab(lo, hi, np.array([*o, 1e-4, *d, np.inf], np.float32), best_t=float(bt))
+        assert hit, (lo, hi, o, d, float(bt))
+    assert met > 100
+
+
+def _rn32(x):
+    """Round a rational to the nearest float32 (ties to even), exactly — no double rounding."""
+    if x == 0:
+        return np.float32(0.0)
+    s = -1 if x < 0 else 1
+    a = abs(x)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fr(2) ** e > a:
+        e -= 1
+    e = max(e, -126)                       # subnormals share the minimum exponent
+    scaled = a / Fr(2) ** (e - 23)         # 24-bit mantissa scale
+    q, r = divmod(scaled.numerator, scaled.denominator)
+    if 2 * r > scaled.denominator or (2 * r == scaled.denominator and q % 2 == 1):
+        q += 1
+    return np.float32(s * float(Fr(q) * Fr(2) ** (e - 23)))
+
+
+def test_plane_crossing_is_one_rounding():
+    """Contract r02's plane crossing is t = RN(plane * inv + noi) — ONE rounding of the
+    exact value (an fma), with noi = RN(-(o * inv)).  Checked on the walker's entry value
+    against exact rational arithmetic: tn = max(min over each axis's two planes, tmin)."""
+    rng = np.random.default_rng(99)
+    checked = 0
+    for lo, hi, o, d in _grazing_cases(300, 99, 1e3):
+        ray = np.array([*o, 1e-4, *d, np.inf], np.float32)
+        inv = [np.float32(1.0) / (d[k] if abs(d[k]) > 2.0 ** -80 else np.copysign(np.float32(2.0 ** -80), d[k]))
+               for k in range(3)]
+        ts = []
+        for k in range(3):
+            noi = _rn32(-(Fr(float(o[k])) * Fr(float(inv[k]))))
+            a = _rn32(Fr(float(lo[k])) * Fr(float(inv[k])) + Fr(float(noi)))
+            b = _rn32(Fr(float(hi[k])) * Fr(float(inv[k])) + Fr(float(noi)))
+            ts.append(min(a, b))
+        tn_expect = max(max(ts), np.float32(1e-4))
+        _, tn, _ = oracle.slab(lo, hi, ray)
+        assert np.float32(tn) == tn_expect, (tn, tn_expect)
+        checked += 1
+    assert checked == 300 and rng is not None
