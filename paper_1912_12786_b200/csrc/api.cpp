@@ -210,7 +210,9 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   const int refill = ev ? std::atoi(ev) : 32;
   p.refill = refill < 1 ? 1 : (refill > 32 ? 32 : refill);
   const char* es = std::getenv("VSR_SCHED");
-  p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent : kSchedDirect;
+  p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent
+            : (es && std::strcmp(es, "warp") == 0)      ? kSchedWarp
+                                                         : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass

@@ -201,6 +201,67 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
 #endif
 }
 
+// Warp-granularity dynamic schedule (VSR_SCHED=warp): a grid sized to
+// residency; each warp claims 32-ray chunks in launch-slot order (chunk c =
+// quarter c & 3 of ray block perm[c >> 2], so the longest-first order holds at
+// 32-ray granularity) with one atomicAdd per chunk, and claims its NEXT chunk
+// before tracing the current one so that chunk's rays are prefetched into L2
+// while this one traces (the ray load is otherwise a DRAM round trip per new
+// CTA).  Lanes never mix chunks (coherent primary rays stay together); the
+// warp takes a new chunk only when all 32 lanes are done.  Per-ray results are
+// independent of the schedule.
+__device__ __forceinline__ uint64_t chunk_first_ray(const TraceParams& p, unsigned long long c) {
+  const uint64_t blk = p.perm ? (uint64_t)__ldcg(p.perm + (c >> 2)) : (uint64_t)(c >> 2);
+  return blk * kBlock + (c & 3ull) * 32ull;
+}
+
+template <int Q, class I, bool OCC = false>
+__global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB))
+    trace_kernel_warp(const TraceParams p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.hist_reset && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) p.hist_reset[i] = 0u;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned long long nchunks = (p.n + 31ull) / 32ull;
+  unsigned long long* ctr = p.counter;
+  unsigned long long c = 0;
+  if (lane == 0) c = atomicAdd(ctr, 1ull);
+  c = __shfl_sync(kFull, c, 0);
+  while (c < nchunks) {
+    unsigned long long nx = 0;
+    if (lane == 0) nx = atomicAdd(ctr, 1ull);
+    nx = __shfl_sync(kFull, nx, 0);
+    if (nx < nchunks) {   // the next chunk's rays toward L2 while this chunk traces
+      const uint64_t nid = chunk_first_ray(p, nx) + lane;
+      if (nid < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.rays + 2 * nid));
+    }
+    const uint64_t id = chunk_first_ray(p, c) + lane;
+    if (id < p.n) {
+      I isect = make_isect<I>(p);
+      Trav T;
+      StackEntry<Q> stack[kMaxStack];
+      const bool go = start_ray(p, T, isect, id);
+      const unsigned live = __activemask();
+      const int oct = ray_octant(T.r);
+      const int woct = __match_any_sync(live, oct) == live ? oct : 8;
+      NoMulti none;
+      if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
+      finish(p, T, isect, id);
+    }
+    c = nx;
+    __syncwarp();
+  }
+  // the launch's last warp resets the counter slot for a later launch
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long warps = (unsigned long long)gridDim.x * (kBlock / 32);
+    if (atomicAdd(ctr + 1, 1ull) == warps - 1ull) {
+      atomicExch(ctr, 0ull);
+      atomicExch(ctr + 1, 0ull);
+    }
+  }
+}
+
 // Multi-hit query: same traversal, the leaf accepts into a K-entry sorted
 // buffer (runtime max_hits <= K).  Output ray-major: hits[id*max_hits + j].
 template <class I, int K>
@@ -323,7 +384,26 @@ int sm_count() {
 template <int Q, class I>
 cudaError_t launch(const TraceParams& p, cudaStream_t st) {
   const uint64_t need = (p.n + kBlock - 1) / kBlock;
-  if (p.sched == kSchedPersistent) {
+  if (p.sched == kSchedWarp && p.counter && !p.gen && !p.out_world) {
+    static std::atomic<int> per_sm_cache[2];   // resident blocks per SM (OCC false / true)
+    int per_sm = per_sm_cache[p.occ ? 1 : 0].load(std::memory_order_relaxed);
+    if (per_sm == 0) {
+      int nb = 0;
+      cudaError_t e = p.occ ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                  &nb, trace_kernel_warp<Q, I, true>, kBlock, 0)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                  &nb, trace_kernel_warp<Q, I, false>, kBlock, 0);
+      if (e != cudaSuccess) return e;
+      per_sm = nb > 0 ? nb : 1;
+      per_sm_cache[p.occ ? 1 : 0].store(per_sm, std::memory_order_relaxed);
+    }
+    const uint64_t full = (uint64_t)per_sm * sm_count();
+    const uint64_t grid = need < full ? need : full;
+    const cudaError_t e =
+        p.occ ? launch_k(trace_kernel_warp<Q, I, true>, grid, kBlock, p.perm && p.pdl, st, p)
+              : launch_k(trace_kernel_warp<Q, I, false>, grid, kBlock, p.perm && p.pdl, st, p);
+    if (e != cudaSuccess) return e;
+  } else if (p.sched == kSchedPersistent) {
     static std::atomic<int> per_sm_cache{0};   // resident blocks per SM for this instantiation
     int per_sm = per_sm_cache.load(std::memory_order_relaxed);
     if (per_sm == 0) {
@@ -455,7 +535,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     }
     return e;
   };
-  if (p.order && p.sched == kSchedDirect && nblocks >= 2ull * sm_count() && nblocks < (1u << 24)) {
+  if (p.order && (p.sched == kSchedDirect || p.sched == kSchedWarp) && nblocks >= 2ull * sm_count() &&
+      nblocks < (1u << 24)) {
     // the owner's per-stream scratch (api.cpp ScratchSet); a stream-ordered
     // allocation only past 16 streams per owner
     const size_t bytes = order_scratch_bytes(p.n);

@@ -11,7 +11,7 @@ namespace vsr {
 
 struct WideNode;
 
-enum : int { kSchedDirect = 0, kSchedPersistent = 1 };
+enum : int { kSchedDirect = 0, kSchedPersistent = 1, kSchedWarp = 2 };
 
 // Kernel parameters (passed by value: they live in the constant parameter bank).
 struct TraceParams {
