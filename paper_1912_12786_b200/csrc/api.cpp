@@ -75,6 +75,18 @@ vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const f
   d.num_nodes = num_nodes;
   d.num_tris = num_tris;
   d.num_textures = num_textures;
+  {   // density grid: the order pass's cost proxy (scheduling only; results never depend on it)
+    density_grid_dims(d.root_lo, d.root_hi, d.gdim, d.gscale);
+    const size_t cells = (size_t)d.gdim[0] * d.gdim[1] * d.gdim[2];
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s->d_grid), cells * sizeof(uint32_t));
+    if (e != cudaSuccess) return cuda_fail(e, "density grid");
+    if ((e = cudaMemset(s->d_grid, 0, cells * sizeof(uint32_t))) != cudaSuccess ||
+        (e = build_density_grid(s->d_tris, num_tris, d.root_lo, d.gdim, d.gscale, s->d_grid,
+                                nullptr)) != cudaSuccess ||
+        (e = cudaDeviceSynchronize()) != cudaSuccess)
+      return cuda_fail(e, "density grid");
+    d.grid = s->d_grid;
+  }
   s->stats.num_nodes = num_nodes;
   s->stats.num_tris = num_tris;
   s->stats.num_textures = num_textures;
@@ -215,6 +227,9 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
                                                          : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
+  // order pass cost proxy: "grid" (density-grid march) or "len" (segment length in the root box)
+  const char* eg = std::getenv("VSR_ORDER_PROXY");
+  p.order_proxy = (eg && std::strcmp(eg, "grid") == 0) ? 1 : 0;
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
   p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
   // 12-CTA occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)

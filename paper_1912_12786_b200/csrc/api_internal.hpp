@@ -107,6 +107,7 @@ struct vsr_scene {
   TexDesc* d_texdescs = nullptr;
   uint8_t* d_texels = nullptr;
   unsigned long long* d_counters = nullptr;   // persistent-kernel work counters
+  uint32_t* d_grid = nullptr;                  // density grid (order-pass cost proxy)
   std::atomic<uint32_t> launch_seq{0};
   uint64_t num_texels = 0;
   vsr_stats stats{};
@@ -169,6 +170,8 @@ struct vsr_scene {
     cudaFree(d_texdescs);
     cudaFree(d_texels);
     cudaFree(d_counters);
+    cudaFree(d_grid);
+    d_grid = nullptr;
     d_nodes = nullptr;
     d_tris = nullptr;
     d_sides = nullptr;

@@ -74,6 +74,11 @@ struct DevScene {
   float root_lo[3], root_hi[3];
   uint32_t num_nodes, num_tris, num_textures;
   unsigned long long* counters;   // kCounterSlots x 2, zero-initialised
+  // density grid over the root box (scheduling hint for the order pass only): per cell
+  // the number of triangles whose box overlaps it; gscale = cells per unit length
+  const uint32_t* grid;
+  uint32_t gdim[3];
+  float gscale[3];
 };
 
 // Work-distribution counters for the persistent trace kernel: slot s holds

@@ -26,6 +26,7 @@
 // contract).
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <string>
 
@@ -77,6 +78,35 @@ __device__ uint32_t instance_cost(const TraceParams& p, const RayCtx& r, float t
   return cnt < cap ? cnt : cap;
 }
 
+// Density-grid cost proxy (order_proxy 1): the sample ray's [tn, tf] segment
+// inside the root box, sampled at kGridSamples evenly spaced points, each
+// weighted by the scene's coarse density grid (the number of triangle boxes
+// overlapping its cell): a line integral of box density.  The samples' cell
+// loads are independent, so they are all in flight at once (a 3D-DDA march
+// was measured: its chain of dependent cold loads made the order pass the
+// long pole).  Motivation: the rays that skim a dense layer (every billboard
+// box reaches down to the ground) cost far more than their segment length
+// says (tools/timeline.py: the launch's last warp started 20 us late with an
+// 83 us run).  Bucket = 6 log2(1 + integral).
+constexpr int kGridSamples = 16;
+__device__ float grid_cost(const DevScene& S, const RayCtx& r, float tn, float tf) {
+  const float step = (tf - tn) * (1.0f / kGridSamples);
+  float sum = 0.0f;
+#pragma unroll
+  for (int k = 0; k < kGridSamples; ++k) {
+    const float t = tn + ((float)k + 0.5f) * step;
+    int c[3];
+    const float pt[3] = {r.ox + t * r.dx, r.oy + t * r.dy, r.oz + t * r.dz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      int ca = (int)floorf((pt[a] - S.root_lo[a]) * S.gscale[a]);
+      c[a] = ca < 0 ? 0 : (ca >= (int)S.gdim[a] ? (int)S.gdim[a] - 1 : ca);
+    }
+    sum += (float)__ldg(S.grid + ((uint64_t)c[2] * S.gdim[1] + c[1]) * S.gdim[0] + c[0]);
+  }
+  return sum * step * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
+}
+
 template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
@@ -97,7 +127,9 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
       const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
       const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
       if (VSR_INST_COST && p.instances) len = (float)instance_cost(p, r, d.w);   // bucket index directly
-      else if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
+      else if (p.order_proxy == 1 && p.scene.grid && !p.instances) {
+        if (tf > tn) len = 6.0f * log2f(1.0f + grid_cost(p.scene, r, tn, tf));   // bucket index
+      } else if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
     }
   }
   len = fmaxf(len, __shfl_xor_sync(0xFFFFFFFFu, len, 1));
@@ -115,7 +147,8 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
     const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
     const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
     const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
-    q = (VSR_INST_COST && p.instances) ? (int)len : diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
+    q = ((VSR_INST_COST && p.instances) || (p.order_proxy == 1 && p.scene.grid && !p.instances))
+            ? (int)len : diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
     q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
     lpos = atomicAdd(lh + q, 1u);
   }
@@ -613,6 +646,57 @@ cudaError_t build_alpha_bits(const TexDesc* d_descs, uint32_t num_textures, cons
   if (num_textures == 0) return cudaSuccess;
   const unsigned gx = (unsigned)std::min<uint64_t>(4096, (max_words + 255) / 256);
   alpha_bits_kernel<<<dim3(gx ? gx : 1, num_textures), 256, 0, st>>>(d_descs, texels, a_min, d_bits);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+void density_grid_dims(const float* lo, const float* hi, uint32_t* dims, float* scale) {
+  double ext[3], vol = 1.0;
+  for (int a = 0; a < 3; ++a) {
+    ext[a] = std::max((double)hi[a] - lo[a], 1e-30);
+    vol *= ext[a];
+  }
+  // ~4096 cubic cells, then 8..32 per axis (at most 8192 cells: the cost kernel stages
+  // the grid in shared memory); thin axes (a forest's height) still get 8 layers
+  const double cell = std::max(std::cbrt(vol / 4096.0), 1e-30);
+  for (int a = 0; a < 3; ++a) {
+    double g = std::ceil(ext[a] / cell);
+    g = std::min(std::max(g, 8.0), 32.0);
+    dims[a] = (uint32_t)g;
+    scale[a] = (float)(g / ext[a]);
+  }
+}
+
+__global__ void __launch_bounds__(256) density_grid_kernel(const Tri* tris, uint32_t n, float lx,
+                                                           float ly, float lz, uint3 dims,
+                                                           float3 scale, uint32_t* grid) {
+  const uint32_t i = blockIdx.x * 256 + threadIdx.x;
+  if (i >= n) return;
+  const Tri t = tris[i];
+  const float lo[3] = {lx, ly, lz}, sc[3] = {scale.x, scale.y, scale.z};
+  const uint32_t dm[3] = {dims.x, dims.y, dims.z};
+  int c0[3], c1[3];
+  for (int a = 0; a < 3; ++a) {
+    const float v0 = t.v0[a], v1 = v0 + t.e1[a], v2 = v0 + t.e2[a];
+    const float mn = fminf(v0, fminf(v1, v2)), mx = fmaxf(v0, fmaxf(v1, v2));
+    c0[a] = max(0, min((int)dm[a] - 1, (int)floorf((mn - lo[a]) * sc[a])));
+    c1[a] = max(0, min((int)dm[a] - 1, (int)floorf((mx - lo[a]) * sc[a])));
+  }
+  int budget = 4096;   // a triangle larger than that many cells counts in its first ones only
+  for (int z = c0[2]; z <= c1[2]; ++z)
+    for (int y = c0[1]; y <= c1[1]; ++y)
+      for (int x = c0[0]; x <= c1[0]; ++x) {
+        if (budget-- <= 0) return;
+        atomicAdd(grid + ((uint64_t)z * dm[1] + y) * dm[0] + x, 1u);
+      }
+}
+
+cudaError_t build_density_grid(const Tri* d_tris, uint32_t n, const float* lo, const uint32_t* dims,
+                               const float* scale, uint32_t* d_grid, cudaStream_t st) {
+  if (n == 0) return cudaSuccess;
+  density_grid_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+      d_tris, n, lo[0], lo[1], lo[2], make_uint3(dims[0], dims[1], dims[2]),
+      make_float3(scale[0], scale[1], scale[2]), d_grid);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

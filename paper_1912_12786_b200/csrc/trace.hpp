@@ -45,6 +45,7 @@ struct TraceParams {
   Pinhole cam;
   int runtime_kind;
   void* filter_fn;
+  int order_proxy;               // order pass cost proxy: 0 segment length, 1 density-grid march
   const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
   uint32_t num_wide;             // its node count (bounds-checked builds)
 };
@@ -56,6 +57,11 @@ cudaError_t build_alpha_bits(const TexDesc* d_descs, uint32_t num_textures, cons
                              uint32_t a_min, uint32_t* d_bits, uint64_t max_words,
                              cudaStream_t st);
 size_t order_scratch_bytes(uint64_t n);
+// Density grid of a scene (order-pass cost proxy): dims chosen for ~4096 cells over the root
+// box; counts the triangles whose box overlaps each cell into d_grid (zeroed by the caller).
+void density_grid_dims(const float* lo, const float* hi, uint32_t* dims, float* scale);
+cudaError_t build_density_grid(const Tri* d_tris, uint32_t n, const float* lo, const uint32_t* dims,
+                               const float* scale, uint32_t* d_grid, cudaStream_t st);
 void set_kernel_events(void* start, void* stop);
 cudaError_t filter_fn_pointer(int kind, void** out);
 uint64_t launch_count();

@@ -25,7 +25,9 @@ q = vsr.ANY if os.environ.get("QUERY", "any") == "any" else vsr.CLOSEST
 flush = torch.zeros(64 << 20, device="cuda")
 for _ in range(5):
     flush.sum()
-    s.trace(d, q, isect, hits=hits, counts=tl)
+    # raw call: the diagnostic build writes one record per WARP into the counts buffer
+    s.trace_raw(d.data_ptr(), rays.n, q, isect, hits.data_ptr(), tl.data_ptr(),
+                torch.cuda.current_stream().cuda_stream)
 torch.cuda.synchronize()
 out = tl.cpu().numpy().view(np.uint32)[: rays.n // 32]
 np.save(os.environ.get("OUT", "gpurun_out/timeline.npy"), out)
@@ -48,3 +50,13 @@ for p in (50, 90, 99, 99.9, 100):
     print(f"warp duration p{p}: {np.percentile(dur, p):.1f} us")
 late = t0 > 0.9 * span
 print(f"warps starting in the last 10 % of the span: {late.sum()}, their mean duration {dur[late].mean() if late.any() else 0:.1f} us")
+# the critical path: the warps that end last — when did they start, how long did they run
+order = np.argsort(-t1)[:10]
+print("last-ending warps (start us, duration us, warp id):")
+for w in order:
+    print(f"  {t0[w]:7.1f} {dur[w]:7.1f} {w}")
+slow = np.argsort(-dur)[:10]
+print("slowest warps (start us, duration us, end us):")
+for w in slow:
+    print(f"  {t0[w]:7.1f} {dur[w]:7.1f} {t1[w]:7.1f}")
+print(f"lower bound from the slowest warp: {dur.max():.1f} us of the {span:.1f} us span")
