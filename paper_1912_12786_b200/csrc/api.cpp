@@ -77,7 +77,7 @@ vsr_status upload(vsr_scene* s, uint32_t root_ref, const float* root_lo, const f
   d.num_textures = num_textures;
   {   // density grid: the order pass's cost proxy (scheduling only; results never depend on it)
     density_grid_dims(d.root_lo, d.root_hi, d.gdim, d.gscale);
-    const size_t cells = (size_t)d.gdim[0] * d.gdim[1] * d.gdim[2];
+    const size_t cells = density_grid_words(d.gdim);
     cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&s->d_grid), cells * sizeof(uint32_t));
     if (e != cudaSuccess) return cuda_fail(e, "density grid");
     if ((e = cudaMemset(s->d_grid, 0, cells * sizeof(uint32_t))) != cudaSuccess ||

@@ -89,8 +89,11 @@ __device__ uint32_t instance_cost(const TraceParams& p, const RayCtx& r, float t
 // says (tools/timeline.py: the launch's last warp started 20 us late with an
 // 83 us run).  Bucket = 6 log2(1 + integral).
 constexpr int kGridSamples = 16;
+constexpr int kGridCopies = 32;   // replicas of the grid, one per CTA modulo: spreads the
+                                  // order pass's burst of loads over 32x more L2 lines
 __device__ float grid_cost(const DevScene& S, const RayCtx& r, float tn, float tf) {
   const float step = (tf - tn) * (1.0f / kGridSamples);
+  const uint32_t* grid = S.grid + (uint64_t)(blockIdx.x % kGridCopies) * S.gdim[0] * S.gdim[1] * S.gdim[2];
   float sum = 0.0f;
 #pragma unroll
   for (int k = 0; k < kGridSamples; ++k) {
@@ -102,7 +105,7 @@ __device__ float grid_cost(const DevScene& S, const RayCtx& r, float tn, float t
       int ca = (int)floorf((pt[a] - S.root_lo[a]) * S.gscale[a]);
       c[a] = ca < 0 ? 0 : (ca >= (int)S.gdim[a] ? (int)S.gdim[a] - 1 : ca);
     }
-    sum += (float)__ldg(S.grid + ((uint64_t)c[2] * S.gdim[1] + c[1]) * S.gdim[0] + c[0]);
+    sum += (float)__ldg(grid + ((uint64_t)c[2] * S.gdim[1] + c[1]) * S.gdim[0] + c[0]);
   }
   return sum * step * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
 }
@@ -111,6 +114,14 @@ template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
   asm volatile("griddepcontrol.launch_dependents;");   // let the scatter kernel's CTAs launch
+  if (p.order_proxy == 1 && p.scene.grid && !p.instances) {
+    // this CTA's grid replica toward L2 now, in parallel with the sample rays' loads, so the
+    // march below does not add a second DRAM round trip (one 128-B line per thread)
+    const uint64_t words = (uint64_t)p.scene.gdim[0] * p.scene.gdim[1] * p.scene.gdim[2];
+    const uint32_t* rep = p.scene.grid + (uint64_t)(blockIdx.x % kGridCopies) * words;
+    for (uint64_t w = (uint64_t)threadIdx.x * 32; w < words; w += 256 * 32)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(rep + w));
+  }
   const uint32_t t = blockIdx.x * 256 + threadIdx.x;   // 4 sample rays per 128-ray block
   const uint32_t b = t >> 2;
   float len = 0.0f;
@@ -698,7 +709,16 @@ cudaError_t build_density_grid(const Tri* d_tris, uint32_t n, const float* lo, c
       d_tris, n, lo[0], lo[1], lo[2], make_uint3(dims[0], dims[1], dims[2]),
       make_float3(scale[0], scale[1], scale[2]), d_grid);
   launch_counter().fetch_add(1, std::memory_order_relaxed);
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  const size_t cells = (size_t)dims[0] * dims[1] * dims[2];
+  for (int k = 1; k < kGridCopies && e == cudaSuccess; ++k)   // the replicas
+    e = cudaMemcpyAsync(d_grid + k * cells, d_grid, cells * sizeof(uint32_t),
+                        cudaMemcpyDeviceToDevice, st);
+  return e;
+}
+
+size_t density_grid_words(const uint32_t* dims) {
+  return (size_t)dims[0] * dims[1] * dims[2] * kGridCopies;
 }
 
 std::atomic<uint64_t>& launch_counter() {

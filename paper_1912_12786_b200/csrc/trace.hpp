@@ -60,6 +60,7 @@ size_t order_scratch_bytes(uint64_t n);
 // Density grid of a scene (order-pass cost proxy): dims chosen for ~4096 cells over the root
 // box; counts the triangles whose box overlaps each cell into d_grid (zeroed by the caller).
 void density_grid_dims(const float* lo, const float* hi, uint32_t* dims, float* scale);
+size_t density_grid_words(const uint32_t* dims);   // grid allocation (with its replicas)
 cudaError_t build_density_grid(const Tri* d_tris, uint32_t n, const float* lo, const uint32_t* dims,
                                const float* scale, uint32_t* d_grid, cudaStream_t st);
 void set_kernel_events(void* start, void* stop);
