@@ -227,9 +227,11 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
                                                          : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
-  // order pass cost proxy: "grid" (density-grid march) or "len" (segment length in the root box)
+  // order pass cost proxy: "grid" (density-grid line integral), "len" (segment length in the
+  // root box); unset = auto: grid for instanced queries (measured +4-5 %), len otherwise
+  // (measured: grid costs the short C2 launch +2 %, C4 -25 %; profiles/r02_tuning.md)
   const char* eg = std::getenv("VSR_ORDER_PROXY");
-  p.order_proxy = (eg && std::strcmp(eg, "grid") == 0) ? 1 : 0;
+  p.order_proxy = !eg ? 2 : (std::strcmp(eg, "grid") == 0 ? 1 : 0);
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
   p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
   // 12-CTA occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)

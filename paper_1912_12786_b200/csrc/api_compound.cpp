@@ -228,6 +228,7 @@ struct vsr_instances {
   Instance* d_records = nullptr;
   DevScene* d_list = nullptr;
   IsectData* d_data = nullptr;
+  uint32_t* d_grid = nullptr;   // density grid over the instance boxes (order-pass proxy)
 };
 
 namespace {
@@ -332,6 +333,7 @@ void free_instances(vsr_instances* I) {
   cudaFree(I->d_records);
   cudaFree(I->d_list);
   cudaFree(I->d_data);
+  cudaFree(I->d_grid);
 }
 
 }  // namespace
@@ -441,6 +443,37 @@ vsr_status vsr_instances_create(vsr_scene* const* scenes, uint32_t num_scenes,
     return cuda_fail(e, "instances upload");
   }
   I->dev.nodes = I->d_nodes;
+  {   // density grid over the instance world boxes, each weighted by nothing but its presence
+      // (order-pass cost proxy VSR_ORDER_PROXY=grid; scheduling only): a box as the triangle
+      // (lo, lo + (hi - lo), lo) covers exactly the box's cells
+    std::vector<Tri> boxes_as_tris(num_instances);
+    for (uint32_t i = 0; i < num_instances; ++i) {
+      Tri& t = boxes_as_tris[i];
+      std::memset(&t, 0, sizeof t);
+      for (int a = 0; a < 3; ++a) {
+        t.v0[a] = boxes[6 * (size_t)i + a];
+        t.e1[a] = boxes[6 * (size_t)i + 3 + a] - boxes[6 * (size_t)i + a];
+      }
+    }
+    density_grid_dims(I->dev.root_lo, I->dev.root_hi, I->dev.gdim, I->dev.gscale);
+    Tri* d_bt = nullptr;
+    const size_t words = density_grid_words(I->dev.gdim);
+    if ((e = cudaMalloc(&I->d_grid, words * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMemset(I->d_grid, 0, words * sizeof(uint32_t))) != cudaSuccess ||
+        (e = cudaMalloc(&d_bt, num_instances * sizeof(Tri))) != cudaSuccess ||
+        (e = cudaMemcpy(d_bt, boxes_as_tris.data(), num_instances * sizeof(Tri),
+                        cudaMemcpyHostToDevice)) != cudaSuccess ||
+        (e = build_density_grid(d_bt, num_instances, I->dev.root_lo, I->dev.gdim, I->dev.gscale,
+                                I->d_grid, nullptr)) != cudaSuccess ||
+        (e = cudaDeviceSynchronize()) != cudaSuccess) {
+      cudaFree(d_bt);
+      free_instances(I);
+      delete I;
+      return cuda_fail(e, "instances density grid");
+    }
+    cudaFree(d_bt);
+    I->dev.grid = I->d_grid;
+  }
   *out = I;
   return VSR_OK;
 }

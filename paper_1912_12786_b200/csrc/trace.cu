@@ -114,7 +114,9 @@ template <bool GEN>
 __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, uint32_t nblocks,
                                                          uint32_t* hist, uint32_t* slot) {
   asm volatile("griddepcontrol.launch_dependents;");   // let the scatter kernel's CTAs launch
-  if (p.order_proxy == 1 && p.scene.grid && !p.instances) {
+  const bool use_grid = p.scene.grid && (p.order_proxy == 1 ? (!p.list || p.instances)
+                                                             : (p.order_proxy == 2 && p.instances));
+  if (use_grid) {
     // this CTA's grid replica toward L2 now, in parallel with the sample rays' loads, so the
     // march below does not add a second DRAM round trip (one 128-B line per thread)
     const uint64_t words = (uint64_t)p.scene.gdim[0] * p.scene.gdim[1] * p.scene.gdim[2];
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
       const float tn = fmaxf(fmaxf(fminf(t0x, t1x), fminf(t0y, t1y)), fmaxf(fminf(t0z, t1z), a.w));
       const float tf = fminf(fminf(fmaxf(t0x, t1x), fmaxf(t0y, t1y)), fminf(fmaxf(t0z, t1z), d.w));
       if (VSR_INST_COST && p.instances) len = (float)instance_cost(p, r, d.w);   // bucket index directly
-      else if (p.order_proxy == 1 && p.scene.grid && !p.instances) {
+      else if (use_grid) {
         if (tf > tn) len = 6.0f * log2f(1.0f + grid_cost(p.scene, r, tn, tf));   // bucket index
       } else if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
     }
@@ -158,8 +160,7 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
     const float dy = p.scene.root_hi[1] - p.scene.root_lo[1];
     const float dz = p.scene.root_hi[2] - p.scene.root_lo[2];
     const float diag = sqrtf(dx * dx + dy * dy + dz * dz);
-    q = ((VSR_INST_COST && p.instances) || (p.order_proxy == 1 && p.scene.grid && !p.instances))
-            ? (int)len : diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
+    q = ((VSR_INST_COST && p.instances) || use_grid) ? (int)len : diag > 0.0f ? (int)(len / diag * kOrderBuckets) : 0;
     q = q < 0 ? 0 : (q >= kOrderBuckets ? kOrderBuckets - 1 : q);
     lpos = atomicAdd(lh + q, 1u);
   }

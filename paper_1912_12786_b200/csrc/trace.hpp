@@ -45,7 +45,7 @@ struct TraceParams {
   Pinhole cam;
   int runtime_kind;
   void* filter_fn;
-  int order_proxy;               // order pass cost proxy: 0 segment length, 1 density-grid march
+  int order_proxy;               // order pass cost proxy: 0 segment length, 1 density grid, 2 auto
   const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
   uint32_t num_wide;             // its node count (bounds-checked builds)
 };
