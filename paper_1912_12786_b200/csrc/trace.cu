@@ -26,6 +26,8 @@
 // contract).
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -599,12 +601,15 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     if (!zeroed &&
         (e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st)) != cudaSuccess)
       return done(e);
-    if (p.gen)
+    if (p.gen) {
+      apply_carveout(reinterpret_cast<const void*>(order_cost_kernel<true>));
       order_cost_kernel<true><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
           p, (uint32_t)nblocks, hist, slot);
-    else
+    } else {
+      apply_carveout(reinterpret_cast<const void*>(order_cost_kernel<false>));
       order_cost_kernel<false><<<(unsigned)((4 * nblocks + 255) / 256), 256, 0, st>>>(
           p, (uint32_t)nblocks, hist, slot);
+    }
     if ((e = cudaGetLastError()) != cudaSuccess) {
       if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
       return done(e);
@@ -720,6 +725,22 @@ cudaError_t build_density_grid(const Tri* d_tris, uint32_t n, const float* lo, c
 
 size_t density_grid_words(const uint32_t* dims) {
   return (size_t)dims[0] * dims[1] * dims[2] * kGridCopies;
+}
+
+void apply_carveout(const void* kernel) {
+  static const int pct = [] {
+    const char* e = std::getenv("VSR_CARVEOUT");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (pct < 0) return;
+  static std::mutex mu;
+  static std::vector<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  for (const void* k : done)
+    if (k == kernel) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaGetLastError();
+  done.push_back(kernel);
 }
 
 std::atomic<uint64_t>& launch_counter() {

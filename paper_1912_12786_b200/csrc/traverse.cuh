@@ -542,9 +542,14 @@ __device__ __forceinline__ void bind_scene_data(I& isect, const IsectData& d) {
 
 // <<<grid, block, 0, st>>>, as a programmatic dependent launch when `pdl`
 // (the kernel starts with griddepcontrol.wait, see launch_block).
+// VSR_CARVEOUT=<percent> (tuning knob): the preferred shared-memory carveout of every kernel
+// this library launches (0 = the most L1), set once per kernel.
+void apply_carveout(const void* kernel);
+
 template <typename... Args, typename... Act>
 cudaError_t launch_k(void (*k)(Args...), uint64_t grid, unsigned block, bool pdl, cudaStream_t st,
                      Act&&... args) {
+  apply_carveout(reinterpret_cast<const void*>(k));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(block);
