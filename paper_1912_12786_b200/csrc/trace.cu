@@ -204,6 +204,9 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
   perm[start[s >> 24] + (s & 0xFFFFFFu)] = b;
 }
 
+#ifndef VSR_KEEP_ID
+#define VSR_KEEP_ID 0
+#endif
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
@@ -231,10 +234,14 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
     const int woct = __match_any_sync(live, oct) == live ? oct : 8;
     NoMulti none;
     if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
+#if VSR_KEEP_ID
+    finish(p, T, isect, id);   // the ray index kept live across the traversal (A/B knob)
+#else
     // the ray index is recomputed (perm re-read through L2) rather than kept live
     // across the traversal: one register less in the hot loop
     const uint64_t blk2 = p.perm ? (uint64_t)__ldcg(p.perm + blockIdx.x) : (uint64_t)blockIdx.x;
     finish(p, T, isect, blk2 * kBlock + threadIdx.x);
+#endif
   }
 #ifdef VSR_TIMELINE
   // diagnostic build only: per-warp (SM id, start ns, end ns) into counts[warp]
