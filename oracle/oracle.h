@@ -182,8 +182,10 @@ typedef struct {
 /* Walker over the wide BVH: the root box of `b` (tested once, counted), then from node 0:
  * test every valid child (counted, one box each), the triangles of hit leaf children in key
  * order (key of slot s = s XOR the ray octant, ascending; octant bit k = sign bit of inv_k),
- * then descend into the hit inner child of smallest key and keep the rest as a pending group
- * (no t on the stack: a pending child is visited whatever best_t has become).  b->tris /
+ * then descend into the hit inner child of smallest key and keep the rest as a pending group;
+ * when a group member is popped, a closest-hit query re-tests its decoded box against the
+ * current best_t (one counted box test) and skips it on a miss — an any-hit query (best_t never
+ * shrinks before it ends) visits it directly.  b->tris /
  * b->sides must be the wide leaf order; b->nodes is unused.  Closest / any only. */
 int walker_trace_wide(const or_bvh* b, const or_wnode* nodes, uint32_t num_nodes,
                       const float* rays, uint64_t n, int query, int isect, float alpha_threshold,

@@ -985,27 +985,47 @@ static int walk_wide_one(const wwjob_t* jb, uint64_t r) {
         }
       }
     }
-    /* inner children: descend into the smallest key, keep the others */
+    /* inner children: descend into the smallest key, keep the others as a group (base =
+     * the parent node: a closest-hit query re-tests a pending child against the current
+     * best_t when it is popped, one counted box test on its decoded box) */
     uint32_t keys = 0;
     for (uint32_t s = 0; s < 8; ++s)
       if ((hits >> s & 1u) && (w->imask >> s & 1u)) keys |= 1u << (s ^ oct);
-    uint32_t base = w->child_base, imask = w->imask;
-    if (!keys) {
-      if (sp == 0) goto done;
-      base = st_base[sp - 1];
-      imask = st_imask[sp - 1];
-      keys = st_keys[sp - 1];
-      sp--;
-    }
-    const uint32_t k0 = (uint32_t)__builtin_ctz(keys);
-    keys &= keys - 1u;
     if (keys) {
-      if (sp >= MAX_STACK) { bad = 1; goto done; }
-      st_base[sp] = base; st_imask[sp] = imask; st_keys[sp] = keys;
-      sp++;
+      const uint32_t k0 = (uint32_t)__builtin_ctz(keys);
+      keys &= keys - 1u;
+      if (keys) {
+        if (sp >= MAX_STACK) { bad = 1; goto done; }
+        st_base[sp] = node; st_imask[sp] = w->imask; st_keys[sp] = keys;
+        sp++;
+      }
+      const uint32_t s0 = k0 ^ oct;
+      node = w->child_base + (uint32_t)__builtin_popcount(w->imask & ((1u << s0) - 1u));
+      continue;
     }
-    const uint32_t s0 = k0 ^ oct;
-    node = base + (uint32_t)__builtin_popcount(imask & ((1u << s0) - 1u));
+    for (;;) {
+      if (sp == 0) goto done;
+      const uint32_t parent = st_base[sp - 1], imask = st_imask[sp - 1];
+      uint32_t pk = st_keys[sp - 1];
+      const uint32_t k0 = (uint32_t)__builtin_ctz(pk);
+      pk &= pk - 1u;
+      if (pk) st_keys[sp - 1] = pk;
+      else sp--;
+      const uint32_t s0 = k0 ^ oct;
+      if (parent >= jb->num_nodes) { bad = 1; goto done; }
+      const or_wnode* pw = &jb->nodes[parent];
+      if (jb->query == OR_CLOSEST) {
+        float lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = wide_plane(pw->qlo[a][s0], pw->e[a], pw->pm[a]);
+          hi[a] = wide_plane(pw->qhi[a][s0], pw->e[a], pw->pm[a]);
+        }
+        c.boxes++;
+        if (!slab(lo, hi, o, inv, tmin, best_t, &tn)) continue;
+      }
+      node = pw->child_base + (uint32_t)__builtin_popcount(imask & ((1u << s0) - 1u));
+      break;
+    }
   }
 done:
   jb->hits[r] = best;

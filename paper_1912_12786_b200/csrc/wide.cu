@@ -85,19 +85,60 @@ __device__ __forceinline__ void traverse_wide(const TraceParams& p, Trav& T, I& 
       const int s = (__ffs(ik) - 1) ^ (OCT >= 0 ? OCT : oct);
       ik &= ik - 1;
       VSR_CHECK(sp < kMaxStack);
-      if (ik) stack[sp++] = make_uint2(w1.x, imask | ik << 8);
+      if constexpr (Q == kClosest) {   // closest: the group remembers its PARENT (re-test on pop)
+        if (ik) stack[sp++] = make_uint2(node, ik);
+      } else {
+        if (ik) stack[sp++] = make_uint2(w1.x, imask | ik << 8);
+      }
       node = w1.x + __popc(imask & ((1u << s) - 1u));
       continue;
     }
-    if (sp == 0) return;
-    const uint2 e = stack[sp - 1];
-    uint32_t keys = e.y >> 8;
-    const uint32_t im = e.y & 0xFFu;
-    const int s = (__ffs(keys) - 1) ^ (OCT >= 0 ? OCT : oct);
-    keys &= keys - 1;
-    if (keys) stack[sp - 1].y = im | keys << 8;
-    else --sp;
-    node = e.x + __popc(im & ((1u << s) - 1u));
+    if constexpr (Q == kClosest) {
+      // closest-hit: a pending child is re-tested against the CURRENT best_t before its node
+      // is fetched (one box hook on its decoded box, counted); culled ones are skipped
+      for (;;) {
+        if (sp == 0) return;
+        const uint2 e = stack[sp - 1];
+        uint32_t keys = e.y;
+        const int s = (__ffs(keys) - 1) ^ (OCT >= 0 ? OCT : oct);
+        keys &= keys - 1;
+        if (keys) stack[sp - 1].y = keys;
+        else --sp;
+        VSR_CHECK(e.x < p.num_wide);
+        const float4* pp = reinterpret_cast<const float4*>(W + e.x);
+        const float4 ph = __ldg(pp);
+        const uint4 pw1 = __ldg(reinterpret_cast<const uint4*>(pp + 1));
+        const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(pp + 2));
+        const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(pp + 3));
+        const uint4 q2 = __ldg(reinterpret_cast<const uint4*>(pp + 4));
+        const uint32_t hw = __float_as_uint(ph.w), pim = hw >> 24;
+        const uint32_t lo_w[3] = {s < 4 ? q0.x : q0.y, s < 4 ? q0.z : q0.w, s < 4 ? q1.x : q1.y};
+        const uint32_t hi_w[3] = {s < 4 ? q1.z : q1.w, s < 4 ? q2.x : q2.y, s < 4 ? q2.z : q2.w};
+        const float pm[3] = {ph.x, ph.y, ph.z};
+        float lo[3], hi[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const float sc = oct_scale(hw, a);
+          lo[a] = __fmaf_rn(qbyte(lo_w[a], s & 3), sc, pm[a]);
+          hi[a] = __fmaf_rn(qbyte(hi_w[a], s & 3), sc, pm[a]);
+        }
+        float tn;
+        if (!box_hook(isect, T.r, Aabb{lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]}, T.best_t, tn))
+          continue;
+        node = pw1.x + __popc(pim & ((1u << s) - 1u));
+        break;
+      }
+    } else {
+      if (sp == 0) return;
+      const uint2 e = stack[sp - 1];
+      uint32_t keys = e.y >> 8;
+      const uint32_t im = e.y & 0xFFu;
+      const int s = (__ffs(keys) - 1) ^ (OCT >= 0 ? OCT : oct);
+      keys &= keys - 1;
+      if (keys) stack[sp - 1].y = im | keys << 8;
+      else --sp;
+      node = e.x + __popc(im & ((1u << s) - 1u));
+    }
   }
 }
 
