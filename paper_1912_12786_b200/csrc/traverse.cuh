@@ -412,10 +412,105 @@ __device__ __forceinline__ bool descend_oct(const DevScene& S, Trav& T, I& isect
   }
 }
 
+// ---- speculative while-while (Aila & Laine, HPG 2009, "postponed leaves") ----
+// The paper's while-while lets a lane that reaches a leaf sit
+// idle until every lane of its warp has left the inner-node loop.  Here a lane
+// that reaches its first leaf POSTPONES it (keeps the ref in `lf`) and keeps
+// descending from its next stack entry; the warp leaves the inner loop once no
+// converged lane is still without a postponed leaf, then every lane runs its
+// postponed leaf — and the leaf it stands on, if any — in one pass.  Each
+// lane's own sequence is still a complete traversal with conservative culls
+// (only the ORDER of leaves and inner nodes changes; a closest-hit lane may
+// visit nodes with a best_t that a postponed leaf will shrink), so the closest
+// t and hit / miss are those of the plain loop; the prim on an exact t tie
+// and the hit an any-hit query returns may differ (both are valid answers).
+// Counting intersectors keep the plain loop: their counts define walker C's
+// visit order (reading A29 / SURVEY §8(c).6).
+#ifndef VSR_SPEC
+#define VSR_SPEC 0
+#endif
+constexpr uint32_t kNoRef = 0xFFFFFFFFu;   // never a valid ref (leaf range past kMaxTris)
+
+template <int OCT, class I, class SE>
+__device__ __forceinline__ void descend_spec(const DevScene& S, Trav& T, I& isect, SE* stack,
+                                             uint32_t& lf) {
+  while (!(T.cur & kLeafBit)) {
+    VSR_CHECK(T.cur < S.num_nodes);
+    const float4* np = reinterpret_cast<const float4*>(S.nodes + T.cur);
+    float4 nx, ny, nz, nr;
+    ldg8(np, nx, ny);
+    ldg8(np + 2, nz, nr);
+    BoxPairHit h;
+    if constexpr (OCT >= 0) h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t, octant<OCT>{});
+    else h = box_pair_hook(isect, T.r, AabbPair{nx, ny, nz}, T.best_t);
+    const uint32_t r0 = __float_as_uint(nr.x), r1 = __float_as_uint(nr.y);
+    if (h.h0 && h.h1) {
+      const bool swap = h.tn1 < h.tn0;   // nearer child first, ties -> child 0 (reading A13)
+      push(T, stack, swap ? r0 : r1, swap ? h.tn0 : h.tn1);
+      T.cur = swap ? r1 : r0;
+    } else if (h.h0) {
+      T.cur = r0;
+    } else if (h.h1) {
+      T.cur = r1;
+    } else if (!pop(T, stack)) {
+      T.cur = kNoRef;
+    }
+    if ((T.cur & kLeafBit) && T.cur != kNoRef && lf == kNoRef) {   // first leaf: postpone it
+      lf = T.cur;
+      if (!pop(T, stack)) T.cur = kNoRef;
+    }
+    if (!__any_sync(__activemask(), lf == kNoRef)) break;   // every lane holds a leaf
+  }
+}
+
+template <class I, class SE>
+__device__ __forceinline__ void descend_spec_oct(const DevScene& S, Trav& T, I& isect, SE* stack,
+                                                 int oct, uint32_t& lf) {
+  switch (oct) {
+    case 0: descend_spec<0>(S, T, isect, stack, lf); break;
+    case 1: descend_spec<1>(S, T, isect, stack, lf); break;
+    case 2: descend_spec<2>(S, T, isect, stack, lf); break;
+    case 3: descend_spec<3>(S, T, isect, stack, lf); break;
+    case 4: descend_spec<4>(S, T, isect, stack, lf); break;
+    case 5: descend_spec<5>(S, T, isect, stack, lf); break;
+    case 6: descend_spec<6>(S, T, isect, stack, lf); break;
+    case 7: descend_spec<7>(S, T, isect, stack, lf); break;
+    default: descend_spec<-1>(S, T, isect, stack, lf); break;
+  }
+}
+
+template <int Q, class I, class SE>
+__device__ __forceinline__ void traverse_spec(const DevScene& S, Trav& T, I& isect, SE* stack,
+                                              int oct) {
+  NoMulti none;
+  uint32_t lf = kNoRef;
+  if (T.cur & kLeafBit) {   // the root is a leaf
+    lf = T.cur;
+    T.cur = kNoRef;
+  }
+  for (;;) {
+    if (T.cur != kNoRef) descend_spec_oct(S, T, isect, stack, oct, lf);
+    while (lf != kNoRef) {   // the postponed leaf, then the one this lane stands on
+      const uint32_t at = T.cur;
+      T.cur = lf;
+      if (leaf<Q>(S, T, isect, none)) return;   // any-hit accepted a primitive
+      T.cur = at;
+      lf = kNoRef;
+      if ((at & kLeafBit) && at != kNoRef) {
+        lf = at;
+        if (!pop(T, stack)) T.cur = kNoRef;
+      }
+    }
+    if (T.cur == kNoRef) return;
+  }
+}
+
 template <int Q, class I, class SE, class M = NoMulti>
 __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, SE* stack,
                                          int oct, M& mb) {
-  if constexpr (std::is_same<SE, uint32_t>::value && VSR_ANY_SENTINEL) {
+  if constexpr (VSR_SPEC && Q != kMulti && !I::kCounts && std::is_same<M, NoMulti>::value) {
+    traverse_spec<Q>(S, T, isect, stack, oct);
+  } else if constexpr (std::is_same<SE, uint32_t>::value && VSR_ANY_SENTINEL) {
     stack[T.sp++] = kSentinel;   // the stack's floor (see descend_any)
     for (;;) {
       descend_any_oct(S, T, isect, stack, oct);
