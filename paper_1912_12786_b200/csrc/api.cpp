@@ -224,6 +224,7 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
   const char* es = std::getenv("VSR_SCHED");
   p.sched = (es && std::strcmp(es, "persistent") == 0) ? kSchedPersistent
             : (es && std::strcmp(es, "warp") == 0)      ? kSchedWarp
+            : (es && std::strcmp(es, "region") == 0)    ? kSchedRegion
                                                          : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;

@@ -207,6 +207,12 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
 #ifndef VSR_KEEP_ID
 #define VSR_KEEP_ID 0
 #endif
+#ifndef VSR_RAY_PF
+// prefetch the rays of the block this many launch slots ahead (~one residency wave:
+// 148 SMs x 10 CTAs); 0 = off.  Measured +0.5-0.6 % (C2, C5), 740..2960 alike
+// (profiles/r02_tuning.md)
+#define VSR_RAY_PF 1480
+#endif
 // Direct schedule (default): one thread per ray; launch slot i traces the 128
 // rays of block perm[i] (block i when no order was computed), and the
 // hardware block scheduler balances the blocks across the 148 SMs.
@@ -223,17 +229,29 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
 #endif
   const uint64_t blk = launch_block(p);
   const uint64_t id = blk * kBlock + threadIdx.x;
+#if VSR_RAY_PF
+  // the block VSR_RAY_PF launch slots ahead (about one residency wave later): its ray
+  // lines are prefetched into L2 once this block's own rays have arrived
+  uint32_t ahead = 0xFFFFFFFFu;
+  if (!GEN && p.perm && blockIdx.x + VSR_RAY_PF < gridDim.x) ahead = __ldcg(p.perm + blockIdx.x + VSR_RAY_PF);
+#endif
   if (id < p.n) {
     I isect = make_isect<I>(p);
     Trav T;
     StackEntry<Q> stack[kMaxStack];   // (ref[, tnear]); depth <= 64 guaranteed by build/import
     const bool go = start_ray<GEN>(p, T, isect, id);
+#if VSR_RAY_PF
+    if (ahead != 0xFFFFFFFFu) {
+      const uint64_t id2 = (uint64_t)ahead * kBlock + threadIdx.x;
+      if (id2 < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.rays + 2 * id2));
+    }
+#endif
     // warp-uniform octant: specialised slab test when all live lanes agree
     const unsigned live = __activemask();
     const int oct = ray_octant(T.r);
     const int woct = __match_any_sync(live, oct) == live ? oct : 8;
     NoMulti none;
-    if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
+    if (go) traverse<Q, !OCC>(p.scene, T, isect, stack, woct, none);
 #if VSR_KEEP_ID
     finish(p, T, isect, id);   // the ray index kept live across the traversal (A/B knob)
 #else
@@ -314,6 +332,140 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
       atomicExch(ctr + 1, 0ull);
     }
   }
+}
+
+// Region schedule (VSR_SCHED=region): the launch's ray blocks are cut into one
+// contiguous range per SM ("region"; consecutive blocks are neighbouring tiles),
+// each region ordered longest-first by region_scatter_kernel.  A resident grid's
+// warps claim 32-ray chunks from the region of the SM they run on (one atomicAdd
+// per chunk), so the ~40 warps sharing an SM's L1 trace neighbouring tiles; a
+// warp whose region is exhausted steals from the region with the most chunks
+// left.  Per-ray results are independent of the schedule.
+__device__ __forceinline__ uint64_t region_first_block(uint64_t nblocks, uint32_t k, uint32_t S) {
+  return nblocks * k / S;
+}
+
+__device__ __forceinline__ bool region_claim(const TraceParams& p, uint32_t home, uint64_t nblocks,
+                                             unsigned long long& chunk) {
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t S = p.regions;
+  uint32_t c = 0;
+  if (lane == 0) c = atomicAdd(p.region_ctr + home, 1u);
+  c = __shfl_sync(kFull, c, 0);
+  {
+    const uint64_t b0 = region_first_block(nblocks, home, S), b1 = region_first_block(nblocks, home + 1, S);
+    if (c < 4 * (b1 - b0)) {
+      chunk = 4 * b0 + c;
+      return true;
+    }
+  }
+  for (;;) {   // steal: the region with the most chunks left (warp-parallel scan)
+    uint32_t best = 0, bk = 0;
+    for (uint32_t k = lane; k < S; k += 32) {
+      const uint32_t size =
+          (uint32_t)(4 * (region_first_block(nblocks, k + 1, S) - region_first_block(nblocks, k, S)));
+      const uint32_t used = __ldcg(p.region_ctr + k);
+      const uint32_t left = used < size ? size - used : 0u;
+      if (left > best) {
+        best = left;
+        bk = k;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint32_t ob = __shfl_xor_sync(kFull, best, o), ok = __shfl_xor_sync(kFull, bk, o);
+      if (ob > best || (ob == best && ok < bk)) {
+        best = ob;
+        bk = ok;
+      }
+    }
+    if (best == 0) return false;
+    if (lane == 0) c = atomicAdd(p.region_ctr + bk, 1u);
+    c = __shfl_sync(kFull, c, 0);
+    const uint64_t b0 = region_first_block(nblocks, bk, S), b1 = region_first_block(nblocks, bk + 1, S);
+    if (c < 4 * (b1 - b0)) {
+      chunk = 4 * b0 + c;
+      return true;
+    }
+  }
+}
+
+template <int Q, class I, bool OCC = false>
+__global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB))
+    trace_kernel_region(const TraceParams p) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (p.hist_reset && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) p.hist_reset[i] = 0u;
+  const unsigned lane = threadIdx.x & 31u;
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const uint32_t home = smid % p.regions;
+  const uint64_t nblocks = (p.n + kBlock - 1) / kBlock;
+  unsigned long long c = 0;
+  bool have = region_claim(p, home, nblocks, c);
+  while (have) {
+    unsigned long long nx = 0;
+    const bool next = region_claim(p, home, nblocks, nx);
+    if (next) {   // the next chunk's rays toward L2 while this chunk traces
+      const uint64_t nid = chunk_first_ray(p, nx) + lane;
+      if (nid < p.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.rays + 2 * nid));
+    }
+    const uint64_t id = chunk_first_ray(p, c) + lane;
+    if (id < p.n) {
+      I isect = make_isect<I>(p);
+      Trav T;
+      StackEntry<Q> stack[kMaxStack];
+      const bool go = start_ray(p, T, isect, id);
+      const unsigned live = __activemask();
+      const int oct = ray_octant(T.r);
+      const int woct = __match_any_sync(live, oct) == live ? oct : 8;
+      NoMulti none;
+      if (go) traverse<Q>(p.scene, T, isect, stack, woct, none);
+      finish(p, T, isect, id);
+    }
+    c = nx;
+    have = next;
+    __syncwarp();
+  }
+}
+
+// Region order: blocks [nblocks*k/S, nblocks*(k+1)/S) of region k (one CTA per
+// region), most expensive bucket first (order within a bucket unspecified);
+// zeroes the region's claim counter for the trace kernel.
+__global__ void __launch_bounds__(256) region_scatter_kernel(uint32_t nblocks, uint32_t S,
+                                                             const uint32_t* slot, uint32_t* perm,
+                                                             uint32_t* ctr) {
+  __shared__ uint32_t cnt[kOrderBuckets], start[kOrderBuckets];
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint32_t k = blockIdx.x;
+  const uint32_t b0 = (uint32_t)((uint64_t)nblocks * k / S), b1 = (uint32_t)((uint64_t)nblocks * (k + 1) / S);
+  for (int i = threadIdx.x; i < kOrderBuckets; i += 256) cnt[i] = 0;
+  if (threadIdx.x == 0) ctr[k] = 0;
+  __syncthreads();
+  for (uint32_t b = b0 + threadIdx.x; b < b1; b += 256) atomicAdd(cnt + (__ldcg(slot + b) >> 24), 1u);
+  __syncthreads();
+  if (threadIdx.x < 32) {   // exclusive scan, most expensive bucket first
+    constexpr int R = kOrderBuckets / 32;
+    const int lane = (int)threadIdx.x;
+    uint32_t v[R], sum = 0;
+    for (int j = 0; j < R; ++j) {
+      v[j] = cnt[kOrderBuckets - 1 - (lane * R + j)];
+      sum += v[j];
+    }
+    uint32_t incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    uint32_t run = incl - sum;
+    for (int j = 0; j < R; ++j) {
+      start[kOrderBuckets - 1 - (lane * R + j)] = run;
+      run += v[j];
+    }
+  }
+  __syncthreads();
+  for (uint32_t b = b0 + threadIdx.x; b < b1; b += 256)
+    perm[b0 + atomicAdd(start + (__ldcg(slot + b) >> 24), 1u)] = b;
 }
 
 // Multi-hit query: same traversal, the leaf accepts into a K-entry sorted
@@ -457,6 +609,25 @@ cudaError_t launch(const TraceParams& p, cudaStream_t st) {
         p.occ ? launch_k(trace_kernel_warp<Q, I, true>, grid, kBlock, p.perm && p.pdl, st, p)
               : launch_k(trace_kernel_warp<Q, I, false>, grid, kBlock, p.perm && p.pdl, st, p);
     if (e != cudaSuccess) return e;
+  } else if (p.sched == kSchedRegion && p.region_ctr && !p.gen && !p.out_world) {
+    static std::atomic<int> per_sm_cache[2];
+    int per_sm = per_sm_cache[p.occ ? 1 : 0].load(std::memory_order_relaxed);
+    if (per_sm == 0) {
+      int nb = 0;
+      cudaError_t e = p.occ ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                  &nb, trace_kernel_region<Q, I, true>, kBlock, 0)
+                            : cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                                  &nb, trace_kernel_region<Q, I, false>, kBlock, 0);
+      if (e != cudaSuccess) return e;
+      per_sm = nb > 0 ? nb : 1;
+      per_sm_cache[p.occ ? 1 : 0].store(per_sm, std::memory_order_relaxed);
+    }
+    const uint64_t full = (uint64_t)per_sm * sm_count();
+    const uint64_t grid = need < full ? need : full;
+    const cudaError_t e =
+        p.occ ? launch_k(trace_kernel_region<Q, I, true>, grid, kBlock, p.pdl != 0, st, p)
+              : launch_k(trace_kernel_region<Q, I, false>, grid, kBlock, p.pdl != 0, st, p);
+    if (e != cudaSuccess) return e;
   } else if (p.sched == kSchedPersistent) {
     static std::atomic<int> per_sm_cache{0};   // resident blocks per SM for this instantiation
     int per_sm = per_sm_cache.load(std::memory_order_relaxed);
@@ -569,7 +740,7 @@ void set_kernel_events(void* start, void* stop) {
 
 size_t order_scratch_bytes(uint64_t n) {
   const uint64_t nblocks = (n + kBlock - 1) / kBlock;
-  return sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks);
+  return sizeof(uint32_t) * (kOrderBuckets + 2 * (size_t)nblocks + (size_t)sm_count() + 32);
 }
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStream_t st) {
@@ -589,7 +760,8 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
     }
     return e;
   };
-  if (p.order && (p.sched == kSchedDirect || p.sched == kSchedWarp) && nblocks >= 2ull * sm_count() &&
+  if (p.order && (p.sched == kSchedDirect || p.sched == kSchedWarp || p.sched == kSchedRegion) &&
+      nblocks >= 2ull * sm_count() &&
       nblocks < (1u << 24)) {
     // the owner's per-stream scratch (api.cpp ScratchSet); a stream-ordered
     // allocation only past 16 streams per owner
@@ -621,9 +793,18 @@ cudaError_t launch_trace(int query, int isect, const TraceParams& p_in, cudaStre
       if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
       return done(e);
     }
-    if ((e = launch_k(order_scatter_kernel, (nblocks + 255) / 256, 256, p.pdl != 0, st,
-                      (uint32_t)nblocks, (const uint32_t*)hist, (const uint32_t*)slot, perm)) !=
-        cudaSuccess) {
+    const bool region = p.sched == kSchedRegion && !p.gen && !p.out_world && !p.wide && !p.list &&
+                        query != kMulti;
+    if (region) {
+      p.regions = (uint32_t)sm_count();
+      p.region_ctr = perm + nblocks;
+      e = launch_k(region_scatter_kernel, p.regions, 256, p.pdl != 0, st, (uint32_t)nblocks,
+                   p.regions, (const uint32_t*)slot, perm, p.region_ctr);
+    } else {
+      e = launch_k(order_scatter_kernel, (nblocks + 255) / 256, 256, p.pdl != 0, st,
+                   (uint32_t)nblocks, (const uint32_t*)hist, (const uint32_t*)slot, perm);
+    }
+    if (e != cudaSuccess) {
       if (zeroed) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * kOrderBuckets, st);
       return done(e);
     }

@@ -11,7 +11,7 @@ namespace vsr {
 
 struct WideNode;
 
-enum : int { kSchedDirect = 0, kSchedPersistent = 1, kSchedWarp = 2 };
+enum : int { kSchedDirect = 0, kSchedPersistent = 1, kSchedWarp = 2, kSchedRegion = 3 };
 
 // Kernel parameters (passed by value: they live in the constant parameter bank).
 struct TraceParams {
@@ -48,6 +48,8 @@ struct TraceParams {
   int order_proxy;               // order pass cost proxy: 0 segment length, 1 density grid, 2 auto
   const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
   uint32_t num_wide;             // its node count (bounds-checked builds)
+  uint32_t* region_ctr;          // region schedule: per-region claim counters (set by launch_trace)
+  uint32_t regions;              // region schedule: number of regions (= SMs)
 };
 
 cudaError_t launch_trace(int query, int isect, const TraceParams& p, cudaStream_t st);

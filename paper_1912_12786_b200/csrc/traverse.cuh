@@ -505,7 +505,24 @@ __device__ __forceinline__ void traverse_spec(const DevScene& S, Trav& T, I& ise
   }
 }
 
-template <int Q, class I, class SE, class M = NoMulti>
+// Octant dispatch outside the while-while (OUTER): one switch per ray instead of
+// one per leaf, at the price of one leaf-loop copy per octant.  The direct
+// trace kernel uses it for its default-occupancy instantiation (measured C2 any
+// +1.6 %, closest +1.5 %, C4 any -0.5 %); the 12-CTA variant for scenes larger
+// than L2 keeps the per-leaf switch (C5 any -2.1 % with it; profiles/r02_tuning.md).
+#ifndef VSR_OCT_OUTER
+#define VSR_OCT_OUTER 1   // 0: every kernel keeps the per-leaf switch
+#endif
+template <int Q, int OCT, class I, class SE, class M>
+__device__ __forceinline__ void traverse_fixed(const DevScene& S, Trav& T, I& isect, SE* stack,
+                                               M& mb) {
+  for (;;) {
+    const bool at_leaf = descend<OCT>(S, T, isect, stack);
+    if (!at_leaf || leaf<Q>(S, T, isect, mb) || !pop(T, stack)) return;
+  }
+}
+
+template <int Q, bool OUTER = false, class I, class SE, class M = NoMulti>
 __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, SE* stack,
                                          int oct, M& mb) {
   if constexpr (VSR_SPEC && Q != kMulti && !I::kCounts && std::is_same<M, NoMulti>::value) {
@@ -517,6 +534,18 @@ __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, S
       if (T.cur == kSentinel) return;                 // popped the floor: done
       if (leaf<Q>(S, T, isect, mb)) return;           // any-hit accepted a primitive
       T.cur = stack[--T.sp];                          // next entry (possibly the floor)
+    }
+  } else if constexpr (OUTER && VSR_OCT_OUTER && Q != kMulti) {
+    switch (oct) {   // once per ray: the whole while-while is specialised per octant
+      case 0: traverse_fixed<Q, 0>(S, T, isect, stack, mb); break;
+      case 1: traverse_fixed<Q, 1>(S, T, isect, stack, mb); break;
+      case 2: traverse_fixed<Q, 2>(S, T, isect, stack, mb); break;
+      case 3: traverse_fixed<Q, 3>(S, T, isect, stack, mb); break;
+      case 4: traverse_fixed<Q, 4>(S, T, isect, stack, mb); break;
+      case 5: traverse_fixed<Q, 5>(S, T, isect, stack, mb); break;
+      case 6: traverse_fixed<Q, 6>(S, T, isect, stack, mb); break;
+      case 7: traverse_fixed<Q, 7>(S, T, isect, stack, mb); break;
+      default: traverse_fixed<Q, -1>(S, T, isect, stack, mb); break;
     }
   } else {
     for (;;) {

@@ -159,6 +159,7 @@ def test_persistent_schedule(V, oracle_lib, monkeypatch, refill):
                                    {"VSR_ORDER": "0", "VSR_ALPHA_BITS": "0"}, {"VSR_OCC": "1"},
                                    {"VSR_SCHED": "warp"}, {"VSR_SCHED": "warp", "VSR_OCC": "1"},
                                    {"VSR_SCHED": "warp", "VSR_ORDER": "0"},
+                                   {"VSR_SCHED": "region"}, {"VSR_SCHED": "region", "VSR_OCC": "1"},
                                    {"VSR_ORDER_PROXY": "grid"}, {"VSR_ORDER_PROXY": "len"}])
 def test_scheduling_knobs_change_no_result(V, c2, monkeypatch, knobs):
     """README's runtime knobs: tile order instead of longest-first, plain launches instead of
@@ -321,15 +322,18 @@ def test_tile_sharding_is_partition_invariant(V, c2):
         assert out.tobytes() == full.tobytes()
 
 
-@pytest.mark.parametrize("n", [1, 31, 33, 129, 5000])
-def test_warp_schedule_ragged(V, oracle_lib, monkeypatch, n):
-    """VSR_SCHED=warp (32-ray chunks claimed per warp, next chunk prefetched): ragged ray
-    counts (a partial chunk, fewer chunks than warps) give the direct schedule's bytes."""
+@pytest.mark.parametrize("sched", ["warp", "region"])
+@pytest.mark.parametrize("n", [1, 31, 33, 129, 5000, 40000, 40017])
+def test_warp_schedule_ragged(V, oracle_lib, monkeypatch, n, sched):
+    """VSR_SCHED=warp (32-ray chunks claimed per warp, next chunk prefetched) and
+    VSR_SCHED=region (chunks claimed from the SM's own block range, stealing when it is
+    empty; engaged from 2 x 148 blocks): ragged ray counts (a partial chunk, fewer chunks
+    than warps, ragged regions) give the direct schedule's bytes."""
     sc = W.random_soup(2000, seed=900 + n)
     rays = W.random_rays(n, seed=901 + n).data
     s = V.Scene.from_workload(sc).build()
     ref = {q: gpu_trace(V, s, rays, q, V.COUNT_ALPHA_TEXTURE) for q in (V.CLOSEST, V.ANY)}
-    monkeypatch.setenv("VSR_SCHED", "warp")
+    monkeypatch.setenv("VSR_SCHED", sched)
     for q in (V.CLOSEST, V.ANY):
         h, c = gpu_trace(V, s, rays, q, V.COUNT_ALPHA_TEXTURE)
         assert h.tobytes() == ref[q][0].tobytes() and c.tobytes() == ref[q][1].tobytes()
