@@ -629,10 +629,16 @@ struct alpha_texture_intersector : basic_intersector<alpha_texture_intersector> 
 // ALPHA_TEXTURE through the 1-bit plane (alpha_keep_bits): chosen by the host
 // for VSR_ISECT_ALPHA_TEXTURE when the scene's plane for the call's threshold
 // exists; otherwise alpha_texture_intersector reads the A8 plane.
+#ifndef VSR_SIDE_PF
+#define VSR_SIDE_PF 0   // 1: prefetch the triangle's alpha sidecar into L1 before the MT test
+#endif
 struct alpha_bits_intersector : alpha_texture_intersector {
   using alpha_texture_intersector::operator();
   __device__ __forceinline__ hit_record operator()(const RayCtx& r, const TriData& t, uint32_t k,
                                                    float tmax_cur) {
+#if VSR_SIDE_PF
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(d.sides + k));
+#endif
     hit_record hr = intersect(r, t, k, tmax_cur);
     if (hr.hit) {
       ++n_lookups;

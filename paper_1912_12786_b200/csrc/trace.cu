@@ -283,8 +283,9 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
 // warp takes a new chunk only when all 32 lanes are done.  Per-ray results are
 // independent of the schedule.
 __device__ __forceinline__ uint64_t chunk_first_ray(const TraceParams& p, unsigned long long c) {
-  const uint64_t blk = p.perm ? (uint64_t)__ldcg(p.perm + (c >> 2)) : (uint64_t)(c >> 2);
-  return blk * kBlock + (c & 3ull) * 32ull;
+  constexpr unsigned long long kQ = kBlock / 32;   // 32-ray chunks per block
+  const uint64_t blk = p.perm ? (uint64_t)__ldcg(p.perm + c / kQ) : (uint64_t)(c / kQ);
+  return blk * kBlock + (c % kQ) * 32ull;
 }
 
 template <int Q, class I, bool OCC = false>
@@ -294,7 +295,9 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
   if (p.hist_reset && blockIdx.x == 0)
     for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) p.hist_reset[i] = 0u;
   const unsigned lane = threadIdx.x & 31u;
-  const unsigned long long nchunks = (p.n + 31ull) / 32ull;
+  // every 32-ray quarter of every block (a ragged last block may sit anywhere in the
+  // longest-first order, so the chunk count is 4 x blocks, not ceil(n / 32))
+  const unsigned long long nchunks = (unsigned long long)(kBlock / 32) * ((p.n + kBlock - 1) / kBlock);
   unsigned long long* ctr = p.counter;
   unsigned long long c = 0;
   if (lane == 0) c = atomicAdd(ctr, 1ull);
@@ -347,6 +350,7 @@ __device__ __forceinline__ uint64_t region_first_block(uint64_t nblocks, uint32_
 
 __device__ __forceinline__ bool region_claim(const TraceParams& p, uint32_t home, uint64_t nblocks,
                                              unsigned long long& chunk) {
+  constexpr uint64_t kQ = kBlock / 32;   // 32-ray chunks per block
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t S = p.regions;
   uint32_t c = 0;
@@ -354,8 +358,8 @@ __device__ __forceinline__ bool region_claim(const TraceParams& p, uint32_t home
   c = __shfl_sync(kFull, c, 0);
   {
     const uint64_t b0 = region_first_block(nblocks, home, S), b1 = region_first_block(nblocks, home + 1, S);
-    if (c < 4 * (b1 - b0)) {
-      chunk = 4 * b0 + c;
+    if (c < kQ * (b1 - b0)) {
+      chunk = kQ * b0 + c;
       return true;
     }
   }
@@ -363,7 +367,7 @@ __device__ __forceinline__ bool region_claim(const TraceParams& p, uint32_t home
     uint32_t best = 0, bk = 0;
     for (uint32_t k = lane; k < S; k += 32) {
       const uint32_t size =
-          (uint32_t)(4 * (region_first_block(nblocks, k + 1, S) - region_first_block(nblocks, k, S)));
+          (uint32_t)(kQ * (region_first_block(nblocks, k + 1, S) - region_first_block(nblocks, k, S)));
       const uint32_t used = __ldcg(p.region_ctr + k);
       const uint32_t left = used < size ? size - used : 0u;
       if (left > best) {
@@ -382,8 +386,8 @@ __device__ __forceinline__ bool region_claim(const TraceParams& p, uint32_t home
     if (lane == 0) c = atomicAdd(p.region_ctr + bk, 1u);
     c = __shfl_sync(kFull, c, 0);
     const uint64_t b0 = region_first_block(nblocks, bk, S), b1 = region_first_block(nblocks, bk + 1, S);
-    if (c < 4 * (b1 - b0)) {
-      chunk = 4 * b0 + c;
+    if (c < kQ * (b1 - b0)) {
+      chunk = kQ * b0 + c;
       return true;
     }
   }
@@ -470,6 +474,9 @@ __global__ void __launch_bounds__(256) region_scatter_kernel(uint32_t nblocks, u
 
 // Multi-hit query: same traversal, the leaf accepts into a K-entry sorted
 // buffer (runtime max_hits <= K).  Output ray-major: hits[id*max_hits + j].
+#ifndef VSR_MULTI_OUTER
+#define VSR_MULTI_OUTER 1   // octant dispatch once per ray, as the direct kernel (k = 4 C2 +0.6 %)
+#endif
 template <class I, int K>
 __global__ void __launch_bounds__(kBlock, VSR_MULTI_MINB) trace_multi_kernel(const TraceParams p) {
   const uint64_t blk = launch_block(p);
@@ -485,7 +492,7 @@ __global__ void __launch_bounds__(kBlock, VSR_MULTI_MINB) trace_multi_kernel(con
   const unsigned live = __activemask();
   const int oct = ray_octant(T.r);
   const int woct = __match_any_sync(live, oct) == live ? oct : 8;
-  if (go) traverse<kMulti>(p.scene, T, isect, stack, woct, mb);
+  if (go) traverse<kMulti, VSR_MULTI_OUTER != 0>(p.scene, T, isect, stack, woct, mb);
   float4* out = p.hits + id * (uint64_t)p.max_hits;
 #pragma unroll
   for (int j = 0; j < K; ++j) {   // static indices: the buffer stays in registers

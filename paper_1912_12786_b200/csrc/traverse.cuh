@@ -535,7 +535,7 @@ __device__ __forceinline__ void traverse(const DevScene& S, Trav& T, I& isect, S
       if (leaf<Q>(S, T, isect, mb)) return;           // any-hit accepted a primitive
       T.cur = stack[--T.sp];                          // next entry (possibly the floor)
     }
-  } else if constexpr (OUTER && VSR_OCT_OUTER && Q != kMulti) {
+  } else if constexpr (OUTER && VSR_OCT_OUTER) {
     switch (oct) {   // once per ray: the whole while-while is specialised per octant
       case 0: traverse_fixed<Q, 0>(S, T, isect, stack, mb); break;
       case 1: traverse_fixed<Q, 1>(S, T, isect, stack, mb); break;

@@ -335,5 +335,8 @@ def test_warp_schedule_ragged(V, oracle_lib, monkeypatch, n, sched):
     ref = {q: gpu_trace(V, s, rays, q, V.COUNT_ALPHA_TEXTURE) for q in (V.CLOSEST, V.ANY)}
     monkeypatch.setenv("VSR_SCHED", sched)
     for q in (V.CLOSEST, V.ANY):
-        h, c = gpu_trace(V, s, rays, q, V.COUNT_ALPHA_TEXTURE)
+        # poisoned outputs: a ray the schedule never traces cannot inherit a stale row
+        hits = torch.full((n, 4), float("nan"), device="cuda")
+        counts = torch.full((n, 4), -1, dtype=torch.int32, device="cuda")
+        h, c = gpu_trace(V, s, rays, q, V.COUNT_ALPHA_TEXTURE, hits=hits, counts=counts)
         assert h.tobytes() == ref[q][0].tobytes() and c.tobytes() == ref[q][1].tobytes()
