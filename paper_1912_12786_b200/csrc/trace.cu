@@ -207,6 +207,11 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
 #ifndef VSR_KEEP_ID
 #define VSR_KEEP_ID 0
 #endif
+#ifndef VSR_ID_SMEM
+// each thread's block id kept in shared memory (512 B per CTA) for the hit write, instead
+// of re-reading the launch slot's perm entry through L2 at the end (+0.2-0.5 %)
+#define VSR_ID_SMEM 1
+#endif
 #ifndef VSR_RAY_PF
 // prefetch the rays of the block this many launch slots ahead (~one residency wave:
 // 148 SMs x 10 CTAs); 0 = off.  Measured +0.5-0.6 % (C2, C5), 740..2960 alike
@@ -235,6 +240,10 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
   uint32_t ahead = 0xFFFFFFFFu;
   if (!GEN && p.perm && blockIdx.x + VSR_RAY_PF < gridDim.x) ahead = __ldcg(p.perm + blockIdx.x + VSR_RAY_PF);
 #endif
+#if VSR_ID_SMEM
+  __shared__ uint32_t s_blk[kBlock];   // this thread's block, for the hit write (no L2 re-read)
+  s_blk[threadIdx.x] = (uint32_t)blk;
+#endif
   if (id < p.n) {
     I isect = make_isect<I>(p);
     Trav T;
@@ -254,6 +263,8 @@ __global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB)
     if (go) traverse<Q, !OCC>(p.scene, T, isect, stack, woct, none);
 #if VSR_KEEP_ID
     finish(p, T, isect, id);   // the ray index kept live across the traversal (A/B knob)
+#elif VSR_ID_SMEM
+    finish(p, T, isect, (uint64_t)s_blk[threadIdx.x] * kBlock + threadIdx.x);
 #else
     // the ray index is recomputed (perm re-read through L2) rather than kept live
     // across the traversal: one register less in the hot loop
