@@ -56,6 +56,16 @@ __global__ void __launch_bounds__(kBlock, VSR_MINB) trace_list_kernel(const Trac
 // best_t; the bottom's stack entries sit above the top level's.
 // ---------------------------------------------------------------------------
 constexpr int kInstStack = 2 * kMaxStack;
+// The bottom traversal reads the instanced scene's DevScene through a private copy: through
+// a reference into p.list the compiler reloads S.nodes from global memory at every node
+// (a store to the local stack may alias a generic pointer), a dependent L1 round trip per
+// visit.  Measured instanced forest any +2.0 %, closest +2.7 % (profiles/r02_tuning.md).
+#ifndef VSR_INST_SCOPY
+#define VSR_INST_SCOPY 1
+#endif
+#ifndef VSR_INST_OUTER
+#define VSR_INST_OUTER 0   // 1: octant dispatch once per instance visit (measured -14 / -29 %)
+#endif
 
 __device__ __forceinline__ void to_object(const float4 r0, const float4 r1, const float4 r2,
                                           const RayCtx& w, float4& a, float4& b) {
@@ -78,7 +88,11 @@ __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& 
   const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
   const uint32_t b = __float_as_uint(ex.x);
   VSR_CHECK(b < p.list_count);
+#if VSR_INST_SCOPY
+  const DevScene S = p.list[b];   // a private copy: the bottom loop keeps its pointers in registers
+#else
   const DevScene& S = p.list[b];
+#endif
   bind_scene_data(isect, p.list_data[b]);
   Trav B = T;   // running best (t, u, v, prim, have, best_t) carried in and out
   float4 oa, ob;
@@ -90,7 +104,7 @@ __device__ __forceinline__ bool instance_leaf(const TraceParams& p, Trav& T, I& 
   float tn;
   if (!box_hook(isect, B.r, root, B.best_t, tn)) return false;
   NoMulti none;
-  traverse<Q>(S, B, isect, stack, warp_octant(B.r), none);
+  traverse<Q, VSR_INST_OUTER != 0>(S, B, isect, stack, warp_octant(B.r), none);
   const bool better = Q == kAny ? B.prim != kMissPrim
                                 : (B.prim != kMissPrim && (T.prim == kMissPrim || B.best_t < T.best_t));
   if (better) {
@@ -201,7 +215,11 @@ __device__ __forceinline__ void instance_leaf_multi(const TraceParams& p, Trav& 
   const float4 r0 = __ldg(ip), r1 = __ldg(ip + 1), r2 = __ldg(ip + 2), ex = __ldg(ip + 3);
   const uint32_t b = __float_as_uint(ex.x);
   VSR_CHECK(b < p.list_count);
+#if VSR_INST_SCOPY
+  const DevScene S = p.list[b];   // a private copy: the bottom loop keeps its pointers in registers
+#else
   const DevScene& S = p.list[b];
+#endif
   bind_scene_data(isect, p.list_data[b]);
   Trav B = T;
   float4 oa, ob;
