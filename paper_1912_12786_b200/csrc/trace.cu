@@ -90,7 +90,10 @@ __device__ uint32_t instance_cost(const TraceParams& p, const RayCtx& r, float t
 // box reaches down to the ground) cost far more than their segment length
 // says (tools/timeline.py: the launch's last warp started 20 us late with an
 // 83 us run).  Bucket = 6 log2(1 + integral).
-constexpr int kGridSamples = 16;
+#ifndef VSR_GRID_SAMPLES
+#define VSR_GRID_SAMPLES 16
+#endif
+constexpr int kGridSamples = VSR_GRID_SAMPLES;
 constexpr int kGridCopies = 32;   // replicas of the grid, one per CTA modulo: spreads the
                                   // order pass's burst of loads over 32x more L2 lines
 __device__ float grid_cost(const DevScene& S, const RayCtx& r, float tn, float tf) {
