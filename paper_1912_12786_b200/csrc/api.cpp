@@ -228,11 +228,13 @@ vsr_status make_params(vsr_scene* s, vsr_query query, vsr_isect isect,
                                                          : kSchedDirect;
   const char* eo = std::getenv("VSR_ORDER");   // "0" disables longest-first block order
   p.order = (eo && std::strcmp(eo, "0") == 0) ? 0 : 1;
-  // order pass cost proxy: "grid" (density-grid line integral), "len" (segment length in the
-  // root box); unset = auto: grid for instanced queries (measured +4-5 %), len otherwise
-  // (measured: grid costs the short C2 launch +2 %, C4 -25 %; profiles/r02_tuning.md)
+  // order pass cost proxy: "grid" (density-grid line integral, 16 samples), "len" (segment
+  // length in the root box), "mix" (mean of a 4-sample grid bucket and the length bucket);
+  // unset = auto: grid for instanced queries (measured +4-5 %), mix otherwise (C2 +1.2 %,
+  // C4 +0.8 %, C5 -0.2 % against len; pure grid: C4 -8 to -25 %; profiles/r02_tuning.md)
   const char* eg = std::getenv("VSR_ORDER_PROXY");
-  p.order_proxy = !eg ? 2 : (std::strcmp(eg, "grid") == 0 ? 1 : 0);
+  p.order_proxy = !eg ? 2
+                  : (std::strcmp(eg, "grid") == 0 ? 1 : std::strcmp(eg, "mix") == 0 ? 3 : 0);
   const char* ep = std::getenv("VSR_PDL");   // "0": plain launches after the order pass
   p.pdl = (ep && std::strcmp(ep, "0") == 0) ? 0 : 1;
   // 12-CTA occupancy variant for scenes that do not fit in L2 (VSR_OCC=0/1 forces it)

@@ -45,7 +45,8 @@ struct TraceParams {
   Pinhole cam;
   int runtime_kind;
   void* filter_fn;
-  int order_proxy;               // order pass cost proxy: 0 segment length, 1 density grid, 2 auto
+  int order_proxy;               // order pass cost proxy: 0 segment length, 1 density grid, 3 blend
+                                 // of the two, 2 auto (grid for instances, blend otherwise)
   const WideNode* wide;          // 8-wide compressed BVH (vsr_trace_bvh8) or nullptr
   uint32_t num_wide;             // its node count (bounds-checked builds)
   uint32_t* region_ctr;          // region schedule: per-region claim counters (set by launch_trace)

@@ -160,7 +160,8 @@ def test_persistent_schedule(V, oracle_lib, monkeypatch, refill):
                                    {"VSR_SCHED": "warp"}, {"VSR_SCHED": "warp", "VSR_OCC": "1"},
                                    {"VSR_SCHED": "warp", "VSR_ORDER": "0"},
                                    {"VSR_SCHED": "region"}, {"VSR_SCHED": "region", "VSR_OCC": "1"},
-                                   {"VSR_ORDER_PROXY": "grid"}, {"VSR_ORDER_PROXY": "len"}])
+                                   {"VSR_ORDER_PROXY": "grid"}, {"VSR_ORDER_PROXY": "len"},
+                                   {"VSR_ORDER_PROXY": "mix"}])
 def test_scheduling_knobs_change_no_result(V, c2, monkeypatch, knobs):
     """README's runtime knobs: tile order instead of longest-first, plain launches instead of
     the PDL chain, A8 instead of the 1-bit plane, the closest-hit occupancy variant — the same
