@@ -61,3 +61,23 @@ if __name__ == "__main__":
     data = sass_hot(rep)
     tot = sum(x[2] for x in data)
     print("total warp instructions (source page):", tot)
+    # stall reasons: the source page's per-instruction pc-sampling columns, summed
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr = rows[1]
+    cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
+    sums = {hdr[i][6:]: 0 for i in cols}
+    for r in rows[2:]:
+        if len(r) < len(hdr):
+            break
+        for i in cols:
+            try:
+                sums[hdr[i][6:]] += int(r[i] or 0)
+            except ValueError:
+                pass
+    allv = sum(sums.values())
+    if allv:
+        print("stall reasons (pc sampling, share of samples):")
+        for k, v in sorted(sums.items(), key=lambda kv: -kv[1])[:8]:
+            print(f"  {k:24s} {100.0 * v / allv:5.1f}%")
