@@ -247,8 +247,11 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(uint32_t nblocks, co
 // DRAM latency (closest: C4 +3 %, C5 +4 %; any: C5 +3 %). Otherwise 10 CTAs
 // (43-45 registers, no spills), which L2-resident scenes prefer (C2 any +0.6 %,
 // closest +1.5 %; profiles/r01_tuning.md).
+#ifndef VSR_ANY_MINB
+#define VSR_ANY_MINB 10
+#endif
 template <int Q, class I, bool GEN = false, bool OCC = false>
-__global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? 10 : VSR_MINB))
+__global__ void __launch_bounds__(kBlock, OCC ? 12 : (Q == kAny ? VSR_ANY_MINB : VSR_MINB))
     trace_kernel(const TraceParams p) {
 #ifdef VSR_TIMELINE
   const uint64_t t0 = global_ns();
