@@ -99,7 +99,13 @@ __device__ uint32_t instance_cost(const TraceParams& p, const RayCtx& r, float t
 // keep the order pass's grid requests (the cost of the 16-sample form: ~1 M
 // requests on a few thousand hot L2 lines) at a quarter.
 constexpr int kGridSamples = 16;   // pure density proxy (instanced queries)
-constexpr int kMixSamples = 4;     // blended proxy
+#ifndef VSR_MIX_SAMPLES
+#define VSR_MIX_SAMPLES 4
+#endif
+#ifndef VSR_MIX_W
+#define VSR_MIX_W 0.5f   // weight of the density bucket in the blend
+#endif
+constexpr int kMixSamples = VSR_MIX_SAMPLES;   // blended proxy
 constexpr int kGridCopies = 32;   // replicas of the grid, one per CTA modulo: spreads the
                                   // order pass's burst of loads over 32x more L2 lines
 template <int NS>
@@ -162,7 +168,8 @@ __global__ void __launch_bounds__(256) order_cost_kernel(const TraceParams p, ui
           const float dg = sqrtf(ex * ex + ey * ey + ez * ez);
           const float seg =
               dg > 0.0f ? (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z) / dg * kOrderBuckets : 0.0f;
-          len = 0.5f * (6.0f * log2f(1.0f + grid_cost<kMixSamples>(p.scene, r, tn, tf)) + seg);
+          len = VSR_MIX_W * (6.0f * log2f(1.0f + grid_cost<kMixSamples>(p.scene, r, tn, tf))) +
+                (1.0f - VSR_MIX_W) * seg;
         }
       } else if (tf > tn) len = (tf - tn) * sqrtf(d.x * d.x + d.y * d.y + d.z * d.z);
     }
